@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""Benchmark of the LUTHAM forward (BASELINE.json metric: "quantized KAN head
+samples/sec (bs1 latency, bs256 tput); achieved GB/s vs roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Workload (configs[1]): the compressed detection head {2048,1408,20},
+K=65536, G=10, int8 tables (12,957,696 B payload), synthetic seeded tables of
+that architecture and synthetic backbone features, batch 1 per GPU per step.
+A step is one forward of the head over one batch.  L2 is flushed (a 256 MiB
+write) before every timed step, so the head is read from HBM each step.
+Each rank runs its own replica on its own batch shard (no data-path
+collective): scaling "weak".  A second object "bs256" reports configs[2]
+(global batch 256 sharded over the ranks).
+
+--impl reference times the reference's own CPU compressed_forward (the
+UNMODIFIED holoquant sources compiled into oracle/_ref) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantized KAN head samples/sec (bs1 latency, bs256 tput); achieved GB/s vs roofline"
+DIMS = (2048, 1408, 20)
+K, G = 65536, 10
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=1, help="samples per GPU per step (configs[1]: 1)")
+    ap.add_argument("--mode", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for n, v in zip(names, r[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(n_gpus):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference(cn, batch_per_step: int, budget_s: float, threads: int):
+    """Time the reference compressed_forward (oracle/_ref) on `threads` host
+    threads over a bounded sample; returns (samples/s, sample description)."""
+    import oracle
+    m = oracle.ref_build(cn)
+    from paper_2512_15742_b200 import synthetic
+    # calibrate: one single-sample call on one thread
+    x1 = synthetic.synthetic_inputs(1, DIMS[0], seed=99)
+    t0 = time.perf_counter()
+    m.forward(x1, 1)
+    per_sample = time.perf_counter() - t0
+    n = max(threads, int(budget_s * threads / max(per_sample, 1e-6)))
+    n = min(n, 4096)
+    x = synthetic.synthetic_inputs(n, DIMS[0], seed=100)
+    t0 = time.perf_counter()
+    m.forward(x, n, threads=threads)
+    dt = time.perf_counter() - t0
+    return n / dt, f"{n} samples of the {DIMS} head, K={K}, int8, batch split over {threads} threads " \
+                   f"(one Workspace each, SPEC.md:536); single-thread calibration {per_sample * 1e3:.1f} ms/sample"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2512_15742_b200 import synthetic
+    import oracle
+    if not oracle.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libholoquant_ref.so was not built"}))
+        return
+    cn = synthetic.synthetic_head(dims=DIMS, k=K, grid=G, int8=True)
+    threads = os.cpu_count() or 1
+    m = oracle.ref_build(cn)
+    per_step_samples = threads  # a bounded sample: one sample per host thread per step
+    x = synthetic.synthetic_inputs(per_step_samples, DIMS[0], seed=100)
+    for _ in range(args.warmup):
+        m.forward(x, per_step_samples, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        m.forward(x, per_step_samples, threads=threads)
+        times.append(time.perf_counter() - t0)
+    dt = sum(times)
+    value = per_step_samples * args.steps / dt
+    sample = (f"each step: {per_step_samples} samples of the {DIMS} int8 head over {threads} host threads "
+              f"(reference holoquant::compressed_forward, one Workspace per thread)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2 compressed head {2048,1408,20} K=65536 G=10 int8, batch 1 per stream",
+                   "global_batch": per_step_samples},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_2512_15742_b200 as hq
+    from paper_2512_15742_b200 import _lib, synthetic
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    pk = peaks()
+    cn = synthetic.synthetic_head(dims=DIMS, k=K, grid=G, int8=True)
+    model = hq.build_model(cn, device=local)
+    plan = model.plan()
+    B = args.batch
+    B256 = max(1, 256 // world)
+    ws = hq.make_workspace(model, max_batch=max(B, B256))
+    stream = torch.cuda.Stream(device=dev)
+    s_ptr = stream.cuda_stream
+    L = _lib.lib()
+    mode = hq.MODE_EXACT if args.mode == "exact" else hq.MODE_FAST
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def timed_loop(batch, d_x, d_y, steps, warmup, what="forward"):
+        """Per-step CUDA-event times (ms) on `stream`, L2 flushed before each step."""
+        def one():
+            if what == "forward":
+                _lib.check(L.skan_forward_async(model.handle, ws.handle, d_x.data_ptr(), batch, d_y.data_ptr(),
+                                                mode, s_ptr))
+            else:
+                _lib.check(L.skan_profile_gather(model.handle, ws.handle, 0, batch, mode, s_ptr))
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                flush.zero_()
+                one()
+            stream.synchronize()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for a, b in ev:
+                flush.zero_()
+                a.record(stream)
+                one()
+                b.record(stream)
+            stream.synchronize()
+        ws.check()
+        return [a.elapsed_time(b) for a, b in ev]
+
+    def sync_max(v: float) -> float:
+        if pg is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---- device-resident headline: batch B per GPU per step --------------
+    x_np = synthetic.synthetic_inputs(B * world, DIMS[0], seed=12345)[rank * B * DIMS[0]:(rank + 1) * B * DIMS[0]]
+    d_x = torch.from_numpy(x_np.copy()).to(dev)
+    d_y = torch.zeros(B * DIMS[-1], dtype=torch.float64, device=dev)
+    barrier()
+    with ClockSampler(local) as clk:
+        times = timed_loop(B, d_x, d_y, args.steps, args.warmup)
+    barrier()
+    launches_per_step = ws.last_launches()
+    step_ms = sync_max(sum(times) / len(times))
+    value = B * world / (step_ms * 1e-3)
+
+    # ---- dominant kernel alone: layer-0 gather -----------------------------
+    k_times = timed_loop(B, d_x, d_y, args.steps, args.warmup, what="gather0")
+    k_ms = statistics.mean(k_times)
+    lp0 = plan.layers[0]
+    kernel_bytes = lp0.payload_bytes() + B * DIMS[0] * 8
+    achieved = kernel_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_gather0_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    call_bytes = plan.payload_total + B * (DIMS[0] + DIMS[-1]) * 8
+
+    # ---- configs[2]: batch 256 sharded over ranks -------------------------
+    x256 = synthetic.synthetic_inputs(256, DIMS[0], seed=777)
+    lo = rank * 256 // world
+    hi = (rank + 1) * 256 // world
+    d_x256 = torch.from_numpy(x256[lo * DIMS[0]:hi * DIMS[0]].copy()).to(dev)
+    d_y256 = torch.zeros((hi - lo) * DIMS[-1], dtype=torch.float64, device=dev)
+    barrier()
+    t256 = timed_loop(hi - lo, d_x256, d_y256, max(5, args.steps // 5), args.warmup)
+    barrier()
+    ms256 = sync_max(statistics.mean(t256))
+    edges = model.edge_count()
+
+    # ---- e2e through the public API with host buffers ---------------------
+    x_host = torch.from_numpy(x_np.copy()).pin_memory()
+    y_host = torch.zeros(B * DIMS[-1], dtype=torch.float64).pin_memory()
+    xh, yh = x_host.numpy(), y_host.numpy()
+    e2e_t = []
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            stream.synchronize()
+            t0 = time.perf_counter()
+            _lib.check(L.skan_forward(model.handle, ws.handle, xh.ctypes.data, xh.size, B, yh.ctypes.data, yh.size,
+                                      mode, _lib.SKAN_PTR_HOST, s_ptr))
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                e2e_t.append(t1 - t0)
+    e2e_s = sync_max(statistics.mean(e2e_t))
+    e2e_value = B * world / e2e_s
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        if oracle.have_ref():
+            threads = os.cpu_count() or 1
+            v, sample = cpu_reference(cn, B, args.cpu_seconds, threads)
+            cpu = {"value": v, "unit": "samples/s", "cores": threads, "kind": "reference", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 edge math, f64 knot selection/IO" if mode == hq.MODE_FAST else "f64",
+            "data": "synthetic (seeded random int8 tables of the head architecture; U(-1.5,1.5) features + 1% knots)",
+            "config": {"workload": "cfg2: compressed head {2048,1408,20}, K=65536, G=10, int8 "
+                                   "(12,957,696 B payload), batch 1 per GPU",
+                       "global_batch": B * world, "per_gpu_batch": B, "mode": args.mode,
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"batch-sharded replicas x{world}"},
+            "latency_us": step_ms * 1e3,
+            "gpu_launches": launches_per_step * args.steps,
+            "launches_per_step": launches_per_step,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+                         "frac": achieved / pk.get("hbm_gbs", 6537.0), "traffic": traffic,
+                         "kernel": "k_gather_fast layer 0 (2048->1408, 2,883,584 edges)",
+                         "kernel_us": k_ms * 1e3, "algorithmic_bytes": kernel_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("_fallback") else "")},
+            "call_roofline": {"bytes_per_call": call_bytes, "achieved_gbs": call_bytes / (step_ms * 1e-3) / 1e9},
+            "bs256": {"metric": "samples/s", "value": 256 / (ms256 * 1e-3), "ms_per_step": ms256,
+                      "global_batch": 256, "per_gpu_batch": hi - lo, "scaling": "strong",
+                      "edge_evals_per_s": 256 * edges / (ms256 * 1e-3),
+                      "effective_gbs": 256 * call_bytes / (ms256 * 1e-3) / 1e9},
+            "e2e": {"value": e2e_value, "unit": "samples/s",
+                    "h2d_bytes_per_step": int(xh.nbytes), "d2h_bytes_per_step": int(yh.nbytes),
+                    "ms_per_step": e2e_s * 1e3, "path": "skan_forward(SKAN_PTR_HOST) from pinned host memory"},
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

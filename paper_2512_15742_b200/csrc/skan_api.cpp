@@ -1,0 +1,862 @@
+// C-ABI implementation: validation, static planner, resident upload, and the
+// per-call launch sequence.  Host C++ only; kernels live in skan_kernels.cu.
+//
+// Reference interfaces replaced (paths under /root/reference/proj):
+//   plan_memory        src/lutham.cpp:52-86       -> skan_plan_memory
+//   build_model        src/lutham.cpp:214-271     -> skan_head_create (COMPRESSED)
+//   build_dense_model  src/lutham.cpp:177-195     -> skan_head_create (DENSE)
+//   make_workspace     src/lutham.cpp:757-763     -> skan_workspace_create
+//   compressed_forward src/lutham.cpp:819-850     -> skan_forward
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "skan.h"
+#include "skan_internal.hpp"
+
+using skan::DevLayer;
+using skan::Error;
+using skan::raise;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// thread-local last error (no exceptions cross the ABI)
+
+struct LastError {
+    skan_status status = SKAN_OK;
+    std::string msg;
+    uint64_t offset = 0;
+    int fault = SKAN_FAULT_NONE;
+};
+thread_local LastError g_err;
+
+template <class F>
+skan_status guarded(F&& f) {
+    try {
+        f();
+        return SKAN_OK;
+    } catch (const Error& e) {
+        g_err = {e.status, e.what(), e.offset, e.fault};
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_err = {SKAN_CONTRACT_ERROR, "host allocation failed", 0, SKAN_FAULT_NONE};
+        return SKAN_CONTRACT_ERROR;
+    } catch (const std::exception& e) {
+        g_err = {SKAN_CONTRACT_ERROR, e.what(), 0, SKAN_FAULT_NONE};
+        return SKAN_CONTRACT_ERROR;
+    }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        skan::cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) skan::cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// planner arithmetic (overflow-checked like lutham.cpp:27-39)
+
+uint64_t mul_checked(uint64_t a, uint64_t b) {
+    if (a != 0 && b > std::numeric_limits<uint64_t>::max() / a)
+        raise(SKAN_PLAN_ERROR, "size arithmetic overflows 64 bits");
+    return a * b;
+}
+uint64_t add_checked(uint64_t a, uint64_t b) {
+    if (b > std::numeric_limits<uint64_t>::max() - a)
+        raise(SKAN_PLAN_ERROR, "size arithmetic overflows 64 bits");
+    return a + b;
+}
+
+int index_bits(uint32_t k) {
+    if (k <= 1) return 0;
+    int b = 0;
+    for (uint32_t v = k - 1; v; v >>= 1) ++b;
+    return b;
+}
+
+bool is_int8(const skan_layer_header& h) { return (h.flags & SKAN_FLAG_INT8) != 0; }
+
+// Bytes of the B200 resident form (layout of upload_layer below).
+constexpr uint64_t kAlign = 256;
+uint64_t align_up(uint64_t v) { return add_checked(v, kAlign - 1) / kAlign * kAlign; }
+
+int device_format(const skan_layer_header& h) {
+    if (h.k == 0) return skan::FMT_DENSE;
+    if (is_int8(h)) return h.k <= 65536 ? skan::FMT_I8_R32 : skan::FMT_I8_WIDE;
+    return skan::FMT_F32;
+}
+
+uint64_t device_bytes(const skan_layer_header& h) {
+    const uint64_t e = mul_checked(h.in_dim, h.out_dim);
+    const int fmt = device_format(h);
+    uint64_t b = 0;
+    if (fmt == skan::FMT_DENSE) return align_up(mul_checked(mul_checked(e, h.grid_size), 4));
+    const uint64_t kg = mul_checked(h.k, h.grid_size);
+    if (fmt == skan::FMT_I8_R32) {
+        b = add_checked(b, align_up(mul_checked(e, 4)));        // records
+        b = add_checked(b, align_up(kg));                        // int8 codebook
+    } else if (fmt == skan::FMT_I8_WIDE) {
+        b = add_checked(b, align_up(mul_checked(e, 4)));        // u32 index
+        b = add_checked(b, align_up(mul_checked(e, 2)));        // gain|bias codes
+        b = add_checked(b, align_up(kg));
+    } else {
+        if (h.k > 1) b = add_checked(b, align_up(mul_checked(e, 4)));  // u32 index
+        b = add_checked(b, align_up(mul_checked(e, 4)));        // gains
+        b = add_checked(b, align_up(mul_checked(e, 4)));        // biases
+        b = add_checked(b, align_up(mul_checked(kg, 4)));       // f32 codebook
+    }
+    b = add_checked(b, align_up(256 * 4) + align_up(256 * 8));  // gain LUTs
+    b = add_checked(b, align_up(mul_checked(h.out_dim, 8)));     // bias sums
+    return b;
+}
+
+// plan_memory, lutham.cpp:52-86 (plus device bytes).
+skan_memory_plan plan(const skan_layer_header* hs, int n, skan_layer_plan* per) {
+    skan_memory_plan tot{};
+    uint64_t max_width = 0;
+    for (int l = 0; l < n; ++l) {
+        const skan_layer_header& h = hs[l];
+        if (h.in_dim == 0 || h.out_dim == 0 || h.grid_size < 2)
+            raise(SKAN_PLAN_ERROR, "layer header has degenerate dimensions");
+        const uint64_t e = mul_checked(h.in_dim, h.out_dim);
+        skan_layer_plan lp{};
+        if (h.k == 0) {
+            lp.codebook_bytes = mul_checked(mul_checked(e, h.grid_size), 4);
+        } else {
+            const uint64_t w = is_int8(h) ? 1 : 4;
+            lp.codebook_bytes = mul_checked(mul_checked(h.k, h.grid_size), w);
+            const int bits = index_bits(h.k);
+            lp.index_bytes = add_checked(mul_checked(e, static_cast<uint64_t>(bits)), 7) / 8;
+            if (bits > 0) lp.unpacked_index_bytes = mul_checked(e, h.k <= 65536 ? 2 : 4);
+            lp.gain_bytes = mul_checked(e, w);
+            lp.bias_bytes = mul_checked(e, w);
+        }
+        lp.device_bytes = device_bytes(h);
+        const uint64_t payload = add_checked(add_checked(lp.codebook_bytes, lp.index_bytes),
+                                             add_checked(lp.gain_bytes, lp.bias_bytes));
+        const uint64_t working = add_checked(add_checked(lp.codebook_bytes, lp.unpacked_index_bytes),
+                                             add_checked(lp.gain_bytes, lp.bias_bytes));
+        tot.payload_total = add_checked(tot.payload_total, payload);
+        tot.working_set_total = add_checked(tot.working_set_total, working);
+        tot.device_total = add_checked(tot.device_total, lp.device_bytes);
+        max_width = std::max<uint64_t>({max_width, h.in_dim, h.out_dim});
+        if (per) per[l] = lp;
+    }
+    tot.scratch_bytes = mul_checked(mul_checked(max_width, 2), sizeof(double));
+    tot.working_set_total = add_checked(tot.working_set_total, tot.scratch_bytes);
+    return tot;
+}
+
+// dequantize_gain_code, quant.cpp:88-91.  The LUT holds exactly the doubles
+// the reference produces per edge (same libm exp2, same expression), so the
+// exact kernel's gains are bitwise the reference's.
+double gain_of_code(int8_t code, double log_min, double log_step) {
+    if (code == 127) return 0.0;
+    return std::exp2(log_min + static_cast<double>(code) * log_step);
+}
+
+}  // namespace
+
+skan_status skan::set_error(skan_status s, const std::string& msg, uint64_t offset, int fault) {
+    g_err = {s, msg, offset, fault};
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// resident objects
+
+struct skan_head {
+    int device = 0;
+    int num_sms = 148;
+    std::vector<skan_layer_header> headers;
+    std::vector<DevLayer> dl;
+    std::vector<skan_layer_plan> lplan;
+    skan_memory_plan totals{};
+    void* dmem = nullptr;
+    uint64_t dbytes = 0;
+    uint64_t edges = 0;
+    int in_dim = 0, out_dim = 0, max_width = 0;
+};
+
+struct skan_workspace {
+    const skan_head* head = nullptr;
+    int device = 0;
+    int max_batch = 0;
+    int width = 0;
+    uint64_t interp_ops = 0;
+    skan::DevScratch d{};
+    double* xin = nullptr;   // staging for host inputs
+    double* yout = nullptr;  // staging for host outputs
+    uint64_t partial_floats = 0;
+    int* h_err = nullptr;    // pinned
+    cudaStream_t last_stream = nullptr;
+    int last_launches = 0;
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// head construction
+
+// Host-side staging of one layer's resident form before upload.
+struct Staged {
+    skan_layer_header h{};
+    std::vector<uint32_t> rec;    // FMT_I8_R32 records
+    std::vector<uint32_t> idx;    // u32 indices (WIDE / F32)
+    std::vector<uint16_t> gb;     // WIDE gain|bias codes
+    std::vector<float> gain, bias;
+    std::vector<int8_t> cb8;
+    std::vector<float> cb32;      // codebook or dense grid
+    double lutd[256] = {};
+    float lutf[256] = {};
+    std::vector<double> bias_sum;
+};
+
+void check_domain(const skan_layer_header& h, int l) {
+    if (!(h.domain_lo < h.domain_hi) || !std::isfinite(h.domain_lo) || !std::isfinite(h.domain_hi))
+        raise(SKAN_CONTRACT_ERROR, "layer " + std::to_string(l) + " has an invalid domain");
+}
+
+void fill_int8_luts(Staged& s) {
+    for (int c = 0; c < 256; ++c) {
+        const int8_t code = static_cast<int8_t>(c);
+        const double g = gain_of_code(code, s.h.gain_log_min, s.h.gain_log_step);
+        s.lutd[c] = g;
+        s.lutf[c] = static_cast<float>(g * s.h.codebook_scale);
+    }
+}
+
+// Σ_i b_ij in ascending i, per output j (fast path bias term; valid because
+// (1-t)+t == 1 in double, SURVEY.md §7 "hard parts").
+template <class BiasAt>
+void fill_bias_sum(Staged& s, BiasAt bias_at) {
+    const uint32_t in = s.h.in_dim, out = s.h.out_dim;
+    s.bias_sum.assign(out, 0.0);
+    for (uint32_t i = 0; i < in; ++i)
+        for (uint32_t j = 0; j < out; ++j)
+            s.bias_sum[j] += bias_at(static_cast<uint64_t>(i) * out + j);
+}
+
+void pack_int8_edges(Staged& s, const uint32_t* idx32, const uint16_t* idx16, const int8_t* gcodes,
+                     const int8_t* bcodes) {
+    const uint64_t e = static_cast<uint64_t>(s.h.in_dim) * s.h.out_dim;
+    auto index_at = [&](uint64_t n) -> uint32_t {
+        if (idx16) return idx16[n];
+        if (idx32) return idx32[n];
+        return 0u;
+    };
+    if (s.h.k <= 65536) {
+        s.rec.resize(e);
+        for (uint64_t n = 0; n < e; ++n)
+            s.rec[n] = (index_at(n) & 0xFFFFu) | (static_cast<uint32_t>(static_cast<uint8_t>(gcodes[n])) << 16) |
+                       (static_cast<uint32_t>(static_cast<uint8_t>(bcodes[n])) << 24);
+    } else {
+        s.idx.resize(e);
+        s.gb.resize(e);
+        for (uint64_t n = 0; n < e; ++n) {
+            s.idx[n] = index_at(n);
+            s.gb[n] = static_cast<uint16_t>(static_cast<uint8_t>(gcodes[n]) |
+                                            (static_cast<uint16_t>(static_cast<uint8_t>(bcodes[n])) << 8));
+        }
+    }
+    fill_int8_luts(s);
+    const double bs = s.h.bias_scale;
+    fill_bias_sum(s, [&](uint64_t n) { return static_cast<double>(bcodes[n]) * bs; });
+}
+
+// build_model semantics (lutham.cpp:214-271) for one CompressedLayer.
+Staged stage_compressed(const skan_layer_desc& d, int l) {
+    const std::string where = "layer " + std::to_string(l);
+    const skan_layer_header& hd = d.header;
+    if (hd.in_dim == 0 || hd.out_dim == 0) raise(SKAN_SHAPE_ERROR, where + " has a zero dimension");
+    const uint64_t e = static_cast<uint64_t>(hd.in_dim) * hd.out_dim;
+    const int k = static_cast<int>(hd.k);
+    if (hd.k < 1 || k < 1) raise(SKAN_CONTRACT_ERROR, "compressed layer has an empty codebook");
+    if (d.n_indices != e || d.n_gains != e || d.n_biases != e)
+        raise(SKAN_CONTRACT_ERROR, "compressed layer tables disagree on edge count");
+    const uint64_t kg = static_cast<uint64_t>(hd.k) * hd.grid_size;
+    if (d.n_codebook != kg) raise(SKAN_CONTRACT_ERROR, "codebook does not match layer grid size");
+    if (e && (!d.indices || !d.gains || !d.biases)) raise(SKAN_CONTRACT_ERROR, where + " is missing tables");
+    if (kg && !d.codebook) raise(SKAN_CONTRACT_ERROR, where + " is missing its codebook");
+    for (uint64_t n = 0; n < e; ++n)
+        if (d.indices[n] >= hd.k) raise(SKAN_CONTRACT_ERROR, "edge index exceeds codebook size");
+    for (uint64_t n = 0; n < e; ++n)
+        if (!(d.gains[n] >= 0.0)) raise(SKAN_CONTRACT_ERROR, "edge gains must be nonnegative");
+    Staged s;
+    s.h = hd;
+    s.h.reserved = 0;
+    if (d.has_int8) {
+        if (d.n_codebook_codes != kg || d.n_gain_codes != e || d.n_bias_codes != e ||
+            (kg && !d.codebook_codes) || (e && (!d.gain_codes || !d.bias_codes)))
+            raise(SKAN_CONTRACT_ERROR, "int8 tables disagree with layer dimensions");
+        s.h.flags = SKAN_FLAG_INT8;
+        s.h.codebook_scale = d.codebook_scale;
+        s.h.gain_log_min = d.gain_log_min;
+        s.h.gain_log_step = d.gain_log_step;
+        s.h.bias_scale = d.bias_scale;
+        s.cb8.assign(d.codebook_codes, d.codebook_codes + kg);
+        pack_int8_edges(s, d.indices, nullptr, d.gain_codes, d.bias_codes);
+    } else {
+        s.h.flags = 0;
+        s.h.codebook_scale = 0.0;
+        s.h.gain_log_min = 0.0;
+        s.h.gain_log_step = 1.0;
+        s.h.bias_scale = 0.0;
+        s.cb32.resize(kg);
+        for (uint64_t n = 0; n < kg; ++n) s.cb32[n] = static_cast<float>(d.codebook[n]);
+        if (hd.k > 1) s.idx.assign(d.indices, d.indices + e);
+        s.gain.resize(e);
+        s.bias.resize(e);
+        for (uint64_t n = 0; n < e; ++n) {
+            s.gain[n] = static_cast<float>(d.gains[n]);
+            s.bias[n] = static_cast<float>(d.biases[n]);
+        }
+        fill_bias_sum(s, [&](uint64_t n) { return static_cast<double>(s.bias[n]); });
+    }
+    return s;
+}
+
+// build_dense_model semantics (lutham.cpp:177-195)
+Staged stage_dense(const skan_layer_desc& d, int l) {
+    const skan_layer_header& hd = d.header;
+    if (hd.in_dim == 0 || hd.out_dim == 0) raise(SKAN_SHAPE_ERROR, "layer dimensions must be positive");
+    if (hd.grid_size < 2) raise(SKAN_SHAPE_ERROR, "grid size must be at least 2");
+    const uint64_t eg = static_cast<uint64_t>(hd.in_dim) * hd.out_dim * hd.grid_size;
+    if (d.n_coefficients != eg || (eg && !d.coefficients))
+        raise(SKAN_SHAPE_ERROR, "layer " + std::to_string(l) + " coefficient table has the wrong size");
+    Staged s;
+    s.h = hd;
+    s.h.k = 0;
+    s.h.flags = 0;
+    s.h.reserved = 0;
+    s.cb32.resize(eg);
+    for (uint64_t n = 0; n < eg; ++n) s.cb32[n] = static_cast<float>(d.coefficients[n]);
+    return s;
+}
+
+// RuntimeLayer resident tables (lutham.hpp:91-109), e.g. from deserialize.
+Staged stage_runtime(const skan_layer_desc& d, int l) {
+    const std::string where = "layer " + std::to_string(l);
+    const skan_layer_header& hd = d.header;
+    if (hd.in_dim == 0 || hd.out_dim == 0 || hd.grid_size < 2)
+        raise(SKAN_CONTRACT_ERROR, where + " has degenerate dimensions");
+    const uint64_t e = static_cast<uint64_t>(hd.in_dim) * hd.out_dim;
+    Staged s;
+    s.h = hd;
+    if (hd.k == 0) {
+        if (is_int8(hd)) raise(SKAN_CONTRACT_ERROR, where + ": dense layers are float only");
+        if (!d.table_f32) raise(SKAN_CONTRACT_ERROR, where + " coefficient table is missing");
+        s.cb32.assign(d.table_f32, d.table_f32 + e * hd.grid_size);
+        return s;
+    }
+    const uint64_t kg = static_cast<uint64_t>(hd.k) * hd.grid_size;
+    const int bits = index_bits(hd.k);
+    const uint16_t* i16 = bits > 0 && hd.k <= 65536 ? d.idx16 : nullptr;
+    const uint32_t* i32 = bits > 0 && hd.k > 65536 ? d.idx32 : nullptr;
+    if (bits > 0 && !i16 && !i32) raise(SKAN_CONTRACT_ERROR, where + " index table has the wrong size");
+    for (uint64_t n = 0; n < e && bits > 0; ++n) {
+        const uint32_t v = i16 ? i16[n] : i32[n];
+        if (v >= hd.k) raise(SKAN_CONTRACT_ERROR, where + " edge " + std::to_string(n) + " indexes past the codebook");
+    }
+    if (is_int8(hd)) {
+        if (!d.table_i8 || !d.rt_gain_codes || !d.rt_bias_codes)
+            raise(SKAN_CONTRACT_ERROR, where + " int8 tables have the wrong size");
+        s.cb8.assign(d.table_i8, d.table_i8 + kg);
+        pack_int8_edges(s, i32, i16, d.rt_gain_codes, d.rt_bias_codes);
+    } else {
+        if (!d.table_f32 || !d.gains_f32 || !d.biases_f32)
+            raise(SKAN_CONTRACT_ERROR, where + " float tables have the wrong size");
+        s.cb32.assign(d.table_f32, d.table_f32 + kg);
+        if (hd.k > 1) {
+            s.idx.resize(e);
+            for (uint64_t n = 0; n < e; ++n) s.idx[n] = i16 ? i16[n] : i32[n];
+        }
+        s.gain.assign(d.gains_f32, d.gains_f32 + e);
+        s.bias.assign(d.biases_f32, d.biases_f32 + e);
+        fill_bias_sum(s, [&](uint64_t n) { return static_cast<double>(s.bias[n]); });
+    }
+    return s;
+}
+
+// Copy the staged layers into one device allocation (sub-buffers 256-B
+// aligned) and fill the kernel-side DevLayer views.
+void upload(skan_head* h, std::vector<Staged>& st) {
+    uint64_t total = 0;
+    for (const auto& lp : h->lplan) total = add_checked(total, lp.device_bytes);
+    h->dbytes = total;
+    skan::cuda_check(cudaMalloc(&h->dmem, std::max<uint64_t>(total, 256)), "cudaMalloc(head)");
+    std::vector<uint8_t> host(total, 0);
+    uint64_t cur = 0;
+    auto put = [&](const void* src, uint64_t bytes) -> void* {
+        void* dst = static_cast<uint8_t*>(h->dmem) + cur;
+        if (bytes) std::memcpy(host.data() + cur, src, bytes);
+        cur = align_up(add_checked(cur, bytes));
+        return dst;
+    };
+    for (size_t l = 0; l < st.size(); ++l) {
+        Staged& s = st[l];
+        DevLayer d{};
+        d.in = static_cast<int>(s.h.in_dim);
+        d.out = static_cast<int>(s.h.out_dim);
+        d.G = static_cast<int>(s.h.grid_size);
+        d.K = static_cast<int>(s.h.k);
+        d.fmt = device_format(s.h);
+        d.lo = s.h.domain_lo;
+        d.hi = s.h.domain_hi;
+        d.dx = (s.h.domain_hi - s.h.domain_lo) / static_cast<double>(static_cast<int>(s.h.grid_size) - 1);
+        d.cs = s.h.codebook_scale;
+        d.bs = s.h.bias_scale;
+        const uint64_t begin = cur;
+        switch (d.fmt) {
+            case skan::FMT_DENSE:
+                d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
+                break;
+            case skan::FMT_I8_R32:
+                d.rec = static_cast<const uint32_t*>(put(s.rec.data(), s.rec.size() * 4));
+                d.cb8 = static_cast<const int8_t*>(put(s.cb8.data(), s.cb8.size()));
+                break;
+            case skan::FMT_I8_WIDE:
+                d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
+                d.gb = static_cast<const uint16_t*>(put(s.gb.data(), s.gb.size() * 2));
+                d.cb8 = static_cast<const int8_t*>(put(s.cb8.data(), s.cb8.size()));
+                break;
+            default:
+                if (s.h.k > 1) d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
+                d.gain = static_cast<const float*>(put(s.gain.data(), s.gain.size() * 4));
+                d.bias = static_cast<const float*>(put(s.bias.data(), s.bias.size() * 4));
+                d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
+                break;
+        }
+        if (d.fmt != skan::FMT_DENSE) {
+            d.lutf = static_cast<const float*>(put(s.lutf, sizeof s.lutf));
+            d.lutd = static_cast<const double*>(put(s.lutd, sizeof s.lutd));
+            d.bias_sum = static_cast<const double*>(put(s.bias_sum.data(), s.bias_sum.size() * 8));
+        } else {
+            cur = add_checked(cur, align_up(256 * 4) + align_up(256 * 8) + align_up(uint64_t(d.out) * 8));
+        }
+        (void)begin;
+        h->dl.push_back(d);
+        h->headers.push_back(s.h);
+    }
+    skan::cuda_check(cudaMemcpy(h->dmem, host.data(), total, cudaMemcpyHostToDevice), "upload head");
+}
+
+skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
+    if (n <= 0 || !layers) raise(SKAN_SHAPE_ERROR, "model has no layers");
+    int ndev = 0;
+    skan::cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) raise(SKAN_CONTRACT_ERROR, "no such CUDA device");
+    std::vector<Staged> st;
+    st.reserve(n);
+    for (int l = 0; l < n; ++l) {
+        switch (layers[l].kind) {
+            case SKAN_LAYER_COMPRESSED: st.push_back(stage_compressed(layers[l], l)); break;
+            case SKAN_LAYER_DENSE: st.push_back(stage_dense(layers[l], l)); break;
+            case SKAN_LAYER_RUNTIME: st.push_back(stage_runtime(layers[l], l)); break;
+            default: raise(SKAN_CONTRACT_ERROR, "unknown layer descriptor kind");
+        }
+        check_domain(st.back().h, l);
+        if (l > 0 && st[l].h.in_dim != st[l - 1].h.out_dim)
+            raise(SKAN_SHAPE_ERROR, "layer " + std::to_string(l - 1) + " out_dim does not match layer " +
+                                        std::to_string(l) + " in_dim");
+    }
+    auto h = std::make_unique<skan_head>();
+    h->device = device;
+    std::vector<skan_layer_header> hs;
+    for (auto& s : st) hs.push_back(s.h);
+    h->lplan.resize(n);
+    h->totals = plan(hs.data(), n, h->lplan.data());
+    DeviceGuard g(device);
+    skan::cuda_check(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    upload(h.get(), st);
+    h->in_dim = static_cast<int>(hs.front().in_dim);
+    h->out_dim = static_cast<int>(hs.back().out_dim);
+    uint32_t w = 0;
+    for (auto& x : hs) {
+        w = std::max({w, x.in_dim, x.out_dim});
+        h->edges += static_cast<uint64_t>(x.in_dim) * x.out_dim;
+    }
+    h->max_width = static_cast<int>(w);
+    return h.release();
+}
+
+// ---------------------------------------------------------------------------
+// forward
+
+uint64_t partial_floats_for(const skan_head* h, int max_batch) {
+    uint64_t best = 0;
+    for (const DevLayer& L : h->dl) {
+        for (int b = 1; b <= max_batch; ++b) {
+            const skan::LaunchCfg c = skan::choose_cfg(L, b, false, h->num_sms);
+            best = std::max<uint64_t>(best, static_cast<uint64_t>(c.nsplit) * b * L.out);
+        }
+    }
+    return best;
+}
+
+// Enqueue one chunk (B <= ws->max_batch) on `s`; x/y are device pointers.
+int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B, double* y,
+                  bool exact, cudaStream_t s) {
+    const int nl = static_cast<int>(h->dl.size());
+    auto& d = ws->d;
+    int launches = 0;
+    skan::launch_locate_input(x, B, h->dl[0].in, h->dl[0], d.bm, d.btf, d.btd, d.err, s);
+    ++launches;
+    for (int l = 0; l < nl; ++l) {
+        const DevLayer& L = h->dl[l];
+        const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
+        double* out = next ? d.act[l & 1] : y;
+        const skan::LaunchCfg c = skan::choose_cfg(L, B, exact, h->num_sms);
+        if (exact) {
+            skan::launch_gather_exact(L, c, B, d.bm, d.btd, out, s);
+            ++launches;
+            if (next) {
+                skan::launch_locate_input(out, B, L.out, *next, d.bm, d.btf, d.btd, d.err, s);
+                ++launches;
+            }
+        } else {
+            skan::launch_gather_fast(L, c, B, d.bm, d.btf, d.partial, s);
+            skan::launch_combine(L, c, B, d.partial, out, next, d.bm, d.btf, d.btd, d.err, s);
+            launches += 2;
+        }
+    }
+    skan::cuda_check(cudaGetLastError(), "kernel launch");
+    return launches;
+}
+
+void check_forward_args(const skan_head* h, const skan_workspace* ws, int batch) {
+    if (!h) raise(SKAN_SHAPE_ERROR, "model has no layers");
+    if (batch < 0) raise(SKAN_SHAPE_ERROR, "batch must be nonnegative");
+    if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
+    if (ws->width < h->max_width)
+        raise(SKAN_CONTRACT_ERROR, "workspace is smaller than the model's widest layer");
+    if (ws->device != h->device) raise(SKAN_CONTRACT_ERROR, "workspace lives on another device");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+skan_status skan_last_error(char* msg, size_t cap, uint64_t* off, int* fault) {
+    if (msg && cap) {
+        std::strncpy(msg, g_err.msg.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    if (off) *off = g_err.offset;
+    if (fault) *fault = g_err.fault;
+    return g_err.status;
+}
+
+const char* skan_status_name(skan_status s) {
+    switch (s) {
+        case SKAN_OK: return "OK";
+        case SKAN_SHAPE_ERROR: return "ShapeError";
+        case SKAN_VALUE_ERROR: return "ValueError";
+        case SKAN_CONTRACT_ERROR: return "ContractError";
+        case SKAN_FORMAT_ERROR: return "FormatError";
+        case SKAN_PLAN_ERROR: return "PlanError";
+        case SKAN_CUDA_ERROR: return "CudaError";
+    }
+    return "Unknown";
+}
+
+int skan_abi_version(void) { return SKAN_ABI_VERSION; }
+
+int skan_index_bits(uint32_t k) { return index_bits(k); }
+
+skan_status skan_plan_memory(const skan_layer_header* hs, int n, skan_layer_plan* per,
+                             skan_memory_plan* totals) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && !hs)) raise(SKAN_SHAPE_ERROR, "bad header list");
+        const skan_memory_plan t = plan(hs, n, per);
+        if (totals) *totals = t;
+    });
+}
+
+skan_status skan_head_create(const skan_layer_desc* layers, int n, int device, skan_head** out) {
+    return guarded([&] {
+        if (!out) raise(SKAN_CONTRACT_ERROR, "null output handle");
+        *out = create_head(layers, n, device);
+    });
+}
+
+skan_status skan_head_destroy(skan_head* h) {
+    return guarded([&] {
+        if (!h) return;
+        if (h->dmem) {
+            DeviceGuard g(h->device);
+            cudaFree(h->dmem);
+        }
+        delete h;
+    });
+}
+
+int skan_head_num_layers(const skan_head* h) { return h ? static_cast<int>(h->dl.size()) : 0; }
+int skan_head_input_dim(const skan_head* h) { return h ? h->in_dim : 0; }
+int skan_head_output_dim(const skan_head* h) { return h ? h->out_dim : 0; }
+int skan_head_max_width(const skan_head* h) { return h ? h->max_width : 0; }
+int skan_head_device(const skan_head* h) { return h ? h->device : -1; }
+uint64_t skan_head_edges(const skan_head* h) { return h ? h->edges : 0; }
+
+skan_status skan_head_layer_header(const skan_head* h, int l, skan_layer_header* out) {
+    return guarded([&] {
+        if (!h || l < 0 || l >= static_cast<int>(h->headers.size()))
+            raise(SKAN_SHAPE_ERROR, "layer index out of range");
+        *out = h->headers[l];
+    });
+}
+
+skan_status skan_head_plan(const skan_head* h, skan_layer_plan* per, skan_memory_plan* totals) {
+    return guarded([&] {
+        if (!h) raise(SKAN_CONTRACT_ERROR, "null head");
+        if (per) std::copy(h->lplan.begin(), h->lplan.end(), per);
+        if (totals) *totals = h->totals;
+    });
+}
+
+skan_status skan_head_set_l2_persist(const skan_head* h, void* stream, float fraction) {
+    return guarded([&] {
+        if (!h) raise(SKAN_CONTRACT_ERROR, "null head");
+        DeviceGuard g(h->device);
+        cudaStreamAttrValue v{};
+        if (fraction > 0.f) {
+            int max_persist = 0, max_window = 0;
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+            const size_t want = std::min<size_t>(h->dbytes, static_cast<size_t>(max_persist));
+            skan::cuda_check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want), "persisting L2 limit");
+            v.accessPolicyWindow.base_ptr = h->dmem;
+            v.accessPolicyWindow.num_bytes = std::min<size_t>(h->dbytes, static_cast<size_t>(max_window));
+            v.accessPolicyWindow.hitRatio = std::min(1.f, fraction);
+            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        } else {
+            v.accessPolicyWindow.num_bytes = 0;
+        }
+        skan::cuda_check(cudaStreamSetAttribute(static_cast<cudaStream_t>(stream),
+                                                cudaStreamAttributeAccessPolicyWindow, &v),
+                         "access policy window");
+    });
+}
+
+skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_workspace** out) {
+    return guarded([&] {
+        if (!h || !out) raise(SKAN_CONTRACT_ERROR, "null head or output handle");
+        if (max_batch < 1) raise(SKAN_SHAPE_ERROR, "workspace needs max_batch >= 1");
+        DeviceGuard g(h->device);
+        auto ws = std::make_unique<skan_workspace>();
+        ws->head = h;
+        ws->device = h->device;
+        ws->max_batch = max_batch;
+        ws->width = h->max_width;
+        const size_t act = static_cast<size_t>(max_batch) * h->max_width;
+        auto alloc = [&](size_t bytes) {
+            void* p = nullptr;
+            skan::cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc(workspace)");
+            ws->allocs.push_back(p);
+            return p;
+        };
+        ws->d.act[0] = static_cast<double*>(alloc(act * 8));
+        ws->d.act[1] = static_cast<double*>(alloc(act * 8));
+        ws->d.bm = static_cast<int*>(alloc(act * 4));
+        ws->d.btf = static_cast<float*>(alloc(act * 4));
+        ws->d.btd = static_cast<double*>(alloc(act * 8));
+        ws->partial_floats = partial_floats_for(h, max_batch);
+        ws->d.partial = static_cast<float*>(alloc(ws->partial_floats * 4));
+        ws->d.err = static_cast<int*>(alloc(sizeof(int)));
+        ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
+        ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
+        skan::cuda_check(cudaMallocHost(&ws->h_err, sizeof(int)), "cudaMallocHost");
+        *ws->h_err = 0;
+        skan::cuda_check(cudaMemset(ws->d.err, 0, sizeof(int)), "cudaMemset");
+        *out = ws.release();
+    });
+}
+
+skan_status skan_workspace_destroy(skan_workspace* ws) {
+    return guarded([&] {
+        if (!ws) return;
+        DeviceGuard g(ws->device);
+        for (void* p : ws->allocs) cudaFree(p);
+        if (ws->h_err) cudaFreeHost(ws->h_err);
+        delete ws;
+    });
+}
+
+uint64_t skan_workspace_interp_ops(const skan_workspace* ws) { return ws ? ws->interp_ops : 0; }
+int skan_workspace_max_batch(const skan_workspace* ws) { return ws ? ws->max_batch : 0; }
+int skan_workspace_width(const skan_workspace* ws) { return ws ? ws->width : 0; }
+int skan_workspace_last_launches(const skan_workspace* ws) { return ws ? ws->last_launches : 0; }
+
+skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* inputs,
+                         uint64_t n_inputs, int batch, double* outputs, uint64_t n_outputs,
+                         int mode, unsigned ptr_flags, void* stream) {
+    return guarded([&] {
+        check_forward_args(h, ws, batch);
+        const uint64_t in = static_cast<uint64_t>(h->in_dim), out = static_cast<uint64_t>(h->out_dim);
+        if (n_inputs != in * static_cast<uint64_t>(batch))
+            raise(SKAN_SHAPE_ERROR, "input buffer does not match batch * input_dim");
+        if (n_outputs != out * static_cast<uint64_t>(batch))
+            raise(SKAN_SHAPE_ERROR, "output buffer does not match batch * output_dim");
+        if (mode != SKAN_MODE_FAST && mode != SKAN_MODE_EXACT) raise(SKAN_CONTRACT_ERROR, "unknown mode");
+        const bool exact = mode == SKAN_MODE_EXACT;
+        const bool host = (ptr_flags & SKAN_PTR_DEVICE) == 0;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        DeviceGuard g(h->device);
+        ws->last_stream = s;
+        ws->last_launches = 0;
+        if (batch == 0) return;
+        skan::cuda_check(cudaMemsetAsync(ws->d.err, 0, sizeof(int), s), "reset error flag");
+        for (int b0 = 0; b0 < batch; b0 += ws->max_batch) {
+            const int B = std::min(ws->max_batch, batch - b0);
+            const double* x = inputs + static_cast<size_t>(b0) * in;
+            double* y = outputs + static_cast<size_t>(b0) * out;
+            if (host) {
+                skan::cuda_check(cudaMemcpyAsync(ws->xin, x, static_cast<size_t>(B) * in * 8,
+                                                 cudaMemcpyHostToDevice, s), "H2D inputs");
+                ws->last_launches += enqueue_chunk(h, ws, ws->xin, B, ws->yout, exact, s);
+                skan::cuda_check(cudaMemcpyAsync(y, ws->yout, static_cast<size_t>(B) * out * 8,
+                                                 cudaMemcpyDeviceToHost, s), "D2H outputs");
+            } else {
+                ws->last_launches += enqueue_chunk(h, ws, x, B, y, exact, s);
+            }
+        }
+        ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;
+        skan::cuda_check(cudaMemcpyAsync(ws->h_err, ws->d.err, sizeof(int), cudaMemcpyDeviceToHost, s),
+                         "error flag");
+        if (host) {
+            skan::cuda_check(cudaStreamSynchronize(s), "forward");
+            if (*ws->h_err) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+        }
+    });
+}
+
+skan_status skan_forward_async(const skan_head* h, skan_workspace* ws, const double* x, int batch,
+                               double* y, int mode, void* stream) {
+    if (!h) return guarded([&] { raise(SKAN_SHAPE_ERROR, "model has no layers"); });
+    return skan_forward(h, ws, x, static_cast<uint64_t>(h->in_dim) * (batch > 0 ? batch : 0), batch, y,
+                        static_cast<uint64_t>(h->out_dim) * (batch > 0 ? batch : 0), mode, SKAN_PTR_DEVICE,
+                        stream);
+}
+
+skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int layer, int batch, int mode,
+                                void* stream) {
+    return guarded([&] {
+        check_forward_args(h, ws, batch);
+        if (layer < 0 || layer >= static_cast<int>(h->dl.size())) raise(SKAN_SHAPE_ERROR, "layer index out of range");
+        if (batch < 1 || batch > ws->max_batch) raise(SKAN_CONTRACT_ERROR, "batch outside the workspace capacity");
+        DeviceGuard g(h->device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const DevLayer& L = h->dl[layer];
+        const bool exact = mode == SKAN_MODE_EXACT;
+        const skan::LaunchCfg c = skan::choose_cfg(L, batch, exact, h->num_sms);
+        if (exact) {
+            skan::launch_gather_exact(L, c, batch, ws->d.bm, ws->d.btd, ws->d.act[1], s);
+        } else {
+            skan::launch_gather_fast(L, c, batch, ws->d.bm, ws->d.btf, ws->d.partial, s);
+        }
+        skan::cuda_check(cudaGetLastError(), "profile launch");
+    });
+}
+
+skan_status skan_workspace_check(skan_workspace* ws) {
+    return guarded([&] {
+        if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
+        DeviceGuard g(ws->device);
+        skan::cuda_check(cudaStreamSynchronize(ws->last_stream), "forward");
+        if (*ws->h_err) {
+            *ws->h_err = 0;
+            raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+        }
+    });
+}
+
+skan_status skan_forward_multi(const skan_head* const* heads, skan_workspace* const* wss, int n,
+                               const double* x, int batch, double* const* ys, int mode, void* stream) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && (!heads || !wss || !ys))) raise(SKAN_SHAPE_ERROR, "bad head list");
+        for (int q = 0; q < n; ++q) {
+            check_forward_args(heads[q], wss[q], batch);
+            if (heads[q]->in_dim != heads[0]->in_dim)
+                raise(SKAN_SHAPE_ERROR, "heads sharing a feature batch must share input_dim");
+            if (heads[q]->device != heads[0]->device)
+                raise(SKAN_CONTRACT_ERROR, "heads must live on one device");
+        }
+        for (int q = 0; q < n; ++q) {
+            const skan_status st = skan_forward_async(heads[q], wss[q], x, batch, ys[q], mode, stream);
+            if (st != SKAN_OK) raise(st, g_err.msg);
+        }
+    });
+}
+
+skan_status skan_locate(const double* x, int n, double lo, double hi, int G, int* idx, double* t,
+                        uint8_t* clamped, void* stream) {
+    return guarded([&] {
+        if (n < 0) raise(SKAN_SHAPE_ERROR, "negative count");
+        if (G < 2) raise(SKAN_SHAPE_ERROR, "grid size must be at least 2");
+        int* d_err = nullptr;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        skan::cuda_check(cudaMallocAsync(&d_err, sizeof(int), s), "cudaMallocAsync");
+        skan::cuda_check(cudaMemsetAsync(d_err, 0, sizeof(int), s), "memset");
+        skan::launch_locate_raw(x, n, lo, hi, G, idx, t, clamped, d_err, s);
+        int herr = 0;
+        skan::cuda_check(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s), "copy");
+        skan::cuda_check(cudaFreeAsync(d_err, s), "free");
+        skan::cuda_check(cudaStreamSynchronize(s), "locate");
+        if (herr) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+    });
+}
+
+skan_status skan_pli_lookup(const double* cb, int k, int G, const int* rows, const double* g,
+                            const double* b, const double* x, double lo, double hi, int n, double* y,
+                            void* stream) {
+    return guarded([&] {
+        if (n < 0) raise(SKAN_SHAPE_ERROR, "negative count");
+        if (G < 2 || k < 1) raise(SKAN_SHAPE_ERROR, "bad codebook shape");
+        int* d_err = nullptr;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        skan::cuda_check(cudaMallocAsync(&d_err, sizeof(int), s), "cudaMallocAsync");
+        skan::cuda_check(cudaMemsetAsync(d_err, 0, sizeof(int), s), "memset");
+        skan::launch_pli_lookup(cb, k, G, rows, g, b, x, lo, hi, n, y, d_err, s);
+        int herr = 0;
+        skan::cuda_check(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s), "copy");
+        skan::cuda_check(cudaFreeAsync(d_err, s), "free");
+        skan::cuda_check(cudaStreamSynchronize(s), "pli_lookup");
+        if (herr & 2) raise(SKAN_SHAPE_ERROR, "codebook row out of range");
+        if (herr & 1) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+    });
+}
+
+skan_status skan_unpack_indices(const uint8_t* bytes, size_t n_bytes, uint64_t count, int bits,
+                                uint32_t* out, void* stream) {
+    return guarded([&] {
+        if (bits < 0 || bits > 32) raise(SKAN_CONTRACT_ERROR, "index width must be 0..32 bits");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        if (bits == 0) {
+            skan::cuda_check(cudaMemsetAsync(out, 0, count * sizeof(uint32_t), s), "memset");
+            return;
+        }
+        if (n_bytes < (count * static_cast<uint64_t>(bits) + 7) / 8)
+            raise(SKAN_CONTRACT_ERROR, "packed index buffer is too small");
+        skan::launch_unpack_indices(bytes, count, bits, out, s);
+        skan::cuda_check(cudaGetLastError(), "unpack launch");
+    });
+}
+
+}  // extern "C"

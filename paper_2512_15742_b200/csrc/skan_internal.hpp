@@ -1,0 +1,112 @@
+// Internal types shared by the C-ABI host code (skan_api.cpp, skan_format.cpp)
+// and the sm_100a kernels (skan_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "skan.h"
+
+namespace skan {
+
+// ---------------------------------------------------------------------------
+// Errors: C++ exceptions inside the library, converted to skan_status at the
+// ABI boundary (skan_api.cpp: guarded()).  Mirrors errors.hpp.
+struct Error : std::runtime_error {
+    skan_status status;
+    uint64_t offset;
+    int fault;
+    Error(skan_status s, const std::string& m, uint64_t off = 0, int f = SKAN_FAULT_NONE)
+        : std::runtime_error(m), status(s), offset(off), fault(f) {}
+};
+
+[[noreturn]] inline void raise(skan_status s, const std::string& m) { throw Error(s, m); }
+[[noreturn]] inline void raise_format(int fault, uint64_t off, const std::string& m) {
+    throw Error(SKAN_FORMAT_ERROR, m + " (byte offset " + std::to_string(off) + ")", off, fault);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(SKAN_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Resident device formats of one layer.
+enum Fmt : int {
+    // int8 tables, K <= 65536: one 32-bit record per edge
+    //   bits 0-15 codebook row, 16-23 log-gain code, 24-31 linear bias code
+    // (PAPER.md:193-194's 32 bits/edge), codebook int8 K x G.
+    FMT_I8_R32 = 0,
+    // int8 tables, K > 65536: u32 row index + u16 (gain code | bias code << 8)
+    FMT_I8_WIDE = 1,
+    // f32 tables: u32 row index, f32 gain, f32 bias, f32 codebook K x G
+    FMT_F32 = 2,
+    // dense layer (k == 0): f32 grid E x G (lutham.cpp:778-791)
+    FMT_DENSE = 3,
+};
+
+// Everything a kernel needs about one layer; passed by value as a kernel
+// parameter.  All pointers are device pointers into the head's single
+// resident allocation.
+struct DevLayer {
+    int in, out, G, K, fmt;
+    double lo, hi, dx;  // dx = (hi - lo) / (G - 1), computed once on the host (IEEE, as kan.cpp:24)
+    double cs, bs;      // int8 codebook scale, bias scale
+    const uint32_t* rec;     // FMT_I8_R32
+    const uint32_t* idx;     // FMT_I8_WIDE / FMT_F32 (nullptr when K == 1)
+    const uint16_t* gb;      // FMT_I8_WIDE
+    const float* gain;       // FMT_F32
+    const float* bias;       // FMT_F32
+    const int8_t* cb8;       // int8 codebook
+    const float* cb32;       // f32 codebook, or dense grid
+    const float* lutf;       // [128] float(gain(code) * cs) — fast int8 path
+    const double* lutd;      // [128] gain(code) as dequantize_gain_code returns it
+    const double* bias_sum;  // [out] sum_i b_ij in i order — fast path
+};
+
+// Per-layer launch plan for one batch size (chosen on the host).
+struct LaunchCfg {
+    int tj;      // outputs per CTA (32/64/128)
+    int spt;     // samples per thread (1/2/4/8)
+    int jt, st;  // CTA tiles along j and samples
+    int nsplit;  // i-splits (fast path); 1 in exact mode
+    int ichunk;  // inputs per split
+};
+
+// Workspace device buffers (one forward stream).
+struct DevScratch {
+    double* act[2];     // ping-pong activations [max_batch * max_width]
+    int* bm;            // bracket index [max_batch * max_width]
+    float* btf;         // bracket t (f32)
+    double* btd;        // bracket t (f64)
+    float* partial;     // split partial sums
+    int* err;           // non-finite flag
+};
+
+// ---- kernel launchers (skan_kernels.cu) ----
+void launch_locate_input(const double* x, int n_rows, int width, const DevLayer& L, int* bm,
+                         float* btf, double* btd, int* err, cudaStream_t s);
+void launch_gather_fast(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
+                        const float* btf, float* partial, cudaStream_t s);
+void launch_combine(const DevLayer& L, const LaunchCfg& c, int B, const float* partial,
+                    double* y, const DevLayer* next, int* bm, float* btf, double* btd, int* err,
+                    cudaStream_t s);
+void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
+                         const double* btd, double* y, cudaStream_t s);
+void launch_locate_raw(const double* x, int n, double lo, double hi, int G, int* idx,
+                       double* t, uint8_t* clamped, int* err, cudaStream_t s);
+void launch_pli_lookup(const double* cb, int k, int G, const int* rows, const double* g,
+                       const double* b, const double* x, double lo, double hi, int n, double* y,
+                       int* err, cudaStream_t s);
+void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint32_t* out,
+                           cudaStream_t s);
+
+// Record a thread-local error for skan_last_error and return its status.
+skan_status set_error(skan_status s, const std::string& msg, uint64_t offset, int fault);
+
+LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms);
+
+}  // namespace skan

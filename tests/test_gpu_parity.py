@@ -1,0 +1,380 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle.
+
+Bars (stated here and in DESIGN.md):
+  * knot selection, index unpack, gain/bias/codebook decode: bit-exact;
+  * SKAN_MODE_EXACT forward: bitwise equal to holoquant::compressed_forward;
+  * SKAN_MODE_FAST forward: |y - y_ref| <= 1e-5 * max(|y_ref|, sum_i |term_ij|)
+    per output (tests/helpers.py), and bitwise reproducible run to run.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2512_15742_b200 as hq
+from paper_2512_15742_b200 import synthetic
+
+from helpers import TOL, assert_close, l1_scale
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, np.float64).view(np.uint64)
+
+
+def _upload(tables):
+    return hq.upload([t.to_runtime() for t in tables], device=0)
+
+
+def _gpu_forward(model, x, batch, mode, max_batch=64):
+    ws = hq.make_workspace(model, max_batch=max_batch)
+    y = np.zeros(batch * model.output_dim())
+    hq.compressed_forward(model, x, batch, y, ws, mode=mode)
+    return y, ws
+
+
+# ---------------------------------------------------------------------------
+# knot selection (kan.cpp:28-58): bit-exact on >= 1e7 inputs incl. nodes
+
+def test_locate_bitexact_1e7(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(7)
+    total = 0
+    for G, (lo, hi) in [(10, (-1.0, 1.0)), (5, (-1.0, 1.0)), (2, (0.3, 0.7)), (128, (-2.5, 3.75)),
+                        (37, (-0.1, 1e-3)), (1000, (-7.0, 11.0))]:
+        n = 2_000_000
+        x = rng.uniform(lo - 0.5 * (hi - lo), hi + 0.5 * (hi - lo), n)
+        nodes = np.array([synthetic.node_position(lo, hi, G, i) for i in range(G)])
+        extra = np.concatenate([nodes, np.nextafter(nodes, -np.inf), np.nextafter(nodes, np.inf),
+                                [lo, hi, -0.0, 0.0, 1e300, -1e300]])
+        x = np.concatenate([x, np.tile(extra, 50)])
+        idx, t, cl = hq.locate(torch.from_numpy(x).cuda(), lo, hi, G)
+        wi, wt, wc, bad = oracle.port_locate_many(lo, hi, G, x)
+        assert bad == 0
+        assert np.array_equal(idx.cpu().numpy(), wi)
+        assert np.array_equal(_bits(t.cpu().numpy()), _bits(wt))
+        assert np.array_equal(cl.cpu().numpy(), wc)
+        total += x.size
+    assert total >= 10_000_000
+
+
+def test_locate_nonfinite_raises(torch_cuda):
+    torch = torch_cuda
+    x = torch.tensor([0.1, float("nan"), 0.3], dtype=torch.float64, device="cuda")
+    with pytest.raises(hq.ValueError):
+        hq.locate(x, -1.0, 1.0, 5)
+    x = torch.tensor([float("inf")], dtype=torch.float64, device="cuda")
+    with pytest.raises(hq.ValueError):
+        hq.locate(x, -1.0, 1.0, 5)
+
+
+# ---------------------------------------------------------------------------
+# forward, exact mode == reference bitwise
+
+def _fixture_models():
+    """Reference-test fixtures built by the reference itself (oracle/_ref)."""
+    ms = [("random_compressed f32", oracle.ref_random([3, 5, 2], 6, 0.4, 16, 5, False)),
+          ("random_compressed int8", oracle.ref_random([3, 5, 2], 6, 0.4, 16, 5, True)),
+          ("dense random_net", oracle.ref_random([2, 4, 1], 7, 0.4, 2, 0, False)),
+          ("zero-alloc fixture int8", oracle.ref_random([4, 24, 2], 12, 0.4, 95, 32, True)),
+          ("iso G=128", oracle.ref_random([2, 16, 1], 128, 0.4, 90, 16, False))]
+    for name, (i, o, G, k, s, q) in [("crafted K=65536 f32", (2, 3, 4, 65536, 5, False)),
+                                     ("crafted K=1", (2, 2, 3, 1, 6, False)),
+                                     ("crafted K=1 int8", (3, 2, 3, 1, 6, True)),
+                                     ("crafted K=65536 int8", (5, 40, 7, 65536, 5, True)),
+                                     ("crafted K=70000 int8 (u32 idx)", (7, 9, 5, 70000, 8, True)),
+                                     ("crafted K=70000 f32 (u32 idx)", (7, 9, 5, 70000, 8, False)),
+                                     ("cfg1 256x256 K=256 int8", (256, 256, 10, 256, 1, True)),
+                                     ("cfg1 256x256 K=256 f32", (256, 256, 10, 256, 1, False))]:
+        ms.append((name, oracle.ref_build(synthetic.CompressedNetwork([synthetic.crafted_layer(i, o, G, k, s,
+                                                                                                int8=q)]))))
+    return ms
+
+
+@pytest.mark.parametrize("batch", [1, 3, 17, 64])
+def test_exact_mode_bitwise_equals_reference(torch_cuda, batch):
+    rng = np.random.default_rng(100 + batch)
+    for name, m in _fixture_models():
+        tables = m.tables()
+        x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+        want, _ = m.forward(x, batch)
+        got, _ = _gpu_forward(_upload(tables), x, batch, "exact")
+        assert np.array_equal(_bits(got), _bits(want)), name
+
+
+def test_exact_mode_build_model_path(torch_cuda):
+    """build_model(CompressedNetwork) on the device == reference build_model + forward."""
+    for q in (False, True):
+        cn = synthetic.synthetic_head(dims=(40, 33, 6), k=300, grid=7, int8=q, seed=21)
+        x = synthetic.synthetic_inputs(9, 40, seed=2, grid=7)
+        want, _ = oracle.ref_build(cn).forward(x, 9)
+        got, _ = _gpu_forward(hq.build_model(cn), x, 9, "exact")
+        assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_exact_mode_mixed_dense_and_compressed(torch_cuda):
+    dense = oracle.ref_random([6, 5], 8, 0.4, 3, 0, False).tables()[0]
+    comp = oracle.ref_build(synthetic.CompressedNetwork([synthetic.crafted_layer(5, 4, 8, 12, 4, int8=True)])).tables()[0]
+    tables = [dense, comp]
+    x = np.random.default_rng(0).uniform(-1.5, 1.5, 11 * 6)
+    want, _ = oracle.port_forward(tables, x, 11)
+    got, _ = _gpu_forward(_upload(tables), x, 11, "exact")
+    assert np.array_equal(_bits(got), _bits(want))
+
+
+def test_exact_mode_headline_head_bitwise(torch_cuda):
+    """cfg2 head {2048,1408,20}, K=65536, G=10, int8 — bitwise at batch 2."""
+    cn = synthetic.synthetic_head()
+    tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
+    x = synthetic.synthetic_inputs(2, 2048, seed=9)
+    want, ops = oracle.port_forward(tables, x, 2)
+    got, ws = _gpu_forward(hq.build_model(cn), x, 2, "exact")
+    assert np.array_equal(_bits(got), _bits(want))
+    assert ws.interp_ops == ops == 2 * 2_911_744
+
+
+# ---------------------------------------------------------------------------
+# forward, fast mode within tolerance
+
+@pytest.mark.parametrize("batch", [1, 5, 64])
+def test_fast_mode_within_tolerance(torch_cuda, batch):
+    rng = np.random.default_rng(200 + batch)
+    for name, m in _fixture_models():
+        tables = m.tables()
+        x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+        want, _ = m.forward(x, batch)
+        got, _ = _gpu_forward(_upload(tables), x, batch, "fast")
+        assert_close(got, want, l1_scale(tables, x, batch))
+
+
+def test_fast_mode_headline_head(torch_cuda):
+    cn = synthetic.synthetic_head()
+    tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
+    model = hq.build_model(cn)
+    for batch in (1, 4):
+        x = synthetic.synthetic_inputs(batch, 2048, seed=30 + batch)
+        want, _ = oracle.port_forward(tables, x, batch)
+        got, _ = _gpu_forward(model, x, batch, "fast")
+        assert_close(got, want, l1_scale(tables, x, batch))
+
+
+def test_fast_mode_headline_head_batch256(torch_cuda):
+    """cfg3 shape: batch 256 (checked with a relative-to-L1 bound computed on
+    a 16-sample slice, the full batch against the multi-threaded oracle)."""
+    cn = synthetic.synthetic_head()
+    tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
+    x = synthetic.synthetic_inputs(256, 2048, seed=77)
+    want, _ = oracle.port_forward(tables, x, 256, threads=8)
+    got, ws = _gpu_forward(hq.build_model(cn), x, 256, "fast", max_batch=256)
+    scale = l1_scale(tables, x[:16 * 2048], 16)
+    assert_close(got[:16 * 20], want[:16 * 20], scale)
+    # whole batch: relative to the head's typical L1 scale
+    assert np.max(np.abs(got - want)) <= TOL * np.median(scale)
+
+
+def test_fast_mode_bitwise_reproducible(torch_cuda):
+    cn = synthetic.synthetic_head(dims=(512, 300, 20), k=4096, grid=10, int8=True, seed=5)
+    model = hq.build_model(cn)
+    x = synthetic.synthetic_inputs(33, 512, seed=6)
+    a, _ = _gpu_forward(model, x, 33, "fast")
+    b, _ = _gpu_forward(model, x, 33, "fast")
+    c, _ = _gpu_forward(model, x, 33, "fast")
+    assert np.array_equal(_bits(a), _bits(b)) and np.array_equal(_bits(a), _bits(c))
+
+
+def test_batch_larger_than_workspace_is_chunked(torch_cuda):
+    cn = synthetic.synthetic_head(dims=(64, 48, 5), k=256, grid=10, int8=True, seed=3)
+    model = hq.build_model(cn)
+    x = synthetic.synthetic_inputs(50, 64, seed=8)
+    a, _ = _gpu_forward(model, x, 50, "exact", max_batch=7)
+    b, _ = _gpu_forward(model, x, 50, "exact", max_batch=64)
+    assert np.array_equal(_bits(a), _bits(b))
+
+
+# ---------------------------------------------------------------------------
+# SKAN v1 files -> device heads
+
+def test_skan_files_load_and_forward_bitwise(torch_cuda):
+    rng = np.random.default_rng(42)
+    for name, m in _fixture_models():
+        data = m.serialize()
+        model = hq.deserialize(data)
+        tables = m.tables()
+        x = rng.uniform(-1.5, 1.5, 5 * tables[0].in_dim)
+        want, _ = m.forward(x, 5)
+        got, _ = _gpu_forward(model, x, 5, "exact")
+        assert np.array_equal(_bits(got), _bits(want)), name
+        assert [h.k for h in model.layers] == [t.k for t in tables]
+
+
+def test_load_model_from_disk(torch_cuda, tmp_path):
+    m = oracle.ref_random([3, 5, 2], 6, 0.4, 21, 4, True)
+    p = tmp_path / "head.skan"
+    p.write_bytes(m.serialize())
+    model = hq.load_model(str(p))
+    x = np.linspace(-1.2, 1.2, 3 * 4)
+    want, _ = m.forward(x, 4)
+    got, _ = _gpu_forward(model, x, 4, "exact")
+    assert np.array_equal(got, want)
+
+
+# ---------------------------------------------------------------------------
+# API contract (lutham.cpp:819-850, test_lutham.cpp:394-424)
+
+def test_interp_ops_counts_edges_times_batch_independent_of_G(torch_cuda):
+    for G in (5, 64):
+        m = oracle.ref_random([2, 4, 1], G, 0.4, 18, 3, False)
+        model = _upload(m.tables())
+        ws = hq.make_workspace(model)
+        x = np.full(7 * 2, 0.25)
+        y = np.zeros(7)
+        hq.compressed_forward(model, x, 7, y, ws)
+        assert ws.interp_ops == 7 * (2 * 4 + 4 * 1)
+        hq.compressed_forward(model, x, 7, y, ws, mode="exact")
+        assert ws.interp_ops == 2 * 7 * 12
+
+
+def test_forward_validates_spans_and_workspace(torch_cuda):
+    big = _upload(oracle.ref_random([2, 9, 1], 4, 0.4, 19, 0, False).tables())
+    small = _upload(oracle.ref_random([2, 3, 1], 4, 0.4, 19, 0, False).tables())
+    ws = hq.make_workspace(small)
+    assert ws.width() == 3
+    x, y = np.zeros(2), np.zeros(1)
+    with pytest.raises(hq.ContractError):
+        hq.compressed_forward(big, x, 1, y, ws)
+    ok = hq.make_workspace(big)
+    assert ok.width() == 9
+    with pytest.raises(hq.ShapeError):
+        hq.compressed_forward(big, np.zeros(1), 1, y, ok)
+    with pytest.raises(hq.ShapeError):
+        hq.compressed_forward(big, x, 1, np.zeros(0), ok)
+    with pytest.raises(hq.ShapeError):
+        hq.compressed_forward(big, x, -1, y, ok)
+    hq.compressed_forward(big, np.zeros(0), 0, np.zeros(0), ok)  # batch 0: no work
+    assert ok.interp_ops == 0
+
+
+def test_nonfinite_input_raises_value_error(torch_cuda):
+    torch = torch_cuda
+    model = _upload(oracle.ref_random([3, 5, 2], 6, 0.4, 16, 5, True).tables())
+    ws = hq.make_workspace(model)
+    for bad in (float("nan"), float("inf"), -float("inf")):
+        x = np.array([0.1, bad, 0.2])
+        for mode in ("fast", "exact"):
+            with pytest.raises(hq.ValueError):
+                hq.compressed_forward(model, x, 1, np.zeros(2), ws, mode=mode)
+    xd = torch.tensor([0.1, float("nan"), 0.2], dtype=torch.float64, device="cuda")
+    yd = torch.zeros(2, dtype=torch.float64, device="cuda")
+    with pytest.raises(hq.ValueError):
+        hq.compressed_forward(model, xd, 1, yd, ws)
+    # the workspace stays usable afterwards
+    y = np.zeros(2)
+    hq.compressed_forward(model, np.array([0.1, 0.2, 0.3]), 1, y, ws)
+
+
+def test_build_model_rejects_inconsistent_layers(torch_cuda):
+    """test_lutham.cpp:277-286."""
+    cl = synthetic.crafted_layer(2, 2, 3, 4, 11)
+    cl.indices = cl.indices.copy(); cl.indices[0] = 4
+    with pytest.raises(hq.ContractError):
+        hq.build_model(synthetic.CompressedNetwork([cl]))
+    cl = synthetic.crafted_layer(2, 2, 3, 4, 11)
+    cl.gains = cl.gains[:-1]
+    with pytest.raises(hq.ContractError):
+        hq.build_model(synthetic.CompressedNetwork([cl]))
+    cl = synthetic.crafted_layer(2, 2, 3, 4, 11)
+    cl.gains = cl.gains.copy(); cl.gains[0] = -0.5
+    with pytest.raises(hq.ContractError):
+        hq.build_model(synthetic.CompressedNetwork([cl]))
+    with pytest.raises(hq.ShapeError):
+        hq.build_model(synthetic.CompressedNetwork([]))
+
+
+def test_device_tensor_forward_matches_host_forward(torch_cuda):
+    torch = torch_cuda
+    cn = synthetic.synthetic_head(dims=(128, 96, 10), k=1024, grid=10, int8=True, seed=12)
+    model = hq.build_model(cn)
+    ws = hq.make_workspace(model, 32)
+    x = synthetic.synthetic_inputs(32, 128, seed=1)
+    y = np.zeros(32 * 10)
+    hq.compressed_forward(model, x, 32, y, ws, mode="exact")
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.zeros(320, dtype=torch.float64, device="cuda")
+    hq.compressed_forward(model, xd, 32, yd, ws, mode="exact")
+    assert np.array_equal(yd.cpu().numpy(), y)
+
+
+def test_multi_head_forward_equals_single_heads(torch_cuda):
+    torch = torch_cuda
+    heads = [hq.build_model(synthetic.synthetic_head(dims=(64, 40, 5), k=512, grid=10, int8=True, seed=s))
+             for s in range(4)]
+    wss = [hq.make_workspace(h, 16) for h in heads]
+    x = synthetic.synthetic_inputs(16, 64, seed=3)
+    xd = torch.from_numpy(x).cuda()
+    ys = [torch.zeros(16 * 5, dtype=torch.float64, device="cuda") for _ in heads]
+    hq.forward_multi(heads, wss, xd, 16, ys, mode="exact")
+    torch.cuda.synchronize()
+    for h, y in zip(heads, ys):
+        want = np.zeros(80)
+        hq.compressed_forward(h, x, 16, want, hq.make_workspace(h, 16), mode="exact")
+        assert np.array_equal(y.cpu().numpy(), want)
+
+
+def test_l2_persistence_window(torch_cuda):
+    torch = torch_cuda
+    model = hq.build_model(synthetic.synthetic_head(dims=(64, 40, 5), k=512, grid=10, int8=True, seed=1))
+    s = torch.cuda.Stream()
+    model.set_l2_persist(s.cuda_stream, 1.0)
+    model.set_l2_persist(s.cuda_stream, 0.0)
+
+
+# ---------------------------------------------------------------------------
+# primitives
+
+def test_pli_lookup_matches_reference(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(14)
+    k, G, lo, hi = 6, 7, -1.0, 1.0
+    cb = rng.uniform(-1, 1, k * G)
+    n = 5000
+    rows = rng.integers(0, k, n).astype(np.int32)
+    g = rng.uniform(0, 2, n)
+    b = rng.uniform(-1, 1, n)
+    x = rng.uniform(-1.3, 1.3, n)
+    y = hq.pli_lookup(torch.from_numpy(cb).cuda(), torch.from_numpy(rows).cuda(), torch.from_numpy(g).cuda(),
+                      torch.from_numpy(b).cuda(), torch.from_numpy(x).cuda(), lo, hi, G).cpu().numpy()
+    for q in range(0, n, 7):
+        want = C.c_double()
+        assert oracle.ref().hqref_pli_lookup(cb.ctypes.data, k, G, int(rows[q]), g[q], b[q], x[q], lo, hi,
+                                             C.byref(want)) == 0
+        assert y[q] == want.value
+    bad = torch.from_numpy(np.array([k], np.int32)).cuda()
+    with pytest.raises(hq.ShapeError):
+        hq.pli_lookup(torch.from_numpy(cb).cuda(), bad, torch.ones(1, dtype=torch.float64, device="cuda"),
+                      torch.zeros(1, dtype=torch.float64, device="cuda"),
+                      torch.zeros(1, dtype=torch.float64, device="cuda"), lo, hi, G)
+
+
+def test_unpack_indices_bitexact(torch_cuda):
+    torch = torch_cuda
+    rng = np.random.default_rng(20)
+    for bits in range(1, 33):
+        for count in (1, 3, 100, 4097):
+            vals = rng.integers(0, 2 ** bits, size=count, dtype=np.uint64).astype(np.uint32)
+            n = oracle.ref().hqref_pack_indices(vals.ctypes.data, vals.size, bits, None, 0)
+            buf = np.zeros(n, np.uint8)
+            oracle.ref().hqref_pack_indices(vals.ctypes.data, vals.size, bits, buf.ctypes.data, n)
+            got = hq.unpack_indices(torch.from_numpy(buf).cuda(), count, bits).cpu().numpy().view(np.uint32)
+            assert np.array_equal(got, vals), (bits, count)
+    # KAT test_lutham.cpp:39-40
+    got = hq.unpack_indices(torch.tensor([0xff, 0x03, 0x10, 0x20], dtype=torch.uint8, device="cuda"), 3, 10)
+    assert got.cpu().tolist() == [1023, 0, 513]
