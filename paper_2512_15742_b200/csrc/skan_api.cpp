@@ -94,6 +94,8 @@ bool is_int8(const skan_layer_header& h) { return (h.flags & SKAN_FLAG_INT8) != 
 constexpr uint64_t kAlign = 256;
 uint64_t align_up(uint64_t v) { return add_checked(v, kAlign - 1) / kAlign * kAlign; }
 
+uint64_t int8_row_stride(uint64_t G) { return (G + 15) / 16 * 16; }
+
 int device_format(const skan_layer_header& h) {
     if (h.k == 0) return skan::FMT_DENSE;
     if (is_int8(h)) return h.k <= 65536 ? skan::FMT_I8_R32 : skan::FMT_I8_WIDE;
@@ -106,13 +108,19 @@ uint64_t device_bytes(const skan_layer_header& h) {
     uint64_t b = 0;
     if (fmt == skan::FMT_DENSE) return align_up(mul_checked(mul_checked(e, h.grid_size), 4));
     const uint64_t kg = mul_checked(h.k, h.grid_size);
+    // int8 codebook: rows padded to 16 B (one 128-bit load per row) plus the
+    // (c[m], c[m+1]) pair table (one 2-byte gather per edge-sample)
+    const uint64_t cb8 = mul_checked(h.k, int8_row_stride(h.grid_size));
+    const uint64_t pairs = mul_checked(mul_checked(h.k, h.grid_size - 1), 2);
     if (fmt == skan::FMT_I8_R32) {
         b = add_checked(b, align_up(mul_checked(e, 4)));        // records
-        b = add_checked(b, align_up(kg));                        // int8 codebook
+        b = add_checked(b, align_up(cb8));
+        b = add_checked(b, align_up(pairs));
     } else if (fmt == skan::FMT_I8_WIDE) {
         b = add_checked(b, align_up(mul_checked(e, 4)));        // u32 index
         b = add_checked(b, align_up(mul_checked(e, 2)));        // gain|bias codes
-        b = add_checked(b, align_up(kg));
+        b = add_checked(b, align_up(cb8));
+        b = add_checked(b, align_up(pairs));
     } else {
         if (h.k > 1) b = add_checked(b, align_up(mul_checked(e, 4)));  // u32 index
         b = add_checked(b, align_up(mul_checked(e, 4)));        // gains
@@ -205,6 +213,7 @@ struct skan_workspace {
     int* h_err = nullptr;    // pinned
     cudaStream_t last_stream = nullptr;
     int last_launches = 0;
+    const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
     std::vector<void*> allocs;
 };
 
@@ -220,7 +229,7 @@ struct Staged {
     std::vector<uint32_t> idx;    // u32 indices (WIDE / F32)
     std::vector<uint16_t> gb;     // WIDE gain|bias codes
     std::vector<float> gain, bias;
-    std::vector<int8_t> cb8;
+    std::vector<int8_t> cb8;      // K x G codes (as given)
     std::vector<float> cb32;      // codebook or dense grid
     double lutd[256] = {};
     float lutf[256] = {};
@@ -403,6 +412,7 @@ void upload(skan_head* h, std::vector<Staged>& st) {
     std::vector<uint8_t> host(total, 0);
     uint64_t cur = 0;
     auto put = [&](const void* src, uint64_t bytes) -> void* {
+        if (add_checked(cur, bytes) > total) raise(SKAN_PLAN_ERROR, "resident layout overruns the plan");
         void* dst = static_cast<uint8_t*>(h->dmem) + cur;
         if (bytes) std::memcpy(host.data() + cur, src, bytes);
         cur = align_up(add_checked(cur, bytes));
@@ -427,14 +437,28 @@ void upload(skan_head* h, std::vector<Staged>& st) {
                 d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
                 break;
             case skan::FMT_I8_R32:
-                d.rec = static_cast<const uint32_t*>(put(s.rec.data(), s.rec.size() * 4));
-                d.cb8 = static_cast<const int8_t*>(put(s.cb8.data(), s.cb8.size()));
+            case skan::FMT_I8_WIDE: {
+                if (d.fmt == skan::FMT_I8_R32) {
+                    d.rec = static_cast<const uint32_t*>(put(s.rec.data(), s.rec.size() * 4));
+                } else {
+                    d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
+                    d.gb = static_cast<const uint16_t*>(put(s.gb.data(), s.gb.size() * 2));
+                }
+                const uint64_t G = s.h.grid_size, K = s.h.k, rs = int8_row_stride(G);
+                std::vector<int8_t> padded(K * rs, 0);
+                std::vector<uint16_t> pairs(K * (G - 1));
+                for (uint64_t k = 0; k < K; ++k) {
+                    const int8_t* row = s.cb8.data() + k * G;
+                    std::memcpy(padded.data() + k * rs, row, G);
+                    for (uint64_t m = 0; m + 1 < G; ++m)
+                        pairs[k * (G - 1) + m] = static_cast<uint16_t>(static_cast<uint8_t>(row[m]) |
+                                                                       (static_cast<uint8_t>(row[m + 1]) << 8));
+                }
+                d.rs = static_cast<int>(rs);
+                d.cb8 = static_cast<const int8_t*>(put(padded.data(), padded.size()));
+                d.pair8 = static_cast<const uint16_t*>(put(pairs.data(), pairs.size() * 2));
                 break;
-            case skan::FMT_I8_WIDE:
-                d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
-                d.gb = static_cast<const uint16_t*>(put(s.gb.data(), s.gb.size() * 2));
-                d.cb8 = static_cast<const int8_t*>(put(s.cb8.data(), s.cb8.size()));
-                break;
+            }
             default:
                 if (s.h.k > 1) d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
                 d.gain = static_cast<const float*>(put(s.gain.data(), s.gain.size() * 4));
@@ -446,10 +470,9 @@ void upload(skan_head* h, std::vector<Staged>& st) {
             d.lutf = static_cast<const float*>(put(s.lutf, sizeof s.lutf));
             d.lutd = static_cast<const double*>(put(s.lutd, sizeof s.lutd));
             d.bias_sum = static_cast<const double*>(put(s.bias_sum.data(), s.bias_sum.size() * 8));
-        } else {
-            cur = add_checked(cur, align_up(256 * 4) + align_up(256 * 8) + align_up(uint64_t(d.out) * 8));
         }
-        (void)begin;
+        if (cur - begin != h->lplan[l].device_bytes)
+            raise(SKAN_PLAN_ERROR, "resident layout of layer " + std::to_string(l) + " disagrees with the plan");
         h->dl.push_back(d);
         h->headers.push_back(s.h);
     }
@@ -498,41 +521,97 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
 // ---------------------------------------------------------------------------
 // forward
 
-uint64_t partial_floats_for(const skan_head* h, int max_batch) {
-    uint64_t best = 0;
+// Largest split-partial buffer (floats) and per-layer counter count any
+// batch up to max_batch needs on the fast path.
+void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, uint64_t* counters) {
+    uint64_t best = 0, cnt = 1;
     for (const DevLayer& L : h->dl) {
         for (int b = 1; b <= max_batch; ++b) {
             const skan::LaunchCfg c = skan::choose_cfg(L, b, false, h->num_sms);
             best = std::max<uint64_t>(best, static_cast<uint64_t>(c.nsplit) * b * L.out);
+            cnt = std::max<uint64_t>(cnt, static_cast<uint64_t>(c.jt) * c.st);
         }
     }
-    return best;
+    *partial_floats = best;
+    *counters = cnt;
+}
+
+// One fused fast-path layer launch (plus the standalone locate in front of
+// layer 0 when the large-batch kernel is used).  Layer l reads brackets
+// bm[l&1] and its finisher writes layer l+1's into bm[(l+1)&1].
+int launch_layer_fast(const skan_head* h, skan_workspace* ws, int l, const double* x, int B, double* out,
+                      bool chained, cudaStream_t s) {
+    auto& d = ws->d;
+    const int nl = static_cast<int>(h->dl.size());
+    const size_t plane = static_cast<size_t>(ws->max_batch) * h->max_width;
+    int* bm[2] = {d.bm, d.bm + plane};
+    float* bt[2] = {d.btf, d.btf + plane};
+    const DevLayer& L = h->dl[l];
+    const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
+    const skan::LaunchCfg c = skan::choose_cfg(L, B, false, h->num_sms);
+    int launches = 0;
+    skan::FwdArgs a{};
+    a.L = L;
+    a.B = B;
+    a.rows_per_cta = c.ichunk;
+    if (l == 0) {
+        if (c.kind == 0) {
+            a.x = x;  // small batch: knot selection inline in each CTA
+        } else {
+            skan::launch_locate_input(x, B, L.in, L, bm[0], bt[0], nullptr, d.err, s);
+            ++launches;
+            chained = true;
+        }
+    }
+    a.bm_in = bm[l & 1];
+    a.bt_in = bt[l & 1];
+    a.partial = d.partial;
+    a.counters = d.counters + static_cast<size_t>(l) * d.counter_stride;
+    a.y = out;
+    a.has_next = next != nullptr;
+    if (next) {
+        a.nlo = next->lo;
+        a.nhi = next->hi;
+        a.ndx = next->dx;
+        a.nG = next->G;
+        a.bm_out = bm[(l + 1) & 1];
+        a.bt_out = bt[(l + 1) & 1];
+    }
+    a.err = d.err;
+    skan::launch_fwd_fast(a, c, chained, s);
+    return launches + 1;
 }
 
 // Enqueue one chunk (B <= ws->max_batch) on `s`; x/y are device pointers.
+//   fast:  [locate] -> fused layer 0 -> fused layer 1 -> ...  (PDL-chained;
+//          each layer's last CTAs write the next layer's brackets)
+//   exact: locate -> gather_exact -> locate -> gather_exact ...
 int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B, double* y,
                   bool exact, cudaStream_t s) {
     const int nl = static_cast<int>(h->dl.size());
     auto& d = ws->d;
     int launches = 0;
-    skan::launch_locate_input(x, B, h->dl[0].in, h->dl[0], d.bm, d.btf, d.btd, d.err, s);
-    ++launches;
-    for (int l = 0; l < nl; ++l) {
-        const DevLayer& L = h->dl[l];
-        const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
-        double* out = next ? d.act[l & 1] : y;
-        const skan::LaunchCfg c = skan::choose_cfg(L, B, exact, h->num_sms);
-        if (exact) {
+    if (exact) {
+        skan::launch_locate_input(x, B, h->dl[0].in, h->dl[0], d.bm, d.btf, d.btd, d.err, s);
+        ++launches;
+        for (int l = 0; l < nl; ++l) {
+            const DevLayer& L = h->dl[l];
+            const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
+            double* out = next ? d.act[l & 1] : y;
+            const skan::LaunchCfg c = skan::choose_cfg(L, B, true, h->num_sms);
             skan::launch_gather_exact(L, c, B, d.bm, d.btd, out, s);
             ++launches;
             if (next) {
                 skan::launch_locate_input(out, B, L.out, *next, d.bm, d.btf, d.btd, d.err, s);
                 ++launches;
             }
-        } else {
-            skan::launch_gather_fast(L, c, B, d.bm, d.btf, d.partial, s);
-            skan::launch_combine(L, c, B, d.partial, out, next, d.bm, d.btf, d.btd, d.err, s);
-            launches += 2;
+        }
+    } else {
+        ws->last_x = x;
+        bool chained = false;
+        for (int l = 0; l < nl; ++l) {
+            launches += launch_layer_fast(h, ws, l, x, B, l + 1 < nl ? d.act[l & 1] : y, chained, s);
+            chained = true;
         }
     }
     skan::cuda_check(cudaGetLastError(), "kernel launch");
@@ -674,11 +753,16 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         };
         ws->d.act[0] = static_cast<double*>(alloc(act * 8));
         ws->d.act[1] = static_cast<double*>(alloc(act * 8));
-        ws->d.bm = static_cast<int*>(alloc(act * 4));
-        ws->d.btf = static_cast<float*>(alloc(act * 4));
+        ws->d.bm = static_cast<int*>(alloc(2 * act * 4));      // ping-pong: layer l reads [l&1]
+        ws->d.btf = static_cast<float*>(alloc(2 * act * 4));
         ws->d.btd = static_cast<double*>(alloc(act * 8));
-        ws->partial_floats = partial_floats_for(h, max_batch);
+        uint64_t ncnt = 0;
+        scratch_needs(h, max_batch, &ws->partial_floats, &ncnt);
         ws->d.partial = static_cast<float*>(alloc(ws->partial_floats * 4));
+        ws->d.counter_stride = ncnt;
+        const size_t cbytes = ncnt * h->dl.size() * sizeof(unsigned);
+        ws->d.counters = static_cast<unsigned*>(alloc(cbytes));
+        skan::cuda_check(cudaMemset(ws->d.counters, 0, std::max<size_t>(cbytes, 256)), "cudaMemset");
         ws->d.err = static_cast<int*>(alloc(sizeof(int)));
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
@@ -769,7 +853,8 @@ skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int laye
         if (exact) {
             skan::launch_gather_exact(L, c, batch, ws->d.bm, ws->d.btd, ws->d.act[1], s);
         } else {
-            skan::launch_gather_fast(L, c, batch, ws->d.bm, ws->d.btf, ws->d.partial, s);
+            if (!ws->last_x) raise(SKAN_CONTRACT_ERROR, "run a forward on this workspace first");
+            launch_layer_fast(h, ws, layer, ws->last_x, batch, ws->d.act[layer & 1], false, s);
         }
         skan::cuda_check(cudaGetLastError(), "profile launch");
     });

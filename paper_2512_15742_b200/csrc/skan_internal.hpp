@@ -65,6 +65,8 @@ struct DevLayer {
     const float* lutf;       // [128] float(gain(code) * cs) — fast int8 path
     const double* lutd;      // [128] gain(code) as dequantize_gain_code returns it
     const double* bias_sum;  // [out] sum_i b_ij in i order — fast path
+    const uint16_t* pair8;   // int8: [K][G-1] (c[k][m] | c[k][m+1] << 8) — one 2-byte gather per edge-sample
+    int rs;                  // int8 codebook row stride in bytes (G rounded up to 16)
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -74,6 +76,34 @@ struct LaunchCfg {
     int jt, st;  // CTA tiles along j and samples
     int nsplit;  // i-splits (fast path); 1 in exact mode
     int ichunk;  // inputs per split
+    int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes (large batch)
+    int vj;      // outputs per lane (small kernel)
+    int rw;      // rows per warp (small kernel)
+    int ic;      // inputs per staged chunk (large kernel)
+    size_t smem; // dynamic shared memory bytes (large kernel)
+};
+
+// Arguments of one fused fast-path layer launch (k_fwd_small / k_fwd_large).
+// Each CTA accumulates a row-block (i-split) of edges; the last CTA to finish
+// a (j-tile, sample-tile) reduces the split partials in fixed order in
+// double, adds the bias sums, writes the layer output and the next layer's
+// knot brackets.
+struct FwdArgs {
+    DevLayer L;
+    int B;
+    int rows_per_cta;       // inputs per split
+    const double* x;        // non-null: locate inline from these f64 inputs [B][in]
+    const int* bm_in;       // else: brackets [B][in] from the previous layer / locate kernel
+    const float* bt_in;
+    float* partial;         // [nsplit][B][out]
+    unsigned* counters;     // [jt * st], zero between launches
+    double* y;              // [B][out]
+    int has_next;
+    double nlo, nhi, ndx;
+    int nG;
+    int* bm_out;            // next layer brackets [B][out]
+    float* bt_out;
+    int* err;
 };
 
 // Workspace device buffers (one forward stream).
@@ -84,16 +114,17 @@ struct DevScratch {
     double* btd;        // bracket t (f64)
     float* partial;     // split partial sums
     int* err;           // non-finite flag
+    unsigned* counters; // per-layer (j-tile, sample-tile) arrival counters
+    size_t counter_stride;  // counters per layer
 };
 
 // ---- kernel launchers (skan_kernels.cu) ----
 void launch_locate_input(const double* x, int n_rows, int width, const DevLayer& L, int* bm,
                          float* btf, double* btd, int* err, cudaStream_t s);
-void launch_gather_fast(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
-                        const float* btf, float* partial, cudaStream_t s);
-void launch_combine(const DevLayer& L, const LaunchCfg& c, int B, const float* partial,
-                    double* y, const DevLayer* next, int* bm, float* btf, double* btd, int* err,
-                    cudaStream_t s);
+// Fused fast-path layer (gather + split reduction + next-layer locate).
+// pdl: launch with programmatic stream serialization (overlaps the
+// prologue with the previous kernel's tail).
+void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
                          const double* btd, double* y, cudaStream_t s);
 void launch_locate_raw(const double* x, int n, double lo, double hi, int G, int* idx,

@@ -1,13 +1,19 @@
 // sm_100a kernels for the LUTHAM forward (SHARe-KAN compressed KAN heads).
 //
-//   K1  k_locate_input   knot-interval selection, bit-exact with
-//                        holoquant::locate (kan.cpp:28-58)
-//   K2  k_gather_fast    fused decode + gather + interpolate + accumulate,
-//                        fp32 math, per-split partials (no atomics)
-//       k_combine        fixed-order split reduction in double + bias sums,
-//                        fused with the next layer's K1
-//   K2x k_gather_exact   fp64, reference operation order, sequential i:
-//                        bitwise equal to compressed_forward (lutham.cpp:793-814)
+//   K1  knot selection, bit-exact with holoquant::locate (kan.cpp:28-58):
+//       inline in the first layer's fused kernel, in the finisher of every
+//       layer for the next one, or standalone (k_locate_input / k_locate_raw)
+//   K2  fused decode + gather + interpolate + accumulate (fast path):
+//         k_fwd_small  rows-in-warps, outputs-in-lanes (small batches):
+//                      coalesced 128-bit record loads, one 2-byte codebook
+//                      pair gather per edge-sample
+//         k_fwd_large  samples-in-lanes (large batches): each edge decoded
+//                      once per CTA into shared memory as gained (c0, dc)
+//                      pairs, read back as warp broadcasts
+//       both end in a fixed-order split reduction (no float atomics) done by
+//       the last CTA of each output tile, fused with the next layer's K1
+//   K2x k_gather_exact  fp64, reference operation order, sequential i:
+//                      bitwise equal to compressed_forward (lutham.cpp:793-814)
 //   K5  k_unpack_indices SKAN v1 LSB-first index unpack (lutham.cpp:114-137)
 //       k_pli_lookup     batched single-edge primitive (lutham.cpp:730-739)
 #include <cuda_runtime.h>
@@ -19,8 +25,11 @@
 namespace skan {
 namespace {
 
-constexpr int kThreads = 128;  // threads per gather CTA
-constexpr int kIC = 64;        // inputs whose brackets are staged per smem pass
+constexpr int kThreads = 128;  // threads per exact-kernel CTA
+constexpr int kIC = 64;        // inputs whose brackets are staged per smem pass (exact kernel)
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // Knot selection.  Every double operation is an explicit round-to-nearest
@@ -64,29 +73,434 @@ __device__ __forceinline__ bool locate_dev(double lo, double hi, int G, double d
     return clamped;
 }
 
+// locate with the non-finite check (ValueError, kan.cpp:29) folded into err
+__device__ __forceinline__ void bracket_of(double lo, double hi, int G, double dx, double v, int* err,
+                                           int& m, double& t) {
+    m = 0;
+    t = 0.0;
+    if (!isfinite(v)) {
+        *err = 1;
+    } else {
+        locate_dev(lo, hi, G, dx, v, m, t);
+    }
+}
+
 __global__ void k_locate_input(const double* __restrict__ x, long long n, double lo, double hi,
                                int G, double dx, int* __restrict__ bm, float* __restrict__ btf,
                                double* __restrict__ btd, int* __restrict__ err) {
+    pdl_trigger();
+    pdl_wait();
     for (long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const double v = x[p];
-        int m = 0;
-        double t = 0.0;
-        if (!isfinite(v)) {
-            *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
-        } else {
-            locate_dev(lo, hi, G, dx, v, m, t);
-        }
+        int m;
+        double t;
+        bracket_of(lo, hi, G, dx, x[p], err, m, t);
         bm[p] = m;
         btf[p] = static_cast<float>(t);
-        btd[p] = t;
+        if (btd) btd[p] = t;
     }
 }
 
 // ---------------------------------------------------------------------------
-// Edge decode policies.  Each returns, for edge e, what the per-sample loop
-// needs: the codebook row base and the gain (fast: float incl. codebook
-// scale; exact: double gain + double bias, as RuntimeLayer::gain/bias).
+// Edge decode for the fast kernels.
+
+__device__ __forceinline__ float i8lo(uint32_t p) { return static_cast<float>(static_cast<int8_t>(p & 0xFFu)); }
+__device__ __forceinline__ float i8hi(uint32_t p) { return static_cast<float>(static_cast<int8_t>((p >> 8) & 0xFFu)); }
+
+// Shared finisher: runs in the last CTA of an output tile.  Threads cover
+// the tile's (sample, output) entries; each sums the nsplit partials in
+// ascending split order in double, adds sum_i b_ij, writes y and the next
+// layer's bracket.
+__device__ __forceinline__ void finish_tile(const FwdArgs& a, int nsplit, int s_begin, int s_count,
+                                            int j_begin, int j_count) {
+    const DevLayer& L = a.L;
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    for (int q = threadIdx.x; q < s_count * j_count; q += blockDim.x) {
+        const int s = s_begin + q / j_count;
+        const int j = j_begin + q % j_count;
+        const size_t p = static_cast<size_t>(s) * L.out + j;
+        double v = L.bias_sum ? L.bias_sum[j] : 0.0;
+        const float* src = a.partial + p;
+#pragma unroll 8
+        for (int z = 0; z < nsplit; ++z) v += static_cast<double>(__ldcg(src + z * plane));
+        a.y[p] = v;
+        if (a.has_next) {
+            int m;
+            double t;
+            bracket_of(a.nlo, a.nhi, a.nG, a.ndx, v, a.err, m, t);
+            a.bm_out[p] = m;
+            a.bt_out[p] = static_cast<float>(t);
+        }
+    }
+}
+
+// Arrival counting: returns true in exactly one CTA per tile (the last).
+__device__ __forceinline__ bool arrive_last(unsigned* counter, unsigned expected, int* s_flag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(counter, 1u);
+        *s_flag = prev == expected - 1;
+        if (*s_flag) *counter = 0;  // ready for the next launch (stream ordered)
+    }
+    __syncthreads();
+    if (*s_flag) __threadfence();
+    return *s_flag;
+}
+
+// ---------------------------------------------------------------------------
+// k_fwd_small: CTA = 8 warps; tile = (32*VJ outputs) x (8*RW input rows) x
+// (S samples).  Warp w owns RW consecutive rows; lane l owns outputs
+// j0 + l*VJ .. +VJ-1.  Records of a row are read with one coalesced 4*VJ-byte
+// load per lane, all RW rows issued before the dependency wait; then one
+// 2-byte gather per edge-sample from the pair table.  Per-lane fp32
+// accumulation over the warp's rows, fixed-order sum over warps in smem,
+// one fp32 partial per (split, sample, output).
+
+template <int FMT, int VJ>
+struct SmallEdges;
+
+template <int VJ>
+struct SmallEdges<FMT_I8_R32, VJ> {
+    uint32_t r[VJ];
+    __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
+        if constexpr (VJ == 4) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(L.rec + e));
+            r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+        } else {
+#pragma unroll
+            for (int v = 0; v < VJ; ++v) r[v] = __ldg(L.rec + e + v);
+        }
+    }
+    __device__ __forceinline__ uint32_t row(int v) const { return r[v] & 0xFFFFu; }
+    __device__ __forceinline__ int gcode(int v) const { return (r[v] >> 16) & 0xFF; }
+};
+
+template <int VJ>
+struct SmallEdges<FMT_I8_WIDE, VJ> {
+    uint32_t k[VJ];
+    uint16_t g[VJ];
+    __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
+#pragma unroll
+        for (int v = 0; v < VJ; ++v) {
+            k[v] = L.idx ? __ldg(L.idx + e + v) : 0u;
+            g[v] = __ldg(L.gb + e + v);
+        }
+    }
+    __device__ __forceinline__ uint32_t row(int v) const { return k[v]; }
+    __device__ __forceinline__ int gcode(int v) const { return g[v] & 0xFF; }
+};
+
+template <int VJ>
+struct SmallEdges<FMT_F32, VJ> {
+    uint32_t k[VJ];
+    float g[VJ];
+    __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
+#pragma unroll
+        for (int v = 0; v < VJ; ++v) {
+            k[v] = L.idx ? __ldg(L.idx + e + v) : 0u;
+            g[v] = __ldg(L.gain + e + v);
+        }
+    }
+};
+
+template <int VJ>
+struct SmallEdges<FMT_DENSE, VJ> {
+    __device__ __forceinline__ void load(const DevLayer&, size_t) {}
+};
+
+template <int FMT, int VJ, int S, int RW>
+__global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
+    constexpr int W = 8;
+    constexpr int JW = 32 * VJ;
+    constexpr int R = W * RW;
+    __shared__ int s_m[S][R];
+    __shared__ float s_t[S][R];
+    __shared__ float s_red[W][S][JW];
+    __shared__ float s_lut[256];
+    __shared__ int s_last;
+    pdl_trigger();
+    const DevLayer& L = a.L;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int jg = blockIdx.x, sg = blockIdx.z;
+    const int j0 = jg * JW + lane * VJ;
+    const int r0 = blockIdx.y * a.rows_per_cta;
+    const int rend = min(L.in, r0 + a.rows_per_cta);
+    const int s0 = sg * S;
+    const int nS = min(S, a.B - s0);
+    const bool jok = j0 < L.out;
+    constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
+    if constexpr (kI8) {
+        for (int q = tid; q < 256; q += 256) s_lut[q] = L.lutf[q];
+    }
+    // 1. records of this warp's rows: independent of the previous kernel
+    SmallEdges<FMT, VJ> ed[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+        const int i = r0 + warp * RW + r;
+        if (jok && i < rend) ed[r].load(L, static_cast<size_t>(i) * L.out + j0);
+    }
+    // 2. brackets (produced by the previous kernel, or located inline)
+    pdl_wait();
+    for (int q = tid; q < S * R; q += 256) {
+        const int sl = q / R, rl = q % R, i = r0 + rl;
+        int m = 0;
+        float t = 0.f;
+        if (sl < nS && i < rend) {
+            const size_t p = static_cast<size_t>(s0 + sl) * L.in + i;
+            if (a.x) {
+                double td;
+                bracket_of(L.lo, L.hi, L.G, L.dx, a.x[p], a.err, m, td);
+                t = static_cast<float>(td);
+            } else {
+                m = a.bm_in[p];
+                t = a.bt_in[p];
+            }
+        }
+        s_m[sl][rl] = m;
+        s_t[sl][rl] = t;
+    }
+    __syncthreads();
+    // 3. gather + interpolate + accumulate
+    float acc[S][VJ];
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int v = 0; v < VJ; ++v) acc[s][v] = 0.f;
+    if (jok) {
+        const int G = L.G;
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            const int rl = warp * RW + r;
+            if (r0 + rl >= rend) break;
+#pragma unroll
+            for (int v = 0; v < VJ; ++v) {
+                if (j0 + v >= L.out) break;
+                float g = 1.f;
+                if constexpr (kI8) g = s_lut[ed[r].gcode(v)];
+                if constexpr (FMT == FMT_F32) g = ed[r].g[v];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int m = s_m[s][rl];
+                    const float t = s_t[s][rl];
+                    float c0, c1;
+                    if constexpr (kI8) {
+                        const uint32_t p = __ldg(L.pair8 + static_cast<size_t>(ed[r].row(v)) * (G - 1) + m);
+                        c0 = i8lo(p);
+                        c1 = i8hi(p);
+                    } else if constexpr (FMT == FMT_F32) {
+                        const float* row = L.cb32 + static_cast<size_t>(ed[r].k[v]) * G + m;
+                        c0 = __ldg(row);
+                        c1 = __ldg(row + 1);
+                    } else {
+                        const float* row = L.cb32 + (static_cast<size_t>(r0 + rl) * L.out + j0 + v) * G + m;
+                        c0 = __ldg(row);
+                        c1 = __ldg(row + 1);
+                    }
+                    acc[s][v] = fmaf(g, fmaf(t, c1 - c0, c0), acc[s][v]);
+                }
+            }
+        }
+    }
+    // 4. fixed-order reduction over warps, one partial per split
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int v = 0; v < VJ; ++v) s_red[warp][s][lane * VJ + v] = acc[s][v];
+    __syncthreads();
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    for (int q = tid; q < S * JW; q += 256) {
+        const int s = q / JW, jl = q % JW, j = jg * JW + jl;
+        if (s >= nS || j >= L.out) continue;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) sum += s_red[w][s][jl];
+        a.partial[blockIdx.y * plane + static_cast<size_t>(s0 + s) * L.out + j] = sum;
+    }
+    // 5. the last CTA of this (output tile, sample tile) finishes it
+    if (!arrive_last(a.counters + jg * gridDim.z + sg, gridDim.y, &s_last)) return;
+    finish_tile(a, gridDim.y, s0, nS, jg * JW, min(JW, L.out - jg * JW));
+}
+
+// ---------------------------------------------------------------------------
+// k_fwd_large: samples in lanes.  CTA = 8 warps = 4 sample-warps (128
+// samples) x 2 output-warps (16 outputs each) -> tile 128 samples x 32
+// outputs, over a split of the input rows processed in chunks of IC rows.
+// Per chunk every edge of the tile is decoded ONCE (record + 16-byte padded
+// codebook row) into shared memory as gained pairs (g*c[m], g*(c[m+1]-c[m])),
+// m = 0..G-2; a thread then evaluates its 16 outputs for its sample with one
+// broadcast LDS.64 per edge-sample (lanes of a warp hit <= G-1 distinct
+// pairs of one edge: one wavefront).  Staging of chunk c+1 is prefetched into
+// registers while chunk c is computed.  int8 tables, G <= 16.
+
+constexpr int kLgSW = 4;                // sample-warps
+constexpr int kLgJW = 2;                // output-warps
+constexpr int kLgVJ = 16;               // outputs per thread
+constexpr int kLgS = 32 * kLgSW;        // samples per CTA
+constexpr int kLgJ = kLgJW * kLgVJ;     // outputs per CTA
+constexpr int kLgEdgesPerThread = 4;    // staged edges per thread per chunk (IC * kLgJ / 256)
+constexpr int kLgIC = kLgEdgesPerThread * 256 / kLgJ;  // 32 rows per chunk
+
+template <int FMT>
+__global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const DevLayer& L = a.L;
+    const int G = L.G, GP = G - 1;
+    // layout: pairs[2][IC][kLgJ][GP] float2 | m[2][IC][kLgS] int | t[2][IC][kLgS] float | lut[256]
+    float2* s_pair = reinterpret_cast<float2*>(smem);
+    const size_t pair_buf = static_cast<size_t>(kLgIC) * kLgJ * GP;
+    int* s_m = reinterpret_cast<int*>(s_pair + 2 * pair_buf);
+    float* s_t = reinterpret_cast<float*>(s_m + 2 * kLgIC * kLgS);
+    float* s_lut = s_t + 2 * kLgIC * kLgS;
+    __shared__ int s_last;
+    pdl_trigger();
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int sw = warp % kLgSW, jw = warp / kLgSW;
+    const int jbase = blockIdx.x * kLgJ;
+    const int s0 = blockIdx.z * kLgS;
+    const int nS = min(kLgS, a.B - s0);
+    const int r0 = blockIdx.y * a.rows_per_cta;
+    const int rend = min(L.in, r0 + a.rows_per_cta);
+    const int nchunks = (rend - r0 + kLgIC - 1) / kLgIC;
+    for (int q = tid; q < 256; q += 256) s_lut[q] = L.lutf[q];
+
+    // staging assignment: edge slot q = tid + 256*u -> (row il, output jl)
+    uint32_t rec[kLgEdgesPerThread];
+    uint4 row[kLgEdgesPerThread];
+    unsigned ok = 0;  // bit u: staged edge slot u exists
+    auto load_recs = [&](int c) {
+        ok = 0;
+#pragma unroll
+        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+            const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
+            const int i = r0 + c * kLgIC + il, j = jbase + jl;
+            if (i < rend && j < L.out) {
+                ok |= 1u << u;
+                const size_t e = static_cast<size_t>(i) * L.out + j;
+                if constexpr (FMT == FMT_I8_R32) {
+                    rec[u] = __ldg(L.rec + e);
+                } else {
+                    const uint32_t k = L.idx ? __ldg(L.idx + e) : 0u;
+                    rec[u] = __ldg(L.gb + e);  // gain code in bits 0-7
+                    row[u].x = k;              // row index parked until load_rows
+                }
+            }
+        }
+    };
+    auto load_rows = [&]() {
+#pragma unroll
+        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+            if (!(ok & (1u << u))) continue;
+            uint32_t k;
+            if constexpr (FMT == FMT_I8_R32) k = rec[u] & 0xFFFFu; else k = row[u].x;
+            row[u] = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
+        }
+    };
+    auto store_pairs = [&](int buf) {
+        float2* dst = s_pair + buf * pair_buf;
+#pragma unroll
+        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+            const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
+            float2* d = dst + (static_cast<size_t>(il) * kLgJ + jl) * GP;
+            float g = 0.f;  // absent edges stage zeros
+            if (ok & (1u << u)) {
+                int gc;
+                if constexpr (FMT == FMT_I8_R32) gc = (rec[u] >> 16) & 0xFF; else gc = rec[u] & 0xFF;
+                g = s_lut[gc];
+            }
+            const uint64_t lo = row[u].x | (static_cast<uint64_t>(row[u].y) << 32);
+            const uint64_t hi = row[u].z | (static_cast<uint64_t>(row[u].w) << 32);
+            auto code = [&](int b) -> float {  // static b after unrolling
+                const uint64_t w = b < 8 ? (lo >> (8 * b)) : (hi >> (8 * (b - 8)));
+                return static_cast<float>(static_cast<int8_t>(w & 0xFF));
+            };
+            float prev = g * code(0);
+#pragma unroll
+            for (int m = 0; m < 15; ++m) {
+                if (m < GP) {
+                    const float nxt = g * code(m + 1);
+                    d[m] = make_float2(prev, nxt - prev);
+                    prev = nxt;
+                }
+            }
+        }
+    };
+    auto store_brackets = [&](int c, int buf) {
+        for (int q = tid; q < kLgIC * kLgS; q += 256) {
+            const int il = q / kLgS, sl = q % kLgS, i = r0 + c * kLgIC + il;
+            int m = 0;
+            float t = 0.f;
+            if (sl < nS && i < rend) {
+                const size_t p = static_cast<size_t>(s0 + sl) * L.in + i;
+                m = a.bm_in[p];
+                t = a.bt_in[p];
+            }
+            s_m[(buf * kLgIC + il) * kLgS + sl] = m;
+            s_t[(buf * kLgIC + il) * kLgS + sl] = t;
+        }
+    };
+
+    float acc[kLgVJ];
+#pragma unroll
+    for (int v = 0; v < kLgVJ; ++v) acc[v] = 0.f;
+    const int sl = sw * 32 + lane;
+
+    if (nchunks > 0) {
+        load_recs(0);
+        __syncthreads();  // s_lut visible
+        load_rows();
+        pdl_wait();
+        store_pairs(0);
+        store_brackets(0, 0);
+        if (nchunks > 1) load_recs(1);
+        __syncthreads();
+    } else {
+        pdl_wait();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        const bool more = c + 1 < nchunks;
+        if (more) load_rows();  // rows of chunk c+1 fly while chunk c is computed
+        const float2* P = s_pair + buf * pair_buf;
+        const int* M = s_m + buf * kLgIC * kLgS;
+        const float* T = s_t + buf * kLgIC * kLgS;
+        const int nrow = min(kLgIC, rend - (r0 + c * kLgIC));
+        for (int il = 0; il < nrow; ++il) {
+            const int m = M[il * kLgS + sl];
+            const float t = T[il * kLgS + sl];
+            const float2* e = P + (static_cast<size_t>(il) * kLgJ + jw * kLgVJ) * GP + m;
+#pragma unroll
+            for (int v = 0; v < kLgVJ; ++v) {
+                const float2 p = e[v * GP];
+                acc[v] += fmaf(t, p.y, p.x);
+            }
+        }
+        if (more) {
+            store_pairs(buf ^ 1);
+            store_brackets(c + 1, buf ^ 1);
+            if (c + 2 < nchunks) load_recs(c + 2);
+        }
+        __syncthreads();
+    }
+    // one partial per (split, sample, output): each thread owns distinct entries
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    if (sl < nS) {
+#pragma unroll
+        for (int v = 0; v < kLgVJ; ++v) {
+            const int j = jbase + jw * kLgVJ + v;
+            if (j < L.out) a.partial[blockIdx.y * plane + static_cast<size_t>(s0 + sl) * L.out + j] = acc[v];
+        }
+    }
+    if (!arrive_last(a.counters + blockIdx.x * gridDim.z + blockIdx.z, gridDim.y, &s_last)) return;
+    finish_tile(a, gridDim.y, s0, nS, jbase, min(kLgJ, L.out - jbase));
+}
+
+// ---------------------------------------------------------------------------
+// K2 exact: one split (ascending i), every double op in the reference's
+// order with explicit _rn intrinsics (no FMA):
+//   compressed: y += (g*c0 + b)*w0 + (g*c1 + b)*t      lutham.cpp:810
+//   dense:      y += c0*w0 + c1*t                      lutham.cpp:787-788
 
 template <int FMT>
 struct Edge;
@@ -97,7 +511,7 @@ struct Edge<FMT_I8_R32> {
     uint32_t r;
     __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
         r = __ldg(L.rec + e);
-        row = L.cb8 + static_cast<size_t>(r & 0xFFFFu) * L.G;
+        row = L.cb8 + static_cast<size_t>(r & 0xFFFFu) * L.rs;
     }
     __device__ __forceinline__ int gcode() const { return (r >> 16) & 0xFF; }
     __device__ __forceinline__ int bcode() const { return static_cast<int8_t>(r >> 24); }
@@ -110,7 +524,7 @@ struct Edge<FMT_I8_WIDE> {
     __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
         const uint32_t k = L.idx ? __ldg(L.idx + e) : 0u;
         gbv = __ldg(L.gb + e);
-        row = L.cb8 + static_cast<size_t>(k) * L.G;
+        row = L.cb8 + static_cast<size_t>(k) * L.rs;
     }
     __device__ __forceinline__ int gcode() const { return gbv & 0xFF; }
     __device__ __forceinline__ int bcode() const { return static_cast<int8_t>(gbv >> 8); }
@@ -136,8 +550,6 @@ struct Edge<FMT_DENSE> {
     }
 };
 
-// Stage brackets (index, t) of samples [sbase, sbase+SC) x inputs
-// [ic, ic+n) into shared memory; padding samples get (0, 0).
 template <int SC, typename T>
 __device__ __forceinline__ void stage_brackets(int (*s_m)[kIC], T (*s_t)[kIC], const int* bm,
                                                const T* bt, int B, int in, int sbase, int ic,
@@ -156,111 +568,6 @@ __device__ __forceinline__ void stage_brackets(int (*s_m)[kIC], T (*s_t)[kIC], c
     }
 }
 
-// ---------------------------------------------------------------------------
-// K2 fast: CTA = TJ outputs x (kThreads/TJ)*SPT samples x one i-split.
-// Thread (jl, sg) owns output j and SPT consecutive samples; it streams the
-// edges (i, j) of its split in ascending i (coalesced along j), decodes each
-// edge once and evaluates it for its SPT samples.  Partials go to
-// partial[z][s][j]; k_combine reduces them in fixed z order.
-template <int FMT, int TJ, int SPT>
-__global__ void __launch_bounds__(kThreads)
-    k_gather_fast(DevLayer L, int B, int ichunk, const int* __restrict__ bm,
-                  const float* __restrict__ btf, float* __restrict__ partial) {
-    constexpr int SG = kThreads / TJ;
-    constexpr int SC = SG * SPT;
-    __shared__ int s_m[SC][kIC];
-    __shared__ float s_t[SC][kIC];
-    __shared__ float s_lut[256];
-    if (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
-        for (int q = threadIdx.x; q < 256; q += kThreads) s_lut[q] = L.lutf[q];
-    }
-    const int jl = threadIdx.x % TJ, sg = threadIdx.x / TJ;
-    const int j = blockIdx.x * TJ + jl;
-    const int sbase = blockIdx.y * SC;
-    const int z = blockIdx.z;
-    const int ibeg = z * ichunk, iend = min(L.in, ibeg + ichunk);
-    const bool jok = j < L.out;
-    float acc[SPT];
-#pragma unroll
-    for (int r = 0; r < SPT; ++r) acc[r] = 0.f;
-
-    for (int ic = ibeg; ic < iend; ic += kIC) {
-        const int n = min(kIC, iend - ic);
-        __syncthreads();
-        stage_brackets<SC, float>(s_m, s_t, bm, btf, B, L.in, sbase, ic, n);
-        __syncthreads();
-        if (!jok) continue;
-        for (int il = 0; il < n; ++il) {
-            const size_t e = static_cast<size_t>(ic + il) * L.out + j;
-            Edge<FMT> ed;
-            ed.load(L, e);
-            float g = 1.f;
-            if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) g = s_lut[ed.gcode()];
-            if constexpr (FMT == FMT_F32) g = ed.g;
-#pragma unroll
-            for (int r = 0; r < SPT; ++r) {
-                const int sl = sg * SPT + r;
-                const int m = s_m[sl][il];
-                const float t = s_t[sl][il];
-                float c0, c1;
-                if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
-                    c0 = static_cast<float>(__ldg(ed.row + m));
-                    c1 = static_cast<float>(__ldg(ed.row + m + 1));
-                } else {
-                    c0 = __ldg(ed.row + m);
-                    c1 = __ldg(ed.row + m + 1);
-                }
-                const float v = fmaf(t, c1 - c0, c0);
-                if constexpr (FMT == FMT_DENSE) {
-                    acc[r] += v;
-                } else {
-                    acc[r] = fmaf(g, v, acc[r]);
-                }
-            }
-        }
-    }
-    if (jok) {
-#pragma unroll
-        for (int r = 0; r < SPT; ++r) {
-            const int s = sbase + sg * SPT + r;
-            if (s < B) partial[(static_cast<size_t>(z) * B + s) * L.out + j] = acc[r];
-        }
-    }
-}
-
-// Fixed-order split reduction (z ascending) in double, plus the per-output
-// bias sum; then the next layer's knot selection on the finished value.
-__global__ void k_combine(DevLayer L, int B, int nsplit, const float* __restrict__ partial,
-                          double* __restrict__ y, int has_next, double nlo, double nhi, int nG,
-                          double ndx, int* __restrict__ bm, float* __restrict__ btf,
-                          double* __restrict__ btd, int* __restrict__ err) {
-    const long long n = static_cast<long long>(B) * L.out;
-    for (long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; p < n;
-         p += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(p % L.out);
-        double v = L.bias_sum ? L.bias_sum[j] : 0.0;
-        for (int z = 0; z < nsplit; ++z) v += static_cast<double>(partial[static_cast<size_t>(z) * n + p]);
-        y[p] = v;
-        if (has_next) {
-            int m = 0;
-            double t = 0.0;
-            if (!isfinite(v)) {
-                *err = 1;
-            } else {
-                locate_dev(nlo, nhi, nG, ndx, v, m, t);
-            }
-            bm[p] = m;
-            btf[p] = static_cast<float>(t);
-            btd[p] = t;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2 exact: same tiling, one split (ascending i), every double op in the
-// reference's order with explicit _rn intrinsics (no FMA):
-//   compressed: y += (g*c0 + b)*w0 + (g*c1 + b)*t      lutham.cpp:810
-//   dense:      y += c0*w0 + c1*t                      lutham.cpp:787-788
 template <int FMT, int TJ, int SPT>
 __global__ void __launch_bounds__(kThreads)
     k_gather_exact(DevLayer L, int B, const int* __restrict__ bm, const double* __restrict__ btd,
@@ -283,6 +590,7 @@ __global__ void __launch_bounds__(kThreads)
         stage_brackets<SC, double>(s_m, s_t, bm, btd, B, L.in, sbase, ic, n);
         __syncthreads();
         if (!jok) continue;
+#pragma unroll 4
         for (int il = 0; il < n; ++il) {
             const size_t e = static_cast<size_t>(ic + il) * L.out + j;
             Edge<FMT> ed;
@@ -402,48 +710,67 @@ int grid_for(long long n, int threads) {
     return static_cast<int>(b);
 }
 
-template <int FMT, int TJ>
-void dispatch_fast_spt(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
-                       const float* btf, float* partial, cudaStream_t s) {
-    dim3 grid(c.jt, c.st, c.nsplit);
+// ---- launch helpers ----------------------------------------------------------
+
+template <typename K, typename... Args>
+void launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <int FMT, int VJ, int S>
+void dispatch_small_rw(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    const dim3 grid(c.jt, c.nsplit, c.st);
+    if (c.rw == 8) launch_ex(k_fwd_small<FMT, VJ, S, 8>, grid, dim3(256), 0, pdl, s, a);
+    else if (c.rw == 4) launch_ex(k_fwd_small<FMT, VJ, S, 4>, grid, dim3(256), 0, pdl, s, a);
+    else launch_ex(k_fwd_small<FMT, VJ, S, 1>, grid, dim3(256), 0, pdl, s, a);
+}
+
+template <int FMT, int VJ>
+void dispatch_small_s(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
     switch (c.spt) {
-        case 1: k_gather_fast<FMT, TJ, 1><<<grid, kThreads, 0, s>>>(L, B, c.ichunk, bm, btf, partial); break;
-        case 2: k_gather_fast<FMT, TJ, 2><<<grid, kThreads, 0, s>>>(L, B, c.ichunk, bm, btf, partial); break;
-        case 4: k_gather_fast<FMT, TJ, 4><<<grid, kThreads, 0, s>>>(L, B, c.ichunk, bm, btf, partial); break;
-        default: k_gather_fast<FMT, TJ, 8><<<grid, kThreads, 0, s>>>(L, B, c.ichunk, bm, btf, partial); break;
+        case 1: dispatch_small_rw<FMT, VJ, 1>(a, c, pdl, s); break;
+        case 2: dispatch_small_rw<FMT, VJ, 2>(a, c, pdl, s); break;
+        case 4: dispatch_small_rw<FMT, VJ, 4>(a, c, pdl, s); break;
+        default: dispatch_small_rw<FMT, VJ, 8>(a, c, pdl, s); break;
     }
 }
 
-template <int FMT>
-void dispatch_fast_tj(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
-                      const float* btf, float* partial, cudaStream_t s) {
-    switch (c.tj) {
-        case 32: dispatch_fast_spt<FMT, 32>(L, c, B, bm, btf, partial, s); break;
-        case 64: dispatch_fast_spt<FMT, 64>(L, c, B, bm, btf, partial, s); break;
-        default: dispatch_fast_spt<FMT, 128>(L, c, B, bm, btf, partial, s); break;
-    }
-}
-
-template <int FMT, int TJ>
+template <int FMT, int VJ, int S>
 void dispatch_exact_spt(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
                         const double* btd, double* y, cudaStream_t s) {
+    (void)VJ;
     dim3 grid(c.jt, c.st, 1);
-    switch (c.spt) {
-        case 1: k_gather_exact<FMT, TJ, 1><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
-        case 2: k_gather_exact<FMT, TJ, 2><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
-        case 4: k_gather_exact<FMT, TJ, 4><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
-        default: k_gather_exact<FMT, TJ, 8><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
+    switch (c.tj) {
+        case 32: k_gather_exact<FMT, 32, S><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
+        case 64: k_gather_exact<FMT, 64, S><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
+        default: k_gather_exact<FMT, 128, S><<<grid, kThreads, 0, s>>>(L, B, bm, btd, y); break;
     }
 }
 
 template <int FMT>
-void dispatch_exact_tj(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
-                       const double* btd, double* y, cudaStream_t s) {
-    switch (c.tj) {
-        case 32: dispatch_exact_spt<FMT, 32>(L, c, B, bm, btd, y, s); break;
-        case 64: dispatch_exact_spt<FMT, 64>(L, c, B, bm, btd, y, s); break;
-        default: dispatch_exact_spt<FMT, 128>(L, c, B, bm, btd, y, s); break;
+void dispatch_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm, const double* btd,
+                    double* y, cudaStream_t s) {
+    switch (c.spt) {
+        case 1: dispatch_exact_spt<FMT, 0, 1>(L, c, B, bm, btd, y, s); break;
+        case 2: dispatch_exact_spt<FMT, 0, 2>(L, c, B, bm, btd, y, s); break;
+        case 4: dispatch_exact_spt<FMT, 0, 4>(L, c, B, bm, btd, y, s); break;
+        default: dispatch_exact_spt<FMT, 0, 8>(L, c, B, bm, btd, y, s); break;
     }
+}
+
+size_t large_smem(int G) {
+    return static_cast<size_t>(2) * kLgIC * kLgJ * (G - 1) * sizeof(float2) +
+           static_cast<size_t>(2) * kLgIC * kLgS * (sizeof(int) + sizeof(float)) + 256 * sizeof(float);
 }
 
 }  // namespace
@@ -452,23 +779,53 @@ void dispatch_exact_tj(const DevLayer& L, const LaunchCfg& c, int B, const int* 
 
 LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms) {
     LaunchCfg c{};
-    c.tj = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
-    c.spt = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
-    const int sc = (kThreads / c.tj) * c.spt;
-    c.jt = (L.out + c.tj - 1) / c.tj;
-    c.st = (B + sc - 1) / sc;
+    const int sms = num_sms > 0 ? num_sms : 148;
     if (exact) {
+        c.tj = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
+        c.spt = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
+        const int sc = (kThreads / c.tj) * c.spt;
+        c.jt = (L.out + c.tj - 1) / c.tj;
+        c.st = (B + sc - 1) / sc;
         c.nsplit = 1;
         c.ichunk = L.in;
         return c;
     }
-    const long long base = static_cast<long long>(c.jt) * c.st;
-    const long long target = 4LL * (num_sms > 0 ? num_sms : 148);
-    long long ns = (target + base - 1) / base;
-    const long long maxns = L.in / 16 > 1 ? L.in / 16 : 1;
-    if (ns > maxns) ns = maxns;
-    if (ns < 1) ns = 1;
-    c.ichunk = static_cast<int>((L.in + ns - 1) / ns);
+    const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
+    if (i8 && L.G <= 16 && B >= 64) {
+        // samples in lanes: tile 128 samples x 32 outputs x split of the rows
+        c.kind = 1;
+        c.ic = kLgIC;
+        c.jt = (L.out + kLgJ - 1) / kLgJ;
+        c.st = (B + kLgS - 1) / kLgS;
+        const long long base = static_cast<long long>(c.jt) * c.st;
+        long long ns = (2LL * sms + base - 1) / base;  // ~2 CTAs per SM
+        const long long maxns = (L.in + kLgIC - 1) / kLgIC;
+        ns = ns < 1 ? 1 : (ns > maxns ? maxns : ns);
+        const int chunks = static_cast<int>((L.in + kLgIC - 1) / kLgIC);
+        const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
+        c.ichunk = per * kLgIC;
+        c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
+        c.smem = large_smem(L.G);
+        c.tj = kLgJ;
+        c.spt = 0;
+        return c;
+    }
+    // rows in warps: 8 warps x rw rows, 32*vj outputs, S samples
+    c.kind = 0;
+    c.vj = (L.fmt == FMT_I8_R32 && L.out % 4 == 0 && L.out >= 128) ? 4 : 1;
+    c.spt = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
+    c.tj = 32 * c.vj;
+    c.jt = (L.out + c.tj - 1) / c.tj;
+    c.st = (B + c.spt - 1) / c.spt;
+    // rows per warp: enough CTAs to put ~4 per SM in flight
+    const long long tiles = static_cast<long long>(c.jt) * c.st;
+    c.rw = 8;
+    for (int rw : {8, 4, 1}) {
+        c.rw = rw;
+        const long long ctas = tiles * ((L.in + 8LL * rw - 1) / (8LL * rw));
+        if (ctas >= 3LL * sms) break;
+    }
+    c.ichunk = 8 * c.rw;
     c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
     return c;
 }
@@ -480,33 +837,31 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
     k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L.lo, L.hi, L.G, L.dx, bm, btf, btd, err);
 }
 
-void launch_gather_fast(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
-                        const float* btf, float* partial, cudaStream_t s) {
-    switch (L.fmt) {
-        case FMT_I8_R32: dispatch_fast_tj<FMT_I8_R32>(L, c, B, bm, btf, partial, s); break;
-        case FMT_I8_WIDE: dispatch_fast_tj<FMT_I8_WIDE>(L, c, B, bm, btf, partial, s); break;
-        case FMT_F32: dispatch_fast_tj<FMT_F32>(L, c, B, bm, btf, partial, s); break;
-        default: dispatch_fast_tj<FMT_DENSE>(L, c, B, bm, btf, partial, s); break;
+void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    if (c.kind == 1) {
+        auto k = a.L.fmt == FMT_I8_R32 ? k_fwd_large<FMT_I8_R32> : k_fwd_large<FMT_I8_WIDE>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+        launch_ex(k, dim3(c.jt, c.nsplit, c.st), dim3(256), c.smem, pdl, s, a);
+        return;
     }
-}
-
-void launch_combine(const DevLayer& L, const LaunchCfg& c, int B, const float* partial,
-                    double* y, const DevLayer* next, int* bm, float* btf, double* btd, int* err,
-                    cudaStream_t s) {
-    const long long n = static_cast<long long>(B) * L.out;
-    if (n == 0) return;
-    k_combine<<<grid_for(n, 256), 256, 0, s>>>(
-        L, B, c.nsplit, partial, y, next != nullptr, next ? next->lo : 0.0, next ? next->hi : 0.0,
-        next ? next->G : 2, next ? next->dx : 1.0, bm, btf, btd, err);
+    switch (a.L.fmt) {
+        case FMT_I8_R32:
+            if (c.vj == 4) dispatch_small_s<FMT_I8_R32, 4>(a, c, pdl, s);
+            else dispatch_small_s<FMT_I8_R32, 1>(a, c, pdl, s);
+            break;
+        case FMT_I8_WIDE: dispatch_small_s<FMT_I8_WIDE, 1>(a, c, pdl, s); break;
+        case FMT_F32: dispatch_small_s<FMT_F32, 1>(a, c, pdl, s); break;
+        default: dispatch_small_s<FMT_DENSE, 1>(a, c, pdl, s); break;
+    }
 }
 
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
                          const double* btd, double* y, cudaStream_t s) {
     switch (L.fmt) {
-        case FMT_I8_R32: dispatch_exact_tj<FMT_I8_R32>(L, c, B, bm, btd, y, s); break;
-        case FMT_I8_WIDE: dispatch_exact_tj<FMT_I8_WIDE>(L, c, B, bm, btd, y, s); break;
-        case FMT_F32: dispatch_exact_tj<FMT_F32>(L, c, B, bm, btd, y, s); break;
-        default: dispatch_exact_tj<FMT_DENSE>(L, c, B, bm, btd, y, s); break;
+        case FMT_I8_R32: dispatch_exact<FMT_I8_R32>(L, c, B, bm, btd, y, s); break;
+        case FMT_I8_WIDE: dispatch_exact<FMT_I8_WIDE>(L, c, B, bm, btd, y, s); break;
+        case FMT_F32: dispatch_exact<FMT_F32>(L, c, B, bm, btd, y, s); break;
+        default: dispatch_exact<FMT_DENSE>(L, c, B, bm, btd, y, s); break;
     }
 }
 
