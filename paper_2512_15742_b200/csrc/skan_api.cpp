@@ -447,12 +447,13 @@ void upload(skan_head* h, std::vector<Staged>& st) {
                 const uint64_t G = s.h.grid_size, K = s.h.k, rs = int8_row_stride(G);
                 std::vector<int8_t> padded(K * rs, 0);
                 std::vector<uint16_t> pairs(K * (G - 1));
+                // pair planes, bracket-major: pairs[m][k] = c[k][m] | c[k][m+1] << 8
                 for (uint64_t k = 0; k < K; ++k) {
                     const int8_t* row = s.cb8.data() + k * G;
                     std::memcpy(padded.data() + k * rs, row, G);
                     for (uint64_t m = 0; m + 1 < G; ++m)
-                        pairs[k * (G - 1) + m] = static_cast<uint16_t>(static_cast<uint8_t>(row[m]) |
-                                                                       (static_cast<uint8_t>(row[m + 1]) << 8));
+                        pairs[m * K + k] = static_cast<uint16_t>(static_cast<uint8_t>(row[m]) |
+                                                                 (static_cast<uint8_t>(row[m + 1]) << 8));
                 }
                 d.rs = static_cast<int>(rs);
                 d.cb8 = static_cast<const int8_t*>(put(padded.data(), padded.size()));
@@ -521,14 +522,28 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
 // ---------------------------------------------------------------------------
 // forward
 
+// Fast-path kernel choice for every layer at batch B.  A layer may use the
+// pair-plane kernel only if it has a successor and its predecessor did not
+// (the successor reduces its partials while locating).
+std::vector<skan::LaunchCfg> plan_head(const skan_head* h, int B) {
+    const int nl = static_cast<int>(h->dl.size());
+    std::vector<skan::LaunchCfg> cfg(nl);
+    for (int l = 0; l < nl; ++l) {
+        const bool allow = l + 1 < nl && !(l > 0 && cfg[l - 1].kind == 2);
+        cfg[l] = skan::choose_cfg(h->dl[l], B, false, h->num_sms, allow);
+    }
+    return cfg;
+}
+
 // Largest split-partial buffer (floats) and per-layer counter count any
 // batch up to max_batch needs on the fast path.
 void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, uint64_t* counters) {
     uint64_t best = 0, cnt = 1;
-    for (const DevLayer& L : h->dl) {
-        for (int b = 1; b <= max_batch; ++b) {
-            const skan::LaunchCfg c = skan::choose_cfg(L, b, false, h->num_sms);
-            best = std::max<uint64_t>(best, static_cast<uint64_t>(c.nsplit) * b * L.out);
+    for (int b = 1; b <= max_batch; ++b) {
+        const std::vector<skan::LaunchCfg> cfg = plan_head(h, b);
+        for (size_t l = 0; l < cfg.size(); ++l) {
+            const skan::LaunchCfg& c = cfg[l];
+            best = std::max<uint64_t>(best, static_cast<uint64_t>(c.nsplit) * b * h->dl[l].out);
             cnt = std::max<uint64_t>(cnt, static_cast<uint64_t>(c.jt) * c.st);
         }
     }
@@ -537,18 +552,22 @@ void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, 
 }
 
 // One fused fast-path layer launch (plus the standalone locate in front of
-// layer 0 when the large-batch kernel is used).  Layer l reads brackets
-// bm[l&1] and its finisher writes layer l+1's into bm[(l+1)&1].
-int launch_layer_fast(const skan_head* h, skan_workspace* ws, int l, const double* x, int B, double* out,
-                      bool chained, cudaStream_t s) {
+// layer 0 when that kernel does not locate inline).  Layer l reads brackets
+// bm[l&1] and its finisher writes layer l+1's into bm[(l+1)&1]; split
+// partials ping-pong between two buffers so a layer can reduce its
+// predecessor's partials while writing its own.
+int launch_layer_fast(const skan_head* h, skan_workspace* ws, const std::vector<skan::LaunchCfg>& cfg, int l,
+                      const double* x, int B, double* out, bool chained, cudaStream_t s) {
     auto& d = ws->d;
     const int nl = static_cast<int>(h->dl.size());
     const size_t plane = static_cast<size_t>(ws->max_batch) * h->max_width;
     int* bm[2] = {d.bm, d.bm + plane};
     float* bt[2] = {d.btf, d.btf + plane};
+    float* part[2] = {d.partial, d.partial + ws->partial_floats};
     const DevLayer& L = h->dl[l];
     const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
-    const skan::LaunchCfg c = skan::choose_cfg(L, B, false, h->num_sms);
+    const skan::LaunchCfg& c = cfg[l];
+    const bool prev_planes = l > 0 && cfg[l - 1].kind == 2;
     int launches = 0;
     skan::FwdArgs a{};
     a.L = L;
@@ -558,14 +577,19 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, int l, const doubl
         if (c.kind == 0) {
             a.x = x;  // small batch: knot selection inline in each CTA
         } else {
-            skan::launch_locate_input(x, B, L.in, L, bm[0], bt[0], nullptr, d.err, s);
+            skan::launch_locate_input(x, B, L.in, L, bm[0], bt[0], nullptr, d.err, s, /*input_major=*/true);
             ++launches;
             chained = true;
         }
     }
     a.bm_in = bm[l & 1];
     a.bt_in = bt[l & 1];
-    a.partial = d.partial;
+    if (prev_planes) {
+        a.prev_partial = part[(l - 1) & 1];
+        a.prev_nsplit = cfg[l - 1].nsplit;
+        a.prev_bias_sum = h->dl[l - 1].bias_sum;
+    }
+    a.partial = part[l & 1];
     a.counters = d.counters + static_cast<size_t>(l) * d.counter_stride;
     a.y = out;
     a.has_next = next != nullptr;
@@ -608,9 +632,10 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
         }
     } else {
         ws->last_x = x;
+        const std::vector<skan::LaunchCfg> cfg = plan_head(h, B);
         bool chained = false;
         for (int l = 0; l < nl; ++l) {
-            launches += launch_layer_fast(h, ws, l, x, B, l + 1 < nl ? d.act[l & 1] : y, chained, s);
+            launches += launch_layer_fast(h, ws, cfg, l, x, B, l + 1 < nl ? d.act[l & 1] : y, chained, s);
             chained = true;
         }
     }
@@ -758,7 +783,7 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         ws->d.btd = static_cast<double*>(alloc(act * 8));
         uint64_t ncnt = 0;
         scratch_needs(h, max_batch, &ws->partial_floats, &ncnt);
-        ws->d.partial = static_cast<float*>(alloc(ws->partial_floats * 4));
+        ws->d.partial = static_cast<float*>(alloc(2 * ws->partial_floats * 4));  // ping-pong
         ws->d.counter_stride = ncnt;
         const size_t cbytes = ncnt * h->dl.size() * sizeof(unsigned);
         ws->d.counters = static_cast<unsigned*>(alloc(cbytes));
@@ -854,7 +879,9 @@ skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int laye
             skan::launch_gather_exact(L, c, batch, ws->d.bm, ws->d.btd, ws->d.act[1], s);
         } else {
             if (!ws->last_x) raise(SKAN_CONTRACT_ERROR, "run a forward on this workspace first");
-            launch_layer_fast(h, ws, layer, ws->last_x, batch, ws->d.act[layer & 1], false, s);
+            if (layer > 0 && plan_head(h, batch)[layer - 1].kind == 2)
+                raise(SKAN_CONTRACT_ERROR, "layer consumes pair-plane partials; profile it with its predecessor");
+            launch_layer_fast(h, ws, plan_head(h, batch), layer, ws->last_x, batch, ws->d.act[layer & 1], false, s);
         }
         skan::cuda_check(cudaGetLastError(), "profile launch");
     });

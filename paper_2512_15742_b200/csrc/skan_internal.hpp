@@ -65,7 +65,8 @@ struct DevLayer {
     const float* lutf;       // [128] float(gain(code) * cs) — fast int8 path
     const double* lutd;      // [128] gain(code) as dequantize_gain_code returns it
     const double* bias_sum;  // [out] sum_i b_ij in i order — fast path
-    const uint16_t* pair8;   // int8: [K][G-1] (c[k][m] | c[k][m+1] << 8) — one 2-byte gather per edge-sample
+    const uint16_t* pair8;   // int8 pair planes [G-1][K]: c[k][m] | c[k][m+1] << 8 — one 2-byte
+                             // gather per edge-sample; plane m is contiguous (smem-stageable)
     int rs;                  // int8 codebook row stride in bytes (G rounded up to 16)
 };
 
@@ -76,7 +77,8 @@ struct LaunchCfg {
     int jt, st;  // CTA tiles along j and samples
     int nsplit;  // i-splits (fast path); 1 in exact mode
     int ichunk;  // inputs per split
-    int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes (large batch)
+    int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes
+                 // (large batch), 2 = pair planes in shared memory (batch 1)
     int vj;      // outputs per lane (small kernel)
     int rw;      // rows per warp (small kernel)
     int ic;      // inputs per staged chunk (large kernel)
@@ -93,17 +95,23 @@ struct FwdArgs {
     int B;
     int rows_per_cta;       // inputs per split
     const double* x;        // non-null: locate inline from these f64 inputs [B][in]
-    const int* bm_in;       // else: brackets [B][in] from the previous layer / locate kernel
-    const float* bt_in;
+    const int* bm_in;       // else: brackets, input-major [in][B], from the previous
+    const float* bt_in;     //   layer's finisher or the locate kernel
     float* partial;         // [nsplit][B][out]
     unsigned* counters;     // [jt * st], zero between launches
     double* y;              // [B][out]
     int has_next;
     double nlo, nhi, ndx;
     int nG;
-    int* bm_out;            // next layer brackets [B][out]
+    int* bm_out;            // next layer brackets, input-major [out][B]
     float* bt_out;
     int* err;
+    // The previous layer ran the pair-plane kernel and left split partials
+    // instead of brackets: this launch reduces them (fixed order, double)
+    // for the rows it consumes, adds the previous bias sums, and locates.
+    const float* prev_partial;    // [prev_nsplit][B][in]
+    int prev_nsplit;
+    const double* prev_bias_sum;  // [in]
 };
 
 // Workspace device buffers (one forward stream).
@@ -120,7 +128,7 @@ struct DevScratch {
 
 // ---- kernel launchers (skan_kernels.cu) ----
 void launch_locate_input(const double* x, int n_rows, int width, const DevLayer& L, int* bm,
-                         float* btf, double* btd, int* err, cudaStream_t s);
+                         float* btf, double* btd, int* err, cudaStream_t s, bool input_major = false);
 // Fused fast-path layer (gather + split reduction + next-layer locate).
 // pdl: launch with programmatic stream serialization (overlaps the
 // prologue with the previous kernel's tail).
@@ -138,6 +146,8 @@ void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint3
 // Record a thread-local error for skan_last_error and return its status.
 skan_status set_error(skan_status s, const std::string& msg, uint64_t offset, int fault);
 
-LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms);
+// allow_planes: the layer has a successor that can reduce its split
+// partials (the pair-plane kernel writes partials, not brackets).
+LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool allow_planes = false);
 
 }  // namespace skan

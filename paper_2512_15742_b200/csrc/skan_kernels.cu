@@ -85,16 +85,21 @@ __device__ __forceinline__ void bracket_of(double lo, double hi, int G, double d
     }
 }
 
+// x is [rows][width] row-major.  Brackets are written in the same layout, or
+// input-major ([width][rows], rows = samples) when `rows_tr` > 0 — the
+// layout the fast-path kernels read (sample-contiguous).
 __global__ void k_locate_input(const double* __restrict__ x, long long n, double lo, double hi,
                                int G, double dx, int* __restrict__ bm, float* __restrict__ btf,
-                               double* __restrict__ btd, int* __restrict__ err) {
+                               double* __restrict__ btd, int* __restrict__ err, int width, int rows_tr) {
     pdl_trigger();
     pdl_wait();
     for (long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<long long>(gridDim.x) * blockDim.x) {
         int m;
         double t;
-        bracket_of(lo, hi, G, dx, x[p], err, m, t);
+        long long src = p;
+        if (rows_tr > 0) src = (p % rows_tr) * width + p / rows_tr;  // p = i*rows + s
+        bracket_of(lo, hi, G, dx, x[src], err, m, t);
         bm[p] = m;
         btf[p] = static_cast<float>(t);
         if (btd) btd[p] = t;
@@ -107,29 +112,114 @@ __global__ void k_locate_input(const double* __restrict__ x, long long n, double
 __device__ __forceinline__ float i8lo(uint32_t p) { return static_cast<float>(static_cast<int8_t>(p & 0xFFu)); }
 __device__ __forceinline__ float i8hi(uint32_t p) { return static_cast<float>(static_cast<int8_t>((p >> 8) & 0xFFu)); }
 
-// Shared finisher: runs in the last CTA of an output tile.  Threads cover
-// the tile's (sample, output) entries; each sums the nsplit partials in
-// ascending split order in double, adds sum_i b_ij, writes y and the next
-// layer's bracket.
+// Shared finisher: runs in the last CTA of an output tile and reduces the
+// tile's split partials.  C lanes cooperate on one (sample, output) entry
+// (lane c sums splits c, c+C, ... in ascending order; a fixed segmented
+// butterfly then combines the C lane sums) and every thread keeps kFinNB
+// entries in flight.  C and the entry-to-thread map depend only on the
+// launch shape, so the summation order -- hence the result bits -- never
+// depends on timing.  Then bias sum, y, and the next layer's bracket.
+constexpr int kFinNB = 8;
+
+__device__ __forceinline__ void finish_entry(const FwdArgs& a, size_t p, int j, double v) {
+    v += a.L.bias_sum ? a.L.bias_sum[j] : 0.0;
+    a.y[p] = v;
+    if (a.has_next) {
+        int m;
+        double t;
+        bracket_of(a.nlo, a.nhi, a.nG, a.ndx, v, a.err, m, t);
+        const size_t s = p / a.L.out;
+        const size_t q = static_cast<size_t>(j) * a.B + s;  // input-major for the next layer
+        a.bm_out[q] = m;
+        a.bt_out[q] = static_cast<float>(t);
+    }
+}
+
 __device__ __forceinline__ void finish_tile(const FwdArgs& a, int nsplit, int s_begin, int s_count,
                                             int j_begin, int j_count) {
     const DevLayer& L = a.L;
     const size_t plane = static_cast<size_t>(a.B) * L.out;
-    for (int q = threadIdx.x; q < s_count * j_count; q += blockDim.x) {
-        const int s = s_begin + q / j_count;
-        const int j = j_begin + q % j_count;
-        const size_t p = static_cast<size_t>(s) * L.out + j;
-        double v = L.bias_sum ? L.bias_sum[j] : 0.0;
-        const float* src = a.partial + p;
-#pragma unroll 8
-        for (int z = 0; z < nsplit; ++z) v += static_cast<double>(__ldcg(src + z * plane));
-        a.y[p] = v;
-        if (a.has_next) {
-            int m;
-            double t;
-            bracket_of(a.nlo, a.nhi, a.nG, a.ndx, v, a.err, m, t);
-            a.bm_out[p] = m;
-            a.bt_out[p] = static_cast<float>(t);
+    const int entries = s_count * j_count;
+    int C = 1;  // lanes per entry: about 4 splits per lane, at most a warp
+    while (C < 32 && C * 4 < nsplit) C <<= 1;
+    const int c = threadIdx.x & (C - 1);
+    const int R = blockDim.x / C;  // entry groups in flight per pass
+    // uniform trip count for all threads (the butterfly needs full warps)
+    for (int pass = 0; pass < entries; pass += R * kFinNB) {
+        const int base = pass + (threadIdx.x / C) * kFinNB;
+        double v[kFinNB];
+        size_t p[kFinNB];
+        int jj[kFinNB];
+#pragma unroll
+        for (int b = 0; b < kFinNB; ++b) {
+            v[b] = 0.0;
+            const int q = min(base + b, entries - 1);
+            jj[b] = j_begin + q % j_count;
+            p[b] = static_cast<size_t>(s_begin + q / j_count) * L.out + jj[b];
+        }
+#pragma unroll 2
+        for (int z = c; z < nsplit; z += C) {
+            const float* src = a.partial + z * plane;
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b) v[b] += static_cast<double>(__ldcg(src + p[b]));
+        }
+        for (int o = C >> 1; o > 0; o >>= 1) {
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b) v[b] += __shfl_xor_sync(0xFFFFFFFFu, v[b], o);
+        }
+        if (c == 0) {
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b)
+                if (base + b < entries) finish_entry(a, p[b], jj[b], v[b]);
+        }
+    }
+}
+
+// Consumer-side reduction (after a pair-plane layer): brackets of the rows
+// [r0, rend) x samples [s0, s0+nS) of THIS layer from the previous layer's
+// split partials, same fixed C-lane order as finish_tile.  Writes
+// s_m/s_t[sl*R + rl] for sl < S (padding entries get (0, 0)).
+__device__ __forceinline__ void reduce_prev_rows(const FwdArgs& a, int r0, int rend, int s0, int nS, int S,
+                                                 int R, int* s_m, float* s_t) {
+    const DevLayer& L = a.L;
+    const size_t plane = static_cast<size_t>(a.B) * L.in;
+    const int entries = S * R;
+    int C = 1;
+    while (C < 32 && C * 4 < a.prev_nsplit) C <<= 1;
+    const int c = threadIdx.x & (C - 1);
+    const int groups = blockDim.x / C;
+    for (int pass = 0; pass < entries; pass += groups * kFinNB) {
+        const int base = pass + (threadIdx.x / C) * kFinNB;
+        double v[kFinNB];
+        size_t idx[kFinNB];
+#pragma unroll
+        for (int b = 0; b < kFinNB; ++b) {
+            v[b] = 0.0;
+            const int q = base + b, sl = q / R, i = r0 + q % R;
+            const bool ok = q < entries && sl < nS && i < rend;
+            idx[b] = ok ? static_cast<size_t>(s0 + sl) * L.in + i : 0;
+        }
+#pragma unroll 2
+        for (int z = c; z < a.prev_nsplit; z += C) {
+            const float* src = a.prev_partial + z * plane;
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b) v[b] += static_cast<double>(__ldcg(src + idx[b]));
+        }
+        for (int o = C >> 1; o > 0; o >>= 1) {
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b) v[b] += __shfl_xor_sync(0xFFFFFFFFu, v[b], o);
+        }
+        if (c == 0) {
+#pragma unroll
+            for (int b = 0; b < kFinNB; ++b) {
+                const int q = base + b, sl = q / R, i = r0 + q % R;
+                if (q >= entries) continue;
+                int m = 0;
+                double t = 0.0;
+                if (sl < nS && i < rend) bracket_of(L.lo, L.hi, L.G, L.dx, v[b] + a.prev_bias_sum[i], a.err, m, t);
+                s_m[q] = m;
+                s_t[q] = static_cast<float>(t);
+            }
         }
     }
 }
@@ -242,7 +332,8 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
     }
     // 2. brackets (produced by the previous kernel, or located inline)
     pdl_wait();
-    for (int q = tid; q < S * R; q += 256) {
+    if (a.prev_partial) reduce_prev_rows(a, r0, rend, s0, nS, S, R, &s_m[0][0], &s_t[0][0]);
+    else for (int q = tid; q < S * R; q += 256) {
         const int sl = q / R, rl = q % R, i = r0 + rl;
         int m = 0;
         float t = 0.f;
@@ -253,8 +344,9 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
                 bracket_of(L.lo, L.hi, L.G, L.dx, a.x[p], a.err, m, td);
                 t = static_cast<float>(td);
             } else {
-                m = a.bm_in[p];
-                t = a.bt_in[p];
+                const size_t pt = static_cast<size_t>(i) * a.B + s0 + sl;  // input-major
+                m = a.bm_in[pt];
+                t = a.bt_in[pt];
             }
         }
         s_m[sl][rl] = m;
@@ -285,7 +377,7 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
                     const float t = s_t[s][rl];
                     float c0, c1;
                     if constexpr (kI8) {
-                        const uint32_t p = __ldg(L.pair8 + static_cast<size_t>(ed[r].row(v)) * (G - 1) + m);
+                        const uint32_t p = __ldg(L.pair8 + static_cast<size_t>(m) * L.K + ed[r].row(v));
                         c0 = i8lo(p);
                         c1 = i8hi(p);
                     } else if constexpr (FMT == FMT_F32) {
@@ -323,6 +415,205 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_fwd_planes (batch 1, int8 tables, non-final layer): at batch 1 every edge
+// of input row i reads the same bracket m_i, i.e. only the pair plane
+// P_m[k] = (c[k][m], c[k][m+1]) (K x 2 bytes: 128 KB at K=65536).  Each CTA
+// (one per SM) takes a share of the rows of ONE bracket bucket, stages that
+// plane into shared memory with a TMA bulk copy, and serves every codebook
+// gather of its rows from shared memory instead of L1/L2 (where a random
+// 2-byte gather costs a full 32-byte sector and an L1 wavefront).
+// Rows -> buckets is a deterministic function of the bracket histogram
+// (largest remainder), rows within a bucket are taken in ascending order,
+// warps take rows round-robin: the fp32 summation order is fixed.  Output:
+// one fp32 partial vector per CTA; the next layer reduces them.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int NV>  // 128-output groups per row (out <= 128*NV), 4 outputs per lane per group
+__global__ void __launch_bounds__(256, 1) k_fwd_planes(FwdArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int kMaxB = 32;  // brackets (G-1) supported
+    __shared__ int s_cnt[kMaxB];
+    __shared__ int s_scan[256];
+    __shared__ int s_bucket, s_lo, s_hi;
+    __shared__ float s_lut[256];
+    __shared__ __align__(8) uint64_t s_bar;
+    const DevLayer& L = a.L;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int GP = L.G - 1;
+    uint16_t* s_plane = reinterpret_cast<uint16_t*>(smem);
+    const uint32_t plane_bytes = static_cast<uint32_t>(L.K) * 2u;
+    int* s_rows = reinterpret_cast<int*>(smem + ((plane_bytes + 127u) & ~127u));
+    pdl_trigger();
+    s_lut[tid] = L.lutf[tid];
+    if (tid < kMaxB) s_cnt[tid] = 0;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait();  // brackets of this layer's inputs
+    // 1. histogram of brackets (order-free integer counts)
+    const int per = (L.in + 255) / 256;  // rows per thread, contiguous
+    const int i0 = tid * per, i1 = min(L.in, i0 + per);
+    int mine[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) mine[q] = (q < i1 - i0) ? a.bm_in[i0 + q] : -1;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        if (mine[q] >= 0) atomicAdd(&s_cnt[mine[q]], 1);
+    __syncthreads();
+    // 2. CTA -> bucket by largest remainder over P CTAs (same in every CTA)
+    if (tid == 0) {
+        const int P = gridDim.x;
+        int alloc[kMaxB], rem_b[kMaxB];
+        int used = 0;
+        for (int b = 0; b < GP; ++b) {
+            const long long num = static_cast<long long>(P) * s_cnt[b];
+            alloc[b] = s_cnt[b] ? static_cast<int>(num / L.in) : 0;
+            if (s_cnt[b] && alloc[b] == 0) alloc[b] = 1;
+            rem_b[b] = static_cast<int>(num % L.in);
+            used += alloc[b];
+        }
+        while (used < P) {  // hand out the rest by remainder, lowest bucket on ties
+            int best = -1;
+            for (int b = 0; b < GP; ++b)
+                if (s_cnt[b] && (best < 0 || rem_b[b] > rem_b[best])) best = b;
+            alloc[best] += 1;
+            rem_b[best] = -1;
+            ++used;
+            bool any = false;
+            for (int b = 0; b < GP; ++b) any |= rem_b[b] >= 0 && s_cnt[b];
+            if (!any)
+                for (int b = 0; b < GP; ++b) rem_b[b] = s_cnt[b] ? 0 : -1;
+        }
+        while (used > P) {  // only if many single-row buckets: take from the largest
+            int best = 0;
+            for (int b = 1; b < GP; ++b)
+                if (alloc[b] > alloc[best]) best = b;
+            alloc[best] -= 1;
+            --used;
+        }
+        int c = blockIdx.x, b = 0;
+        while (b < GP && c >= alloc[b]) c -= alloc[b++];
+        s_bucket = b;
+        const int n = b < GP ? s_cnt[b] : 0, k = b < GP ? alloc[b] : 1;
+        s_lo = static_cast<int>(static_cast<long long>(n) * c / k);
+        s_hi = static_cast<int>(static_cast<long long>(n) * (c + 1) / k);
+        if (b < GP) {  // 3. stage plane b (TMA bulk copies, 32 KB each)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+                         "r"(plane_bytes)
+                         : "memory");
+            const char* src = reinterpret_cast<const char*>(L.pair8 + static_cast<size_t>(b) * L.K);
+            for (uint32_t off = 0; off < plane_bytes; off += 32768u) {
+                const uint32_t len = min(32768u, plane_bytes - off);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(smem + off)),
+                    "l"(src + off), "r"(len), "r"(smem_u32(&s_bar))
+                    : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    const int bucket = s_bucket, lo = s_lo, hi = s_hi;
+    // 4. my rows: rank within the bucket via one block scan of per-thread counts
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) cnt += mine[q] == bucket;
+    s_scan[tid] = cnt;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {  // Hillis-Steele inclusive scan
+        const int v = tid >= o ? s_scan[tid - o] : 0;
+        __syncthreads();
+        s_scan[tid] += v;
+        __syncthreads();
+    }
+    int rank = s_scan[tid] - cnt;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if (mine[q] == bucket) {
+            if (rank >= lo && rank < hi) s_rows[rank - lo] = i0 + q;
+            ++rank;
+        }
+    }
+    __syncthreads();
+    const int nrows = hi - lo;
+    // 5. stream this CTA's rows: warp w takes rows w, w+8, ...; records are
+    //    prefetched one row ahead; codebook pairs come from the staged plane.
+    float acc[NV][4];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = 0.f;
+    uint4 rec[NV], nxt[NV];
+    auto load_row = [&](int rr, uint4* dst) {
+        const int i = s_rows[rr];
+        const uint32_t* base = L.rec + static_cast<size_t>(i) * L.out;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int j = v * 128 + lane * 4;
+            dst[v] = j < L.out ? __ldg(reinterpret_cast<const uint4*>(base + j)) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    if (warp < nrows) load_row(warp, rec);
+    if (bucket < GP) {
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(smem_u32(&s_bar))
+                : "memory");
+        }
+    }
+    for (int rr = warp; rr < nrows; rr += 8) {
+        const bool more = rr + 8 < nrows;
+        if (more) load_row(rr + 8, nxt);
+        const float t = a.bt_in[s_rows[rr]];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t r4[4] = {rec[v].x, rec[v].y, rec[v].z, rec[v].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t p = s_plane[r4[e] & 0xFFFFu];
+                const float c0 = i8lo(p), c1 = i8hi(p);
+                acc[v][e] = fmaf(s_lut[(r4[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[v][e]);
+            }
+        }
+        if (more) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rec[v] = nxt[v];
+        }
+    }
+    // 6. fixed-order reduction over warps (plane region reused), one partial per CTA
+    __syncthreads();
+    float* s_red = reinterpret_cast<float*>(smem);  // [8][128*NV]
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int j = v * 128 + lane * 4;
+        *reinterpret_cast<float4*>(s_red + warp * (128 * NV) + j) =
+            make_float4(acc[v][0], acc[v][1], acc[v][2], acc[v][3]);
+    }
+    __syncthreads();
+    for (int j = tid; j < L.out; j += 256) {
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sum += s_red[w * (128 * NV) + j];
+        a.partial[static_cast<size_t>(blockIdx.x) * L.out + j] = sum;
+    }
+}
+
+size_t planes_smem(const DevLayer& L) {
+    const size_t plane = (static_cast<size_t>(L.K) * 2 + 127) / 128 * 128;
+    const size_t red = static_cast<size_t>(8) * 128 * ((L.out + 127) / 128) * sizeof(float);
+    return (plane + static_cast<size_t>(L.in) * sizeof(int)) > red ? plane + static_cast<size_t>(L.in) * sizeof(int)
+                                                                     : red;
+}
+
+// ---------------------------------------------------------------------------
 // k_fwd_large: samples in lanes.  CTA = 8 warps = 4 sample-warps (128
 // samples) x 2 output-warps (16 outputs each) -> tile 128 samples x 32
 // outputs, over a split of the input rows processed in chunks of IC rows.
@@ -338,20 +629,19 @@ constexpr int kLgJW = 2;                // output-warps
 constexpr int kLgVJ = 16;               // outputs per thread
 constexpr int kLgS = 32 * kLgSW;        // samples per CTA
 constexpr int kLgJ = kLgJW * kLgVJ;     // outputs per CTA
-constexpr int kLgEdgesPerThread = 4;    // staged edges per thread per chunk (IC * kLgJ / 256)
-constexpr int kLgIC = kLgEdgesPerThread * 256 / kLgJ;  // 32 rows per chunk
 
-template <int FMT>
-__global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+template <int FMT, int EPT>  // EPT: staged edges per thread per chunk
+__global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
+    constexpr int IC = EPT * 256 / kLgJ;  // input rows per chunk
+    extern __shared__ __align__(128) unsigned char smem[];
     const DevLayer& L = a.L;
     const int G = L.G, GP = G - 1;
     // layout: pairs[2][IC][kLgJ][GP] float2 | m[2][IC][kLgS] int | t[2][IC][kLgS] float | lut[256]
     float2* s_pair = reinterpret_cast<float2*>(smem);
-    const size_t pair_buf = static_cast<size_t>(kLgIC) * kLgJ * GP;
+    const size_t pair_buf = static_cast<size_t>(IC) * kLgJ * GP;
     int* s_m = reinterpret_cast<int*>(s_pair + 2 * pair_buf);
-    float* s_t = reinterpret_cast<float*>(s_m + 2 * kLgIC * kLgS);
-    float* s_lut = s_t + 2 * kLgIC * kLgS;
+    float* s_t = reinterpret_cast<float*>(s_m + 2 * IC * kLgS);
+    float* s_lut = s_t + 2 * IC * kLgS;
     __shared__ int s_last;
     pdl_trigger();
 
@@ -362,19 +652,19 @@ __global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
     const int nS = min(kLgS, a.B - s0);
     const int r0 = blockIdx.y * a.rows_per_cta;
     const int rend = min(L.in, r0 + a.rows_per_cta);
-    const int nchunks = (rend - r0 + kLgIC - 1) / kLgIC;
+    const int nchunks = (rend - r0 + IC - 1) / IC;
     for (int q = tid; q < 256; q += 256) s_lut[q] = L.lutf[q];
 
     // staging assignment: edge slot q = tid + 256*u -> (row il, output jl)
-    uint32_t rec[kLgEdgesPerThread];
-    uint4 row[kLgEdgesPerThread];
+    uint32_t rec[EPT];
+    uint4 row[EPT];
     unsigned ok = 0;  // bit u: staged edge slot u exists
     auto load_recs = [&](int c) {
         ok = 0;
 #pragma unroll
-        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+        for (int u = 0; u < EPT; ++u) {
             const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
-            const int i = r0 + c * kLgIC + il, j = jbase + jl;
+            const int i = r0 + c * IC + il, j = jbase + jl;
             if (i < rend && j < L.out) {
                 ok |= 1u << u;
                 const size_t e = static_cast<size_t>(i) * L.out + j;
@@ -390,7 +680,7 @@ __global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
     };
     auto load_rows = [&]() {
 #pragma unroll
-        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+        for (int u = 0; u < EPT; ++u) {
             if (!(ok & (1u << u))) continue;
             uint32_t k;
             if constexpr (FMT == FMT_I8_R32) k = rec[u] & 0xFFFFu; else k = row[u].x;
@@ -400,7 +690,7 @@ __global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
     auto store_pairs = [&](int buf) {
         float2* dst = s_pair + buf * pair_buf;
 #pragma unroll
-        for (int u = 0; u < kLgEdgesPerThread; ++u) {
+        for (int u = 0; u < EPT; ++u) {
             const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
             float2* d = dst + (static_cast<size_t>(il) * kLgJ + jl) * GP;
             float g = 0.f;  // absent edges stage zeros
@@ -427,17 +717,17 @@ __global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
         }
     };
     auto store_brackets = [&](int c, int buf) {
-        for (int q = tid; q < kLgIC * kLgS; q += 256) {
-            const int il = q / kLgS, sl = q % kLgS, i = r0 + c * kLgIC + il;
+        for (int q = tid; q < IC * kLgS; q += 256) {
+            const int il = q / kLgS, sl = q % kLgS, i = r0 + c * IC + il;
             int m = 0;
             float t = 0.f;
             if (sl < nS && i < rend) {
-                const size_t p = static_cast<size_t>(s0 + sl) * L.in + i;
+                const size_t p = static_cast<size_t>(i) * a.B + s0 + sl;  // input-major: coalesced
                 m = a.bm_in[p];
                 t = a.bt_in[p];
             }
-            s_m[(buf * kLgIC + il) * kLgS + sl] = m;
-            s_t[(buf * kLgIC + il) * kLgS + sl] = t;
+            s_m[(buf * IC + il) * kLgS + sl] = m;
+            s_t[(buf * IC + il) * kLgS + sl] = t;
         }
     };
 
@@ -463,9 +753,9 @@ __global__ void __launch_bounds__(256, 1) k_fwd_large(FwdArgs a) {
         const bool more = c + 1 < nchunks;
         if (more) load_rows();  // rows of chunk c+1 fly while chunk c is computed
         const float2* P = s_pair + buf * pair_buf;
-        const int* M = s_m + buf * kLgIC * kLgS;
-        const float* T = s_t + buf * kLgIC * kLgS;
-        const int nrow = min(kLgIC, rend - (r0 + c * kLgIC));
+        const int* M = s_m + buf * IC * kLgS;
+        const float* T = s_t + buf * IC * kLgS;
+        const int nrow = min(IC, rend - (r0 + c * IC));
         for (int il = 0; il < nrow; ++il) {
             const int m = M[il * kLgS + sl];
             const float t = T[il * kLgS + sl];
@@ -768,18 +1058,35 @@ void dispatch_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
     }
 }
 
-size_t large_smem(int G) {
-    return static_cast<size_t>(2) * kLgIC * kLgJ * (G - 1) * sizeof(float2) +
-           static_cast<size_t>(2) * kLgIC * kLgS * (sizeof(int) + sizeof(float)) + 256 * sizeof(float);
+size_t large_smem(int G, int ept) {
+    const size_t ic = static_cast<size_t>(ept) * 256 / kLgJ;
+    return 2 * ic * kLgJ * (G - 1) * sizeof(float2) + 2 * ic * kLgS * (sizeof(int) + sizeof(float)) +
+           256 * sizeof(float);
 }
+
+// Shared-memory budget of one large-batch CTA: two fit per SM.
+constexpr size_t kLgSmemBudget = 110 * 1024;
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
 
-LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms) {
+LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool allow_planes) {
     LaunchCfg c{};
     const int sms = num_sms > 0 ? num_sms : 148;
+    if (!exact && allow_planes && B == 1 && L.fmt == FMT_I8_R32 && L.out % 4 == 0 && L.out <= 1536 &&
+        L.in <= 4096 && L.K % 8 == 0 && static_cast<size_t>(L.K) * 2 <= 160 * 1024 && L.G - 1 <= 32 &&
+        static_cast<long long>(L.in) * L.out >= 256LL * 1024) {
+        c.kind = 2;
+        const int groups = (L.out + 127) / 128;
+        c.vj = groups <= 2 ? 2 : (groups <= 4 ? 4 : (groups <= 8 ? 8 : 12));
+        c.nsplit = sms;  // one CTA per SM, each a share of one bracket bucket
+        c.jt = 1;
+        c.st = 1;
+        c.ichunk = L.in;
+        c.smem = planes_smem(L);
+        return c;
+    }
     if (exact) {
         c.tj = L.out <= 32 ? 32 : (L.out <= 64 ? 64 : 128);
         c.spt = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
@@ -794,18 +1101,22 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms) {
     if (i8 && L.G <= 16 && B >= 64) {
         // samples in lanes: tile 128 samples x 32 outputs x split of the rows
         c.kind = 1;
-        c.ic = kLgIC;
+        int ept = 4;
+        while (ept > 1 && large_smem(L.G, ept) > kLgSmemBudget) ept >>= 1;
+        c.vj = ept;
+        c.ic = ept * 256 / kLgJ;
         c.jt = (L.out + kLgJ - 1) / kLgJ;
         c.st = (B + kLgS - 1) / kLgS;
         const long long base = static_cast<long long>(c.jt) * c.st;
-        long long ns = (2LL * sms + base - 1) / base;  // ~2 CTAs per SM
-        const long long maxns = (L.in + kLgIC - 1) / kLgIC;
+        long long ns = (2LL * sms + base - 1) / base;  // ~2 CTAs per SM, one wave
+        if (ns > 16) ns = 16;                          // bounds the finisher's partial traffic
+        const long long maxns = (L.in + c.ic - 1) / c.ic;
         ns = ns < 1 ? 1 : (ns > maxns ? maxns : ns);
-        const int chunks = static_cast<int>((L.in + kLgIC - 1) / kLgIC);
+        const int chunks = static_cast<int>((L.in + c.ic - 1) / c.ic);
         const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
-        c.ichunk = per * kLgIC;
+        c.ichunk = per * c.ic;
         c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
-        c.smem = large_smem(L.G);
+        c.smem = large_smem(L.G, ept);
         c.tj = kLgJ;
         c.spt = 0;
         return c;
@@ -817,13 +1128,14 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms) {
     c.tj = 32 * c.vj;
     c.jt = (L.out + c.tj - 1) / c.tj;
     c.st = (B + c.spt - 1) / c.spt;
-    // rows per warp: enough CTAs to put ~4 per SM in flight
+    // rows per warp: 8 (deepest record prefetch, fewest splits) unless that
+    // leaves SMs idle
     const long long tiles = static_cast<long long>(c.jt) * c.st;
     c.rw = 8;
     for (int rw : {8, 4, 1}) {
         c.rw = rw;
         const long long ctas = tiles * ((L.in + 8LL * rw - 1) / (8LL * rw));
-        if (ctas >= 3LL * sms) break;
+        if (ctas >= sms) break;
     }
     c.ichunk = 8 * c.rw;
     c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
@@ -831,15 +1143,32 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms) {
 }
 
 void launch_locate_input(const double* x, int n_rows, int width, const DevLayer& L, int* bm,
-                         float* btf, double* btd, int* err, cudaStream_t s) {
+                         float* btf, double* btd, int* err, cudaStream_t s, bool input_major) {
     const long long n = static_cast<long long>(n_rows) * width;
     if (n == 0) return;
-    k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L.lo, L.hi, L.G, L.dx, bm, btf, btd, err);
+    k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L.lo, L.hi, L.G, L.dx, bm, btf, btd, err, width,
+                                                    input_major ? n_rows : 0);
 }
 
 void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    if (c.kind == 2) {
+        void (*k)(FwdArgs);
+        switch (c.vj) {
+            case 2: k = k_fwd_planes<2>; break;
+            case 4: k = k_fwd_planes<4>; break;
+            case 8: k = k_fwd_planes<8>; break;
+            default: k = k_fwd_planes<12>; break;
+        }
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+        launch_ex(k, dim3(c.nsplit), dim3(256), c.smem, pdl, s, a);
+        return;
+    }
     if (c.kind == 1) {
-        auto k = a.L.fmt == FMT_I8_R32 ? k_fwd_large<FMT_I8_R32> : k_fwd_large<FMT_I8_WIDE>;
+        void (*k)(FwdArgs);
+        const bool r32 = a.L.fmt == FMT_I8_R32;
+        if (c.vj == 4) k = r32 ? k_fwd_large<FMT_I8_R32, 4> : k_fwd_large<FMT_I8_WIDE, 4>;
+        else if (c.vj == 2) k = r32 ? k_fwd_large<FMT_I8_R32, 2> : k_fwd_large<FMT_I8_WIDE, 2>;
+        else k = r32 ? k_fwd_large<FMT_I8_R32, 1> : k_fwd_large<FMT_I8_WIDE, 1>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
         launch_ex(k, dim3(c.jt, c.nsplit, c.st), dim3(256), c.smem, pdl, s, a);
         return;
