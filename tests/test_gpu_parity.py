@@ -191,6 +191,24 @@ def test_fast_mode_bitwise_reproducible(torch_cuda):
     assert np.array_equal(_bits(a), _bits(b)) and np.array_equal(_bits(a), _bits(c))
 
 
+def test_fast_mode_batch1_pair_planes(torch_cuda):
+    """Batch 1 routes big int8 layers through the shared-memory pair-plane
+    kernel (k_fwd_planes) and the next layer's consumer-side reduction:
+    within tolerance, bitwise reproducible, several heads and seeds."""
+    for dims, k, G, seed in [((512, 512, 8), 4096, 10, 1), ((1024, 700, 12), 8192, 6, 2),
+                             ((2048, 1408, 20), 65536, 10, 3), ((640, 1536, 24, 3), 1000, 16, 4)]:
+        cn = synthetic.synthetic_head(dims=dims, k=k, grid=G, int8=True, seed=seed)
+        tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
+        model = hq.build_model(cn)
+        for xs in (1, 2):
+            x = synthetic.synthetic_inputs(1, dims[0], seed=10 * seed + xs, grid=G)
+            want, _ = oracle.port_forward(tables, x, 1)
+            a, _ = _gpu_forward(model, x, 1, "fast")
+            b, _ = _gpu_forward(model, x, 1, "fast")
+            assert np.array_equal(_bits(a), _bits(b))
+            assert_close(a, want, l1_scale(tables, x, 1))
+
+
 def test_batch_larger_than_workspace_is_chunked(torch_cuda):
     cn = synthetic.synthetic_head(dims=(64, 48, 5), k=256, grid=10, int8=True, seed=3)
     model = hq.build_model(cn)
