@@ -465,44 +465,33 @@ __global__ void __launch_bounds__(256, 1) k_fwd_planes(FwdArgs a) {
     for (int q = 0; q < 16; ++q)
         if (mine[q] >= 0) atomicAdd(&s_cnt[mine[q]], 1);
     __syncthreads();
-    // 2. CTA -> bucket by largest remainder over P CTAs (same in every CTA)
-    if (tid == 0) {
+    // 2. CTA -> bucket (same in every CTA): warp 0, lane b = bucket b.  Each
+    //    non-empty bucket gets 1 + floor((P - nonempty) * n_b / in) CTAs
+    //    (sum <= P; the few spare CTAs idle); CTA c serves the bucket whose
+    //    CTA range contains c and an even share of its rows (ascending i).
+    if (warp == 0) {
         const int P = gridDim.x;
-        int alloc[kMaxB], rem_b[kMaxB];
-        int used = 0;
-        for (int b = 0; b < GP; ++b) {
-            const long long num = static_cast<long long>(P) * s_cnt[b];
-            alloc[b] = s_cnt[b] ? static_cast<int>(num / L.in) : 0;
-            if (s_cnt[b] && alloc[b] == 0) alloc[b] = 1;
-            rem_b[b] = static_cast<int>(num % L.in);
-            used += alloc[b];
+        const int n = lane < GP ? s_cnt[lane] : 0;
+        const int nonempty = __popc(__ballot_sync(0xFFFFFFFFu, n > 0));
+        const int alloc = n > 0 ? 1 + static_cast<int>(static_cast<long long>(P - nonempty) * n / L.in) : 0;
+        int incl = alloc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
         }
-        while (used < P) {  // hand out the rest by remainder, lowest bucket on ties
-            int best = -1;
-            for (int b = 0; b < GP; ++b)
-                if (s_cnt[b] && (best < 0 || rem_b[b] > rem_b[best])) best = b;
-            alloc[best] += 1;
-            rem_b[best] = -1;
-            ++used;
-            bool any = false;
-            for (int b = 0; b < GP; ++b) any |= rem_b[b] >= 0 && s_cnt[b];
-            if (!any)
-                for (int b = 0; b < GP; ++b) rem_b[b] = s_cnt[b] ? 0 : -1;
+        const int c = blockIdx.x;
+        const unsigned hit = __ballot_sync(0xFFFFFFFFu, c >= incl - alloc && c < incl);
+        if (lane == 0) s_bucket = hit ? (__ffs(hit) - 1) : GP;
+        if (hit && lane == __ffs(hit) - 1) {
+            const int q = c - (incl - alloc);
+            s_lo = static_cast<int>(static_cast<long long>(n) * q / alloc);
+            s_hi = static_cast<int>(static_cast<long long>(n) * (q + 1) / alloc);
         }
-        while (used > P) {  // only if many single-row buckets: take from the largest
-            int best = 0;
-            for (int b = 1; b < GP; ++b)
-                if (alloc[b] > alloc[best]) best = b;
-            alloc[best] -= 1;
-            --used;
-        }
-        int c = blockIdx.x, b = 0;
-        while (b < GP && c >= alloc[b]) c -= alloc[b++];
-        s_bucket = b;
-        const int n = b < GP ? s_cnt[b] : 0, k = b < GP ? alloc[b] : 1;
-        s_lo = static_cast<int>(static_cast<long long>(n) * c / k);
-        s_hi = static_cast<int>(static_cast<long long>(n) * (c + 1) / k);
-        if (b < GP) {  // 3. stage plane b (TMA bulk copies, 32 KB each)
+        if (!hit && lane == 0) s_lo = s_hi = 0;
+        __syncwarp();
+        if (lane == 0 && hit) {  // 3. stage plane b: TMA bulk copies, 32 KB each
+            const int b = __ffs(hit) - 1;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
                          "r"(plane_bytes)
                          : "memory");
@@ -519,19 +508,21 @@ __global__ void __launch_bounds__(256, 1) k_fwd_planes(FwdArgs a) {
     }
     __syncthreads();
     const int bucket = s_bucket, lo = s_lo, hi = s_hi;
-    // 4. my rows: rank within the bucket via one block scan of per-thread counts
+    // 4. my rows: rank within the bucket = exclusive scan of per-thread counts
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) cnt += mine[q] == bucket;
-    s_scan[tid] = cnt;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {  // Hillis-Steele inclusive scan
-        const int v = tid >= o ? s_scan[tid - o] : 0;
-        __syncthreads();
-        s_scan[tid] += v;
-        __syncthreads();
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
     }
-    int rank = s_scan[tid] - cnt;
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    int wbase = 0;
+    for (int w = 0; w < warp; ++w) wbase += s_scan[w];
+    int rank = wbase + incl - cnt;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         if (mine[q] == bucket) {
@@ -606,9 +597,9 @@ __global__ void __launch_bounds__(256, 1) k_fwd_planes(FwdArgs a) {
     }
 }
 
-size_t planes_smem(const DevLayer& L) {
+size_t planes_smem(const DevLayer& L, int nv) {
     const size_t plane = (static_cast<size_t>(L.K) * 2 + 127) / 128 * 128;
-    const size_t red = static_cast<size_t>(8) * 128 * ((L.out + 127) / 128) * sizeof(float);
+    const size_t red = static_cast<size_t>(8) * 128 * nv * sizeof(float);  // [8 warps][128*NV]
     return (plane + static_cast<size_t>(L.in) * sizeof(int)) > red ? plane + static_cast<size_t>(L.in) * sizeof(int)
                                                                      : red;
 }
@@ -1084,7 +1075,7 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         c.jt = 1;
         c.st = 1;
         c.ichunk = L.in;
-        c.smem = planes_smem(L);
+        c.smem = planes_smem(L, c.vj);
         return c;
     }
     if (exact) {
