@@ -198,6 +198,10 @@ struct skan_head {
     uint64_t dbytes = 0;
     uint64_t edges = 0;
     int in_dim = 0, out_dim = 0, max_width = 0;
+    // batch-1 persistent kernel plan (skan_head_b1.cu)
+    bool b1_ok = false, b1_planes0 = false;
+    int b1_grid = 0, b1_nv = 0;
+    size_t b1_smem = 0;
 };
 
 struct skan_workspace {
@@ -214,6 +218,8 @@ struct skan_workspace {
     cudaStream_t last_stream = nullptr;
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
+    float* b1_part = nullptr;        // 2 x [grid][max_width] partials of the batch-1 kernel
+    unsigned* b1_bar = nullptr;      // its grid barrier
     std::vector<void*> allocs;
 };
 
@@ -516,6 +522,16 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
         h->edges += static_cast<uint64_t>(x.in_dim) * x.out_dim;
     }
     h->max_width = static_cast<int>(w);
+    // batch-1 persistent kernel: eligible heads get one CTA per SM, all
+    // co-resident (checked against the occupancy calculator at its smem size)
+    const int nl = static_cast<int>(h->dl.size());
+    if (skan::head_b1_supported(h->dl.data(), nl)) {
+        h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_planes0, &h->b1_nv);
+        if (h->b1_smem <= 200 * 1024) {
+            h->b1_ok = true;
+            h->b1_grid = h->num_sms;
+        }
+    }
     return h.release();
 }
 
@@ -632,6 +648,23 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
         }
     } else {
         ws->last_x = x;
+        if (B == 1 && h->b1_ok && ws->b1_part) {
+            // the whole head in one persistent cooperative kernel
+            skan::HeadB1Args a{};
+            a.nl = nl;
+            for (int l = 0; l < nl; ++l) a.L[l] = h->dl[l];
+            a.planes0 = h->b1_planes0;
+            a.x = x;
+            a.y = y;
+            const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
+            a.part[0] = ws->b1_part;
+            a.part[1] = ws->b1_part + n;
+            a.bar = ws->b1_bar;
+            a.err = d.err;
+            skan::launch_head_b1(a, h->b1_grid, h->b1_smem, h->b1_nv, s);
+            skan::cuda_check(cudaGetLastError(), "kernel launch");
+            return 1;
+        }
         const std::vector<skan::LaunchCfg> cfg = plan_head(h, B);
         bool chained = false;
         for (int l = 0; l < nl; ++l) {
@@ -789,6 +822,12 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         ws->d.counters = static_cast<unsigned*>(alloc(cbytes));
         skan::cuda_check(cudaMemset(ws->d.counters, 0, std::max<size_t>(cbytes, 256)), "cudaMemset");
         ws->d.err = static_cast<int*>(alloc(sizeof(int)));
+        if (h->b1_ok) {
+            const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
+            ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
+            ws->b1_bar = static_cast<unsigned*>(alloc(2 * sizeof(unsigned)));
+            skan::cuda_check(cudaMemset(ws->b1_bar, 0, 2 * sizeof(unsigned)), "cudaMemset");
+        }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
         skan::cuda_check(cudaMallocHost(&ws->h_err, sizeof(int)), "cudaMallocHost");

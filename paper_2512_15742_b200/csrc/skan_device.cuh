@@ -1,0 +1,108 @@
+// Device helpers shared by the sm_100a kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "skan_internal.hpp"
+
+namespace skan {
+namespace dev {
+
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------------------
+// Knot selection.  Every double operation is an explicit round-to-nearest
+// intrinsic so nvcc can neither contract lo + i*dx (kan.cpp:25) nor
+// (x - lo)/dx into an FMA: the bracket and t are bitwise the reference's.
+
+__device__ __forceinline__ double node_pos(double lo, double hi, int G, int i, double dx) {
+    if (i == 0) return lo;
+    if (i == G - 1) return hi;
+    return __dadd_rn(lo, __dmul_rn(static_cast<double>(i), dx));  // kan.cpp:21-26
+}
+
+// kan.cpp:28-58
+__device__ __forceinline__ bool locate_dev(double lo, double hi, int G, double dx, double x, int& idx,
+                                           double& t) {
+    bool clamped = false;
+    if (x < lo) {
+        x = lo;
+        clamped = true;
+    } else if (x > hi) {
+        x = hi;
+        clamped = true;
+    }
+    int i = static_cast<int>(floor(__ddiv_rn(__dsub_rn(x, lo), dx)));
+    if (i < 0) i = 0;
+    if (i > G - 2) i = G - 2;
+    if (i < G - 2 && x >= node_pos(lo, hi, G, i + 1, dx)) {
+        ++i;
+    } else if (i > 0 && x < node_pos(lo, hi, G, i, dx)) {
+        --i;
+    }
+    double tt;
+    if (x >= node_pos(lo, hi, G, i + 1, dx)) {
+        tt = 1.0;
+    } else {
+        tt = __ddiv_rn(__dsub_rn(x, node_pos(lo, hi, G, i, dx)), dx);
+        if (tt < 0.0) tt = 0.0;
+        if (tt > 1.0) tt = 1.0;
+    }
+    idx = i;
+    t = tt;
+    return clamped;
+}
+
+// locate with the non-finite check (ValueError, kan.cpp:29) folded into err
+__device__ __forceinline__ void bracket_of(double lo, double hi, int G, double dx, double v, int* err, int& m,
+                                           double& t) {
+    m = 0;
+    t = 0.0;
+    if (!isfinite(v)) {
+        *err = 1;
+    } else {
+        locate_dev(lo, hi, G, dx, v, m, t);
+    }
+}
+
+__device__ __forceinline__ float i8lo(uint32_t p) { return static_cast<float>(static_cast<int8_t>(p & 0xFFu)); }
+__device__ __forceinline__ float i8hi(uint32_t p) {
+    return static_cast<float>(static_cast<int8_t>((p >> 8) & 0xFFu));
+}
+
+// TMA 1-D bulk copy global -> shared, completing on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+}  // namespace dev
+}  // namespace skan

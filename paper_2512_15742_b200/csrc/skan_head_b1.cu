@@ -1,0 +1,375 @@
+// Batch-1 latency path: the whole head in ONE persistent, cooperative kernel.
+//
+// At batch 1 the head is a chain of dependent memory round trips, so the
+// design minimises round trips, not bytes:
+//   * one CTA per SM, grid barriers between layers (no kernel boundaries);
+//   * layer 0 (the wide one, e.g. 2048 -> 1408): every edge of input row i
+//     uses the same bracket m_i, so rows are bucketed by bracket and each CTA
+//     serves a share of ONE bucket with that bucket's codebook pair plane
+//     P_m[k] = (c[k][m], c[k][m+1]) staged in shared memory by a TMA bulk
+//     copy; the 2-byte codebook gathers hit shared memory instead of costing
+//     a 32-byte L2 sector and an L1 wavefront each;
+//   * later layers are split by input rows across CTAs; each CTA reduces
+//     exactly the previous-layer outputs it consumes (fixed order, double),
+//     adds their bias sums, and locates them;
+//   * the last layer's partials are reduced by a few CTAs into y.
+// All summation orders are fixed functions of the launch shape and the
+// bracket histogram: results are bitwise reproducible run to run.
+// int8 tables with <= 65536-row codebooks (FMT_I8_R32) only; other heads
+// use the multi-kernel path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "skan_device.cuh"
+#include "skan_internal.hpp"
+
+namespace skan {
+namespace {
+
+using namespace dev;
+
+constexpr int kT = 256;   // threads per CTA
+constexpr int kW = kT / 32;
+
+// Sense-reversing grid barrier over a {count, generation} pair.  Requires
+// all CTAs co-resident (cooperative launch).  Every thread fences its own
+// writes first, so data written before the barrier is visible after it.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = bar + 1;
+        const unsigned gen = *vgen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Reduce rows [r0, r1) of the previous layer's per-CTA partials
+// prev[z*width + i] (z < nz) in fixed order: C lanes per row, ascending z
+// per lane, then a fixed butterfly; + bias; then locate with layer L's grid.
+__device__ void reduce_rows(const float* prev, int width, int nz, const double* bias, const DevLayer& L, int r0,
+                            int r1, int* s_m, float* s_t, int* err) {
+    const int n = r1 - r0;
+    int C = 1;
+    while (C < 32 && C * 4 < nz) C <<= 1;
+    const int c = threadIdx.x & (C - 1), groups = kT / C;
+    for (int pass = 0; pass < n; pass += groups) {
+        const int q = pass + threadIdx.x / C;
+        const int i = r0 + min(q, n - 1);
+        double v = 0.0;
+#pragma unroll 4
+        for (int z = c; z < nz; z += C) v += static_cast<double>(__ldcg(prev + static_cast<size_t>(z) * width + i));
+        for (int o = C >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (c == 0 && q < n) {
+            int m;
+            double t;
+            bracket_of(L.lo, L.hi, L.G, L.dx, v + (bias ? bias[i] : 0.0), err, m, t);
+            s_m[q] = m;
+            s_t[q] = static_cast<float>(t);
+        }
+    }
+}
+
+// Row-split layer: this CTA's rows [r0, r1) (brackets in s_m/s_t), all
+// outputs.  Warp w takes rows w, w+8, ...; lane l outputs l, l+32, ...;
+// per-warp accumulators in shared memory; fixed-order sum over warps.
+__device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m, const float* s_t,
+                               const float* s_lut, float* s_acc, float* part_out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int q = threadIdx.x; q < kW * L.out; q += kT) s_acc[q] = 0.f;
+    __syncthreads();
+    float* acc = s_acc + warp * L.out;
+    for (int rl = warp; rl < r1 - r0; rl += kW) {
+        const int i = r0 + rl, m = s_m[rl];
+        const float t = s_t[rl];
+        const uint32_t* rec = L.rec + static_cast<size_t>(i) * L.out;
+        const uint16_t* plane = L.pair8 + static_cast<size_t>(m) * L.K;
+        for (int j = lane; j < L.out; j += 128) {  // 4 independent edges per lane per step
+            uint32_t r[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) r[e] = j + 32 * e < L.out ? __ldg(rec + j + 32 * e) : 0u;
+            uint32_t p[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[e] = j + 32 * e < L.out ? __ldg(plane + (r[e] & 0xFFFFu)) : 0u;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (j + 32 * e >= L.out) break;
+                const float c0 = i8lo(p[e]), c1 = i8hi(p[e]);
+                acc[j + 32 * e] = fmaf(s_lut[(r[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[j + 32 * e]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < L.out; j += kT) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) s += s_acc[w * L.out + j];
+        part_out[static_cast<size_t>(blockIdx.x) * L.out + j] = s;
+    }
+}
+
+// Pair-plane layer 0 (see k_fwd_planes in skan_kernels.cu for the scheme).
+template <int NV>
+__device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, float* s_lut, uint64_t* bar,
+                              float* part_out) {
+    const DevLayer& L = h.L[0];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int GP = L.G - 1;
+    __shared__ int s_cnt[32];
+    __shared__ int s_scan[kW];
+    __shared__ int s_bucket, s_lo, s_hi;
+    uint16_t* s_plane = reinterpret_cast<uint16_t*>(smem);
+    const uint32_t plane_bytes = static_cast<uint32_t>(L.K) * 2u;
+    int* s_rows = reinterpret_cast<int*>(smem + ((plane_bytes + 127u) & ~127u));
+    float* s_tall = reinterpret_cast<float*>(s_rows + L.in);
+    if (tid < 32) s_cnt[tid] = 0;
+    __syncthreads();
+    // 1. locate all inputs (contiguous slice per thread) + histogram
+    const int per = (L.in + kT - 1) / kT;
+    const int i0 = tid * per;
+    int mine[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        mine[q] = -1;
+        const int i = i0 + q;
+        if (q < per && i < L.in) {
+            int m;
+            double t;
+            bracket_of(L.lo, L.hi, L.G, L.dx, h.x[i], h.err, m, t);
+            mine[q] = m;
+            s_tall[i] = static_cast<float>(t);
+            atomicAdd(&s_cnt[m], 1);
+        }
+    }
+    __syncthreads();
+    // 2. CTA -> bucket; 3. stage the plane (warp 0)
+    if (warp == 0) {
+        const int P = gridDim.x;
+        const int n = lane < GP ? s_cnt[lane] : 0;
+        const int nonempty = __popc(__ballot_sync(0xFFFFFFFFu, n > 0));
+        const int alloc = n > 0 ? 1 + static_cast<int>(static_cast<long long>(P - nonempty) * n / L.in) : 0;
+        int incl = alloc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int c = blockIdx.x;
+        const unsigned hit = __ballot_sync(0xFFFFFFFFu, c >= incl - alloc && c < incl);
+        const int b = hit ? __ffs(hit) - 1 : GP;
+        if (lane == 0) {
+            s_bucket = b;
+            s_lo = s_hi = 0;
+        }
+        __syncwarp();
+        if (hit && lane == b) {
+            const int q = c - (incl - alloc);
+            s_lo = static_cast<int>(static_cast<long long>(n) * q / alloc);
+            s_hi = static_cast<int>(static_cast<long long>(n) * (q + 1) / alloc);
+        }
+        if (lane == 0 && hit) {
+            mbar_expect_tx(bar, plane_bytes);
+            const char* src = reinterpret_cast<const char*>(L.pair8 + static_cast<size_t>(b) * L.K);
+            for (uint32_t off = 0; off < plane_bytes; off += 32768u)
+                bulk_g2s(smem + off, src + off, min(32768u, plane_bytes - off), bar);
+        }
+    }
+    __syncthreads();
+    const int bucket = s_bucket, lo = s_lo, hi = s_hi;
+    // 4. my rows: rank within the bucket (exclusive scan of per-thread counts)
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) cnt += mine[q] == bucket;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_scan[warp] = incl;
+    __syncthreads();
+    int rank = incl - cnt;
+    for (int w = 0; w < warp; ++w) rank += s_scan[w];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if (mine[q] == bucket) {
+            if (rank >= lo && rank < hi) s_rows[rank - lo] = i0 + q;
+            ++rank;
+        }
+    }
+    __syncthreads();
+    const int nrows = hi - lo;
+    // 5. stream rows; gathers from the staged plane
+    float acc[NV][4];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = 0.f;
+    uint4 rec[NV], nxt[NV];
+    auto load_row = [&](int rr, uint4* dst) {
+        const uint32_t* base = L.rec + static_cast<size_t>(s_rows[rr]) * L.out;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int j = v * 128 + lane * 4;
+            dst[v] = j < L.out ? __ldg(reinterpret_cast<const uint4*>(base + j)) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    if (warp < nrows) load_row(warp, rec);
+    if (bucket < GP) mbar_wait(bar, 0);
+    for (int rr = warp; rr < nrows; rr += kW) {
+        const bool more = rr + kW < nrows;
+        if (more) load_row(rr + kW, nxt);
+        const float t = s_tall[s_rows[rr]];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t r4[4] = {rec[v].x, rec[v].y, rec[v].z, rec[v].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t p = s_plane[r4[e] & 0xFFFFu];
+                const float c0 = i8lo(p), c1 = i8hi(p);
+                acc[v][e] = fmaf(s_lut[(r4[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[v][e]);
+            }
+        }
+        if (more) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rec[v] = nxt[v];
+        }
+    }
+    // 6. fixed-order reduction over warps -> this CTA's partial
+    __syncthreads();
+    float* s_red = reinterpret_cast<float*>(smem);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const int j = v * 128 + lane * 4;
+        *reinterpret_cast<float4*>(s_red + warp * (128 * NV) + j) =
+            make_float4(acc[v][0], acc[v][1], acc[v][2], acc[v][3]);
+    }
+    __syncthreads();
+    for (int j = tid; j < L.out; j += kT) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) s += s_red[w * (128 * NV) + j];
+        part_out[static_cast<size_t>(blockIdx.x) * L.out + j] = s;
+    }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ float s_lut[256];
+    __shared__ __align__(8) uint64_t s_bar;
+    const int P = gridDim.x, c = blockIdx.x;
+    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    int* s_m = reinterpret_cast<int*>(smem);  // row-split scratch (after layer 0)
+    for (int l = 0; l < h.nl; ++l) {
+        const DevLayer& L = h.L[l];
+        float* part_out = h.part[l & 1];
+        __syncthreads();
+        s_lut[threadIdx.x] = L.lutf[threadIdx.x];
+        __syncthreads();
+        if (l == 0 && h.planes0) {
+            planes_layer0<NV>(h, smem, s_lut, &s_bar, part_out);
+        } else {
+            const int r0 = static_cast<int>(static_cast<long long>(L.in) * c / P);
+            const int r1 = static_cast<int>(static_cast<long long>(L.in) * (c + 1) / P);
+            const int nr = r1 - r0;
+            float* s_t = reinterpret_cast<float*>(s_m + nr);
+            float* s_acc = s_t + nr;
+            if (l == 0) {
+                for (int q = threadIdx.x; q < nr; q += kT) {
+                    int m;
+                    double t;
+                    bracket_of(L.lo, L.hi, L.G, L.dx, h.x[r0 + q], h.err, m, t);
+                    s_m[q] = m;
+                    s_t[q] = static_cast<float>(t);
+                }
+            } else {
+                reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, r0, r1, s_m, s_t, h.err);
+            }
+            __syncthreads();
+            rowsplit_layer(L, r0, r1, s_m, s_t, s_lut, s_acc, part_out);
+        }
+        grid_sync(h.bar);
+    }
+    // final: outputs [c*out/P, (c+1)*out/P) of the last layer, one warp each
+    const DevLayer& L = h.L[h.nl - 1];
+    const float* part = h.part[(h.nl - 1) & 1];
+    const int j0 = static_cast<int>(static_cast<long long>(L.out) * c / P);
+    const int j1 = static_cast<int>(static_cast<long long>(L.out) * (c + 1) / P);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = j0 + warp; j < j1; j += kW) {
+        double v = 0.0;
+        for (int z = lane; z < P; z += 32) v += static_cast<double>(__ldcg(part + static_cast<size_t>(z) * L.out + j));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) h.y[j] = v + (L.bias_sum ? L.bias_sum[j] : 0.0);
+    }
+}
+
+}  // namespace
+
+// Eligibility: every layer int8 with <= 65536 codebook rows (4-byte records),
+// G-1 <= 32 brackets, and the layer-0 plane + row list in shared memory.
+bool head_b1_supported(const DevLayer* L, int nl) {
+    if (nl < 1 || nl > kMaxHeadLayers) return false;
+    for (int l = 0; l < nl; ++l) {
+        if (L[l].fmt != FMT_I8_R32 || L[l].G - 1 > 32 || L[l].out > 16384) return false;
+    }
+    return true;
+}
+
+size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, bool* planes0, int* nv) {
+    const DevLayer& L0 = L[0];
+    *planes0 = L0.out % 4 == 0 && L0.out <= 1536 && L0.in <= 16 * kT && L0.K % 8 == 0 &&
+               static_cast<size_t>(L0.K) * 2 <= 150 * 1024 && static_cast<long long>(L0.in) * L0.out >= 256LL * 1024;
+    const int groups = (L0.out + 127) / 128;
+    *nv = groups <= 2 ? 2 : (groups <= 4 ? 4 : (groups <= 8 ? 8 : 12));
+    size_t need = 0;
+    if (*planes0) {
+        const size_t plane = (static_cast<size_t>(L0.K) * 2 + 127) / 128 * 128;
+        const size_t a = plane + static_cast<size_t>(L0.in) * (sizeof(int) + sizeof(float));
+        const size_t b = static_cast<size_t>(kW) * 128 * (*nv) * sizeof(float);
+        need = a > b ? a : b;
+    }
+    for (int l = 0; l < nl; ++l) {
+        if (l == 0 && *planes0) continue;
+        const int nr = (L[l].in + num_sms - 1) / num_sms + 1;
+        const size_t s = static_cast<size_t>(nr) * 8 + static_cast<size_t>(kW) * L[l].out * sizeof(float);
+        if (s > need) need = s;
+    }
+    return need;
+}
+
+void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s) {
+    void (*k)(HeadB1Args);
+    switch (nv) {
+        case 2: k = k_head_b1<2>; break;
+        case 4: k = k_head_b1<4>; break;
+        case 8: k = k_head_b1<8>; break;
+        default: k = k_head_b1<12>; break;
+    }
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, h);
+}
+
+}  // namespace skan

@@ -114,6 +114,22 @@ struct FwdArgs {
     const double* prev_bias_sum;  // [in]
 };
 
+// Batch-1 persistent head kernel (skan_head_b1.cu).
+constexpr int kMaxHeadLayers = 8;
+struct HeadB1Args {
+    int nl;
+    DevLayer L[kMaxHeadLayers];
+    int planes0;       // layer 0 served from shared-memory pair planes
+    const double* x;   // [in]
+    double* y;         // [out]
+    float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
+    unsigned* bar;     // grid barrier {count, generation}
+    int* err;
+};
+bool head_b1_supported(const DevLayer* L, int nl);
+size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, bool* planes0, int* nv);
+void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s);
+
 // Workspace device buffers (one forward stream).
 struct DevScratch {
     double* act[2];     // ping-pong activations [max_batch * max_width]
