@@ -32,11 +32,11 @@ using namespace dev;
 constexpr int kT = 256;   // threads per CTA
 constexpr int kW = kT / 32;
 
-// Sense-reversing grid barrier over a {count, generation} pair.  Requires
-// all CTAs co-resident (cooperative launch).  Every thread fences its own
-// writes first, so data written before the barrier is visible after it.
+// Generation grid barrier over a {count, generation} pair.  Requires all
+// CTAs co-resident (cooperative launch).  The CTA barrier orders the CTA's
+// writes before thread 0's gpu-scope fence (cumulativity), as in
+// cooperative_groups::grid_group::sync.
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned* vgen = bar + 1;
@@ -60,15 +60,25 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 __device__ void reduce_rows(const float* prev, int width, int nz, const double* bias, const DevLayer& L, int r0,
                             int r1, int* s_m, float* s_t, int* err) {
     const int n = r1 - r0;
+    // as many lanes per row as keep every thread busy (<= 32): few rows, many
+    // splits -> each thread loads <= ~8 partials, all issued at once
     int C = 1;
-    while (C < 32 && C * 4 < nz) C <<= 1;
+    while (C < 32 && (C * 2) * n <= kT) C <<= 1;
     const int c = threadIdx.x & (C - 1), groups = kT / C;
     for (int pass = 0; pass < n; pass += groups) {
         const int q = pass + threadIdx.x / C;
         const int i = r0 + min(q, n - 1);
         double v = 0.0;
-#pragma unroll 4
-        for (int z = c; z < nz; z += C) v += static_cast<double>(__ldcg(prev + static_cast<size_t>(z) * width + i));
+        for (int z0 = c; z0 < nz; z0 += 16 * C) {
+            float buf[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int z = z0 + u * C;
+                buf[u] = z < nz ? __ldcg(prev + static_cast<size_t>(z) * width + i) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v += static_cast<double>(buf[u]);
+        }
         for (int o = C >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (c == 0 && q < n) {
             int m;
@@ -120,7 +130,7 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
 
 // Pair-plane layer 0 (see k_fwd_planes in skan_kernels.cu for the scheme).
 template <int NV>
-__device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, float* s_lut, uint64_t* bar,
+__device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const float* s_lut, uint64_t* bar,
                               float* part_out) {
     const DevLayer& L = h.L[0];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -138,6 +148,9 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, float* s
     const int per = (L.in + kT - 1) / kT;
     const int i0 = tid * per;
     int mine[16];
+    double xv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) xv[q] = (q < per && i0 + q < L.in) ? h.x[i0 + q] : 0.0;  // one round trip
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         mine[q] = -1;
@@ -145,12 +158,14 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, float* s
         if (q < per && i < L.in) {
             int m;
             double t;
-            bracket_of(L.lo, L.hi, L.G, L.dx, h.x[i], h.err, m, t);
+            bracket_of(L.lo, L.hi, L.G, L.dx, xv[q], h.err, m, t);
             mine[q] = m;
             s_tall[i] = static_cast<float>(t);
-            atomicAdd(&s_cnt[m], 1);
         }
     }
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        if (mine[q] >= 0) atomicAdd(&s_cnt[mine[q]], 1);
     __syncthreads();
     // 2. CTA -> bucket; 3. stage the plane (warp 0)
     if (warp == 0) {
@@ -266,16 +281,17 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, float* s
 template <int NV>
 __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float s_lut[256];
+    __shared__ float s_luts[kMaxHeadLayers][256];
     __shared__ __align__(8) uint64_t s_bar;
     const int P = gridDim.x, c = blockIdx.x;
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+    for (int l = 0; l < h.nl; ++l) s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];  // one round trip
+    __syncthreads();
     int* s_m = reinterpret_cast<int*>(smem);  // row-split scratch (after layer 0)
     for (int l = 0; l < h.nl; ++l) {
         const DevLayer& L = h.L[l];
         float* part_out = h.part[l & 1];
-        __syncthreads();
-        s_lut[threadIdx.x] = L.lutf[threadIdx.x];
+        const float* s_lut = s_luts[l];
         __syncthreads();
         if (l == 0 && h.planes0) {
             planes_layer0<NV>(h, smem, s_lut, &s_bar, part_out);
@@ -309,7 +325,16 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = j0 + warp; j < j1; j += kW) {
         double v = 0.0;
-        for (int z = lane; z < P; z += 32) v += static_cast<double>(__ldcg(part + static_cast<size_t>(z) * L.out + j));
+        for (int z0 = lane; z0 < P; z0 += 8 * 32) {  // all loads of a lane issued at once
+            float buf[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int z = z0 + 32 * u;
+                buf[u] = z < P ? __ldcg(part + static_cast<size_t>(z) * L.out + j) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v += static_cast<double>(buf[u]);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) h.y[j] = v + (L.bias_sum ? L.bias_sum[j] : 0.0);
