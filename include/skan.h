@@ -248,6 +248,13 @@ int skan_workspace_last_launches(const skan_workspace* ws);
 skan_status skan_profile_gather(const skan_head* head, skan_workspace* ws, int layer, int batch,
                                 int mode, void* stream);
 
+/* Profiling hook: batch-1 forwards on ws record, per CTA of the persistent
+ * head kernel, %globaltimer stamps (ns) at 16 fixed phase slots into the
+ * device buffer d_stamps[grid][16] (NULL disables). */
+skan_status skan_debug_b1_timeline(skan_workspace* ws, unsigned long long* d_stamps);
+/* Grid size of the persistent batch-1 kernel for head (0 if not eligible). */
+int skan_head_b1_grid(const skan_head* head);
+
 /* ---- single-edge primitive (lutham.cpp:730-755) ----------------------- */
 
 /* Batched pli_lookup over n independent (row, g, b, x) tuples on the GPU:

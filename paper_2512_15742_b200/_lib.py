@@ -91,6 +91,8 @@ _SIGS = {
     "skan_forward_async": (C.c_int, [_p, _p, _p, C.c_int, _p, C.c_int, _p]),
     "skan_workspace_check": (C.c_int, [_p]),
     "skan_profile_gather": (C.c_int, [_p, _p, C.c_int, C.c_int, C.c_int, _p]),
+    "skan_debug_b1_timeline": (C.c_int, [_p, _p]),
+    "skan_head_b1_grid": (C.c_int, [_p]),
     "skan_forward_multi": (C.c_int, [C.POINTER(_p), C.POINTER(_p), C.c_int, _p, C.c_int, C.POINTER(_p), C.c_int, _p]),
     "skan_pli_lookup": (C.c_int, [_p, C.c_int, C.c_int, _p, _p, _p, _p, C.c_double, C.c_double, C.c_int, _p, _p]),
     "skan_locate": (C.c_int, [_p, C.c_int, C.c_double, C.c_double, C.c_int, _p, _p, _p, _p]),

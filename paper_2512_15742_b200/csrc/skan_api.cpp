@@ -220,6 +220,7 @@ struct skan_workspace {
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
     float* b1_part = nullptr;        // 2 x [grid][max_width] partials of the batch-1 kernel
     unsigned* b1_bar = nullptr;      // its grid barrier
+    unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
     std::vector<void*> allocs;
 };
 
@@ -661,6 +662,7 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
             a.part[1] = ws->b1_part + n;
             a.bar = ws->b1_bar;
             a.err = d.err;
+            a.timeline = ws->b1_timeline;
             skan::launch_head_b1(a, h->b1_grid, h->b1_smem, h->b1_nv, s);
             skan::cuda_check(cudaGetLastError(), "kernel launch");
             return 1;
@@ -925,6 +927,15 @@ skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int laye
         skan::cuda_check(cudaGetLastError(), "profile launch");
     });
 }
+
+skan_status skan_debug_b1_timeline(skan_workspace* ws, unsigned long long* d_stamps) {
+    return guarded([&] {
+        if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
+        ws->b1_timeline = d_stamps;
+    });
+}
+
+int skan_head_b1_grid(const skan_head* h) { return h && h->b1_ok ? h->b1_grid : 0; }
 
 skan_status skan_workspace_check(skan_workspace* ws) {
     return guarded([&] {

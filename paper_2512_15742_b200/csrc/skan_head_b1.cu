@@ -32,6 +32,16 @@ using namespace dev;
 constexpr int kT = 256;   // threads per CTA
 constexpr int kW = kT / 32;
 
+// Optional phase timeline (debug/profiling): thread 0 of each CTA stamps
+// %globaltimer (ns) at fixed phase ids.
+__device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
+    if (h.timeline && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        h.timeline[blockIdx.x * 16 + phase] = t;
+    }
+}
+
 // Generation grid barrier over a {count, generation} pair.  Requires all
 // CTAs co-resident (cooperative launch).  The CTA barrier orders the CTA's
 // writes before thread 0's gpu-scope fence (cumulativity), as in
@@ -167,6 +177,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     for (int q = 0; q < 16; ++q)
         if (mine[q] >= 0) atomicAdd(&s_cnt[mine[q]], 1);
     __syncthreads();
+    stamp(h, 2);
     // 2. CTA -> bucket; 3. stage the plane (warp 0)
     if (warp == 0) {
         const int P = gridDim.x;
@@ -201,6 +212,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     }
     __syncthreads();
     const int bucket = s_bucket, lo = s_lo, hi = s_hi;
+    stamp(h, 3);
     // 4. my rows: rank within the bucket (exclusive scan of per-thread counts)
     int cnt = 0;
 #pragma unroll
@@ -224,6 +236,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     }
     __syncthreads();
     const int nrows = hi - lo;
+    stamp(h, 4);
     // 5. stream rows; gathers from the staged plane
     float acc[NV][4];
 #pragma unroll
@@ -241,6 +254,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     };
     if (warp < nrows) load_row(warp, rec);
     if (bucket < GP) mbar_wait(bar, 0);
+    stamp(h, 5);
     for (int rr = warp; rr < nrows; rr += kW) {
         const bool more = rr + kW < nrows;
         if (more) load_row(rr + kW, nxt);
@@ -260,6 +274,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
             for (int v = 0; v < NV; ++v) rec[v] = nxt[v];
         }
     }
+    stamp(h, 6);
     // 6. fixed-order reduction over warps -> this CTA's partial
     __syncthreads();
     float* s_red = reinterpret_cast<float*>(smem);
@@ -284,9 +299,11 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     __shared__ float s_luts[kMaxHeadLayers][256];
     __shared__ __align__(8) uint64_t s_bar;
     const int P = gridDim.x, c = blockIdx.x;
+    stamp(h, 0);
     if (threadIdx.x == 0) mbar_init(&s_bar, 1);
     for (int l = 0; l < h.nl; ++l) s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];  // one round trip
     __syncthreads();
+    stamp(h, 1);
     int* s_m = reinterpret_cast<int*>(smem);  // row-split scratch (after layer 0)
     for (int l = 0; l < h.nl; ++l) {
         const DevLayer& L = h.L[l];
@@ -313,9 +330,12 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
                 reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, r0, r1, s_m, s_t, h.err);
             }
             __syncthreads();
+            if (l == 1) stamp(h, 9);
             rowsplit_layer(L, r0, r1, s_m, s_t, s_lut, s_acc, part_out);
         }
+        stamp(h, l == 0 ? 7 : 10);
         grid_sync(h.bar);
+        stamp(h, l == 0 ? 8 : 11);
     }
     // final: outputs [c*out/P, (c+1)*out/P) of the last layer, one warp each
     const DevLayer& L = h.L[h.nl - 1];
@@ -339,6 +359,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) h.y[j] = v + (L.bias_sum ? L.bias_sum[j] : 0.0);
     }
+    stamp(h, 12);
 }
 
 }  // namespace

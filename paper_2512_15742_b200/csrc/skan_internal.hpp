@@ -125,6 +125,7 @@ struct HeadB1Args {
     float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
     unsigned* bar;     // grid barrier {count, generation}
     int* err;
+    unsigned long long* timeline;  // optional: [grid][16] %globaltimer stamps per phase
 };
 bool head_b1_supported(const DevLayer* L, int nl);
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, bool* planes0, int* nv);

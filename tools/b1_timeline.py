@@ -1,0 +1,57 @@
+"""Phase timeline of the persistent batch-1 head kernel (skan_head_b1.cu).
+
+Runs the cfg2 head at batch 1 with L2 flushed before each forward and prints,
+per phase, the min / median / max over CTAs of the %globaltimer stamp
+relative to the earliest kernel start (microseconds).
+
+    python tools/b1_timeline.py [--reps 5]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_15742_b200 as hq  # noqa: E402
+from paper_2512_15742_b200 import _lib, synthetic  # noqa: E402
+
+PHASES = {0: "start", 1: "luts", 2: "locate+hist", 3: "alloc+tma", 4: "rowlist", 5: "plane ready",
+          6: "rows done", 7: "L0 partial", 8: "grid sync 1", 9: "L1 reduce+locate", 10: "L1 rows",
+          11: "grid sync 2", 12: "end"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    cn = synthetic.synthetic_head()
+    model = hq.build_model(cn)
+    ws = hq.make_workspace(model, 1)
+    grid = _lib.lib().skan_head_b1_grid(model.handle)
+    stamps = torch.zeros(grid * 16, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().skan_debug_b1_timeline(ws.handle, stamps.data_ptr()))
+    x = torch.from_numpy(synthetic.synthetic_inputs(1, 2048, seed=1)).cuda()
+    y = torch.zeros(20, dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    for rep in range(args.reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        stamps.zero_()
+        hq.forward_async(model, x, 1, y, ws)
+        torch.cuda.synchronize()
+        s = stamps.view(grid, 16).cpu().numpy().astype(np.float64)
+        t0 = s[:, 0].min()
+        print(f"rep {rep}: kernel span {(s[:, 12].max() - t0) / 1e3:.2f} us")
+        for p, name in PHASES.items():
+            col = s[:, p]
+            col = col[col > 0]
+            if col.size == 0:
+                continue
+            rel = (col - t0) / 1e3
+            print(f"   {p:2d} {name:18s} min {rel.min():7.2f}  med {np.median(rel):7.2f}  max {rel.max():7.2f}")
+
+
+if __name__ == "__main__":
+    main()
