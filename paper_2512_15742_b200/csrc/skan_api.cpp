@@ -199,9 +199,10 @@ struct skan_head {
     uint64_t edges = 0;
     int in_dim = 0, out_dim = 0, max_width = 0;
     // batch-1 persistent kernel plan (skan_head_b1.cu)
-    bool b1_ok = false, b1_planes0 = false;
+    bool b1_ok = false;
     int b1_grid = 0, b1_nv = 0;
     size_t b1_smem = 0;
+    skan::HeadB1Args b1_plan{};  // layers + shared-memory plan; per-call pointers filled at launch
 };
 
 struct skan_workspace {
@@ -527,8 +528,10 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
     // co-resident (checked against the occupancy calculator at its smem size)
     const int nl = static_cast<int>(h->dl.size());
     if (skan::head_b1_supported(h->dl.data(), nl)) {
-        h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_planes0, &h->b1_nv);
-        if (h->b1_smem <= 200 * 1024) {
+        h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan, &h->b1_nv);
+        h->b1_plan.nl = nl;
+        for (int l = 0; l < nl; ++l) h->b1_plan.L[l] = h->dl[l];
+        if (h->b1_smem <= 227 * 1024) {
             h->b1_ok = true;
             h->b1_grid = h->num_sms;
         }
@@ -651,10 +654,7 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
         ws->last_x = x;
         if (B == 1 && h->b1_ok && ws->b1_part) {
             // the whole head in one persistent cooperative kernel
-            skan::HeadB1Args a{};
-            a.nl = nl;
-            for (int l = 0; l < nl; ++l) a.L[l] = h->dl[l];
-            a.planes0 = h->b1_planes0;
+            skan::HeadB1Args a = h->b1_plan;
             a.x = x;
             a.y = y;
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
@@ -827,8 +827,8 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         if (h->b1_ok) {
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
-            ws->b1_bar = static_cast<unsigned*>(alloc(2 * sizeof(unsigned)));
-            skan::cuda_check(cudaMemset(ws->b1_bar, 0, 2 * sizeof(unsigned)), "cudaMemset");
+            ws->b1_bar = static_cast<unsigned*>(alloc(skan::kHeadB1BarrierWords * sizeof(unsigned)));
+            skan::cuda_check(cudaMemset(ws->b1_bar, 0, skan::kHeadB1BarrierWords * sizeof(unsigned)), "cudaMemset");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));

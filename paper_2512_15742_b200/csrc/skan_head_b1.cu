@@ -7,16 +7,18 @@
 //     uses the same bracket m_i, so rows are bucketed by bracket and each CTA
 //     serves a share of ONE bucket with that bucket's codebook pair plane
 //     P_m[k] = (c[k][m], c[k][m+1]) staged in shared memory by a TMA bulk
-//     copy; the 2-byte codebook gathers hit shared memory instead of costing
-//     a 32-byte L2 sector and an L1 wavefront each;
+//     copy, together with its rows' records (one more bulk copy per row):
+//     a single DRAM round trip, then every 2-byte codebook gather hits
+//     shared memory instead of costing a 32-byte sector + an L1 wavefront;
 //   * later layers are split by input rows across CTAs; each CTA reduces
 //     exactly the previous-layer outputs it consumes (fixed order, double),
-//     adds their bias sums, and locates them;
+//     adds their bias sums and locates them; its records were bulk-copied
+//     to shared memory at kernel start;
 //   * the last layer's partials are reduced by a few CTAs into y.
 // All summation orders are fixed functions of the launch shape and the
 // bracket histogram: results are bitwise reproducible run to run.
-// int8 tables with <= 65536-row codebooks (FMT_I8_R32) only; other heads
-// use the multi-kernel path.
+// int8 tables with <= 65536-row codebooks (FMT_I8_R32); other heads use the
+// multi-kernel path.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,10 +31,11 @@ namespace {
 
 using namespace dev;
 
-constexpr int kT = 256;   // threads per CTA
+constexpr int kT = 256;  // threads per CTA
 constexpr int kW = kT / 32;
+constexpr size_t kPrefetchBytes = 16 * 1024;  // row-split records prefetched at kernel start
 
-// Optional phase timeline (debug/profiling): thread 0 of each CTA stamps
+// Optional phase timeline (profiling hook): thread 0 of each CTA stamps
 // %globaltimer (ns) at fixed phase ids.
 __device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
     if (h.timeline && threadIdx.x == 0) {
@@ -42,22 +45,34 @@ __device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
     }
 }
 
-// Generation grid barrier over a {count, generation} pair.  Requires all
-// CTAs co-resident (cooperative launch).  The CTA barrier orders the CTA's
-// writes before thread 0's gpu-scope fence (cumulativity), as in
-// cooperative_groups::grid_group::sync.
+// Two-level generation grid barrier: CTAs arrive on one of kSub
+// sub-counters; the last of each group arrives on the top counter; the last
+// top arrival resets and bumps the generation.  bar = {top, gen, sub[kSub]}.
+// The CTA barrier orders the CTA's writes before thread 0's gpu-scope fence
+// (cumulativity), as in cooperative_groups::grid_group::sync.
+constexpr int kSub = 16;
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned* vgen = bar + 1;
         const unsigned gen = *vgen;
+        const int g = blockIdx.x % kSub;
+        const unsigned members = (gridDim.x - g + kSub - 1) / kSub;
+        const unsigned ngroups = gridDim.x < kSub ? gridDim.x : kSub;
         __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
+        bool release = false;
+        if (atomicAdd(bar + 2 + g, 1u) == members - 1) {
+            bar[2 + g] = 0;
+            if (atomicAdd(bar, 1u) == ngroups - 1) {
+                bar[0] = 0;
+                release = true;
+            }
+        }
+        if (release) {
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
-            while (*vgen == gen) __nanosleep(20);
+            while (*vgen == gen) __nanosleep(16);
         }
         __threadfence();
     }
@@ -65,13 +80,12 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 }
 
 // Reduce rows [r0, r1) of the previous layer's per-CTA partials
-// prev[z*width + i] (z < nz) in fixed order: C lanes per row, ascending z
-// per lane, then a fixed butterfly; + bias; then locate with layer L's grid.
+// prev[z*width + i] (z < nz): C lanes per row, ascending z per lane, then a
+// fixed butterfly; + bias; then locate with layer L's grid.  All of a
+// thread's loads are issued before any is consumed.
 __device__ void reduce_rows(const float* prev, int width, int nz, const double* bias, const DevLayer& L, int r0,
                             int r1, int* s_m, float* s_t, int* err) {
     const int n = r1 - r0;
-    // as many lanes per row as keep every thread busy (<= 32): few rows, many
-    // splits -> each thread loads <= ~8 partials, all issued at once
     int C = 1;
     while (C < 32 && (C * 2) * n <= kT) C <<= 1;
     const int c = threadIdx.x & (C - 1), groups = kT / C;
@@ -102,23 +116,24 @@ __device__ void reduce_rows(const float* prev, int width, int nz, const double* 
 
 // Row-split layer: this CTA's rows [r0, r1) (brackets in s_m/s_t), all
 // outputs.  Warp w takes rows w, w+8, ...; lane l outputs l, l+32, ...;
-// per-warp accumulators in shared memory; fixed-order sum over warps.
+// records from shared memory when prefetched (s_rec != nullptr); per-warp
+// accumulators in shared memory; fixed-order sum over warps.
 __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m, const float* s_t,
-                               const float* s_lut, float* s_acc, float* part_out) {
+                               const uint32_t* s_rec, const float* s_lut, float* s_acc, float* part_out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int q = threadIdx.x; q < kW * L.out; q += kT) s_acc[q] = 0.f;
     __syncthreads();
     float* acc = s_acc + warp * L.out;
     for (int rl = warp; rl < r1 - r0; rl += kW) {
-        const int i = r0 + rl, m = s_m[rl];
+        const int m = s_m[rl];
         const float t = s_t[rl];
-        const uint32_t* rec = L.rec + static_cast<size_t>(i) * L.out;
+        const uint32_t* rec = s_rec ? s_rec + static_cast<size_t>(rl) * L.out
+                                    : L.rec + static_cast<size_t>(r0 + rl) * L.out;
         const uint16_t* plane = L.pair8 + static_cast<size_t>(m) * L.K;
         for (int j = lane; j < L.out; j += 128) {  // 4 independent edges per lane per step
-            uint32_t r[4];
+            uint32_t r[4], p[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) r[e] = j + 32 * e < L.out ? __ldg(rec + j + 32 * e) : 0u;
-            uint32_t p[4];
+            for (int e = 0; e < 4; ++e) r[e] = j + 32 * e < L.out ? rec[j + 32 * e] : 0u;
 #pragma unroll
             for (int e = 0; e < 4; ++e) p[e] = j + 32 * e < L.out ? __ldg(plane + (r[e] & 0xFFFFu)) : 0u;
 #pragma unroll
@@ -138,52 +153,84 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
     }
 }
 
-// Pair-plane layer 0 (see k_fwd_planes in skan_kernels.cu for the scheme).
+// Pair-plane layer 0.  Shared memory: [plane K*2 B][records rec_cap rows x
+// out x 4 B]; rows beyond rec_cap (only for very skewed shapes) read their
+// records from global memory.
 template <int NV>
 __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const float* s_lut, uint64_t* bar,
                               float* part_out) {
     const DevLayer& L = h.L[0];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int GP = L.G - 1;
+    __shared__ int s_whist[kW][32];
     __shared__ int s_cnt[32];
     __shared__ int s_scan[kW];
     __shared__ int s_bucket, s_lo, s_hi;
+    __shared__ int s_rows[128];
+    __shared__ float s_trow[128];
     uint16_t* s_plane = reinterpret_cast<uint16_t*>(smem);
     const uint32_t plane_bytes = static_cast<uint32_t>(L.K) * 2u;
-    int* s_rows = reinterpret_cast<int*>(smem + ((plane_bytes + 127u) & ~127u));
-    float* s_tall = reinterpret_cast<float*>(s_rows + L.in);
-    if (tid < 32) s_cnt[tid] = 0;
-    __syncthreads();
-    // 1. locate all inputs (contiguous slice per thread) + histogram
-    const int per = (L.in + kT - 1) / kT;
+    uint32_t* s_rec = reinterpret_cast<uint32_t*>(smem + ((plane_bytes + 127u) & ~127u));
+    const uint32_t row_bytes = static_cast<uint32_t>(L.out) * 4u;
+
+    // 1. inputs of this thread (contiguous slice) -> brackets, two lock-step groups of 8
+    const int per = (L.in + kT - 1) / kT;  // <= 16
     const int i0 = tid * per;
     int mine[16];
-    double xv[16];
+    float tmine[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) xv[q] = (q < per && i0 + q < L.in) ? h.x[i0 + q] : 0.0;  // one round trip
+    for (int g = 0; g < 2; ++g) {
+        double xv[8], tt[8];
+        bool ok[8];
+        int mm[8];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        mine[q] = -1;
-        const int i = i0 + q;
-        if (q < per && i < L.in) {
-            int m;
-            double t;
-            bracket_of(L.lo, L.hi, L.G, L.dx, xv[q], h.err, m, t);
-            mine[q] = m;
-            s_tall[i] = static_cast<float>(t);
+        for (int q = 0; q < 8; ++q) {
+            const int k = g * 8 + q;
+            ok[q] = k < per && i0 + k < L.in;
+            xv[q] = ok[q] ? h.x[i0 + k] : 0.0;
+        }
+        if (g * 8 < per) {
+            locate_many<8>(L.lo, L.hi, L.G, L.dx, xv, ok, mm, tt, h.err);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                mm[q] = -1;
+                tt[q] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            mine[g * 8 + q] = ok[q] ? mm[q] : -1;
+            tmine[g * 8 + q] = static_cast<float>(tt[q]);
         }
     }
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-        if (mine[q] >= 0) atomicAdd(&s_cnt[mine[q]], 1);
-    __syncthreads();
     stamp(h, 2);
-    // 2. CTA -> bucket; 3. stage the plane (warp 0)
+    // 2. histogram: per-warp ballot counts (lane b counts bracket b), then a
+    //    fixed-order sum over warps -- no atomics
+    int wcnt = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if (q >= per) break;
+        for (int b = 0; b < GP; ++b) {
+            const int cb = __popc(__ballot_sync(0xFFFFFFFFu, mine[q] == b));
+            if (lane == b) wcnt += cb;
+        }
+    }
+    s_whist[warp][lane] = wcnt;
+    __syncthreads();
+    if (tid < 32) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) s += s_whist[w][tid];
+        s_cnt[tid] = s;
+    }
+    __syncthreads();
+    // 3. CTA -> bucket (warp 0, lane b = bucket b; 32-bit math), plane TMA
     if (warp == 0) {
         const int P = gridDim.x;
         const int n = lane < GP ? s_cnt[lane] : 0;
         const int nonempty = __popc(__ballot_sync(0xFFFFFFFFu, n > 0));
-        const int alloc = n > 0 ? 1 + static_cast<int>(static_cast<long long>(P - nonempty) * n / L.in) : 0;
+        const int alloc = n > 0 ? 1 + (P - nonempty) * n / L.in : 0;
         int incl = alloc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -200,20 +247,23 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
         __syncwarp();
         if (hit && lane == b) {
             const int q = c - (incl - alloc);
-            s_lo = static_cast<int>(static_cast<long long>(n) * q / alloc);
-            s_hi = static_cast<int>(static_cast<long long>(n) * (q + 1) / alloc);
-        }
-        if (lane == 0 && hit) {
-            mbar_expect_tx(bar, plane_bytes);
-            const char* src = reinterpret_cast<const char*>(L.pair8 + static_cast<size_t>(b) * L.K);
-            for (uint32_t off = 0; off < plane_bytes; off += 32768u)
-                bulk_g2s(smem + off, src + off, min(32768u, plane_bytes - off), bar);
+            s_lo = n * q / alloc;
+            s_hi = n * (q + 1) / alloc;
         }
     }
     __syncthreads();
     const int bucket = s_bucket, lo = s_lo, hi = s_hi;
+    const int nrows = min(hi - lo, 128);
+    const int rec_rows = min(nrows, h.rec_cap);
+    if (tid == 0 && bucket < GP) {
+        mbar_expect_tx(bar, plane_bytes + static_cast<uint32_t>(rec_rows) * row_bytes);
+        const char* src = reinterpret_cast<const char*>(L.pair8 + static_cast<size_t>(bucket) * L.K);
+        for (uint32_t off = 0; off < plane_bytes; off += 32768u)
+            bulk_g2s(smem + off, src + off, min(32768u, plane_bytes - off), bar);
+    }
     stamp(h, 3);
-    // 4. my rows: rank within the bucket (exclusive scan of per-thread counts)
+    // 4. my rows: rank within the bucket (exclusive scan of per-thread counts);
+    //    the owning thread issues that row's record bulk copy
     int cnt = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) cnt += mine[q] == bucket;
@@ -230,48 +280,43 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         if (mine[q] == bucket) {
-            if (rank >= lo && rank < hi) s_rows[rank - lo] = i0 + q;
+            const int r = rank - lo;
+            if (r >= 0 && r < nrows) {
+                s_rows[r] = i0 + q;
+                s_trow[r] = tmine[q];
+                if (r < rec_rows)
+                    bulk_g2s(s_rec + static_cast<size_t>(r) * L.out, L.rec + static_cast<size_t>(i0 + q) * L.out,
+                             row_bytes, bar);
+            }
             ++rank;
         }
     }
     __syncthreads();
-    const int nrows = hi - lo;
     stamp(h, 4);
-    // 5. stream rows; gathers from the staged plane
+    if (bucket < GP) mbar_wait(bar, 0);
+    stamp(h, 5);
+    // 5. rows: warp w takes rows w, w+8, ...; gathers from the staged plane
     float acc[NV][4];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[v][e] = 0.f;
-    uint4 rec[NV], nxt[NV];
-    auto load_row = [&](int rr, uint4* dst) {
-        const uint32_t* base = L.rec + static_cast<size_t>(s_rows[rr]) * L.out;
+    for (int rr = warp; rr < nrows; rr += kW) {
+        const float t = s_trow[rr];
+        const uint32_t* base = rr < rec_rows ? s_rec + static_cast<size_t>(rr) * L.out
+                                             : L.rec + static_cast<size_t>(s_rows[rr]) * L.out;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const int j = v * 128 + lane * 4;
-            dst[v] = j < L.out ? __ldg(reinterpret_cast<const uint4*>(base + j)) : make_uint4(0, 0, 0, 0);
-        }
-    };
-    if (warp < nrows) load_row(warp, rec);
-    if (bucket < GP) mbar_wait(bar, 0);
-    stamp(h, 5);
-    for (int rr = warp; rr < nrows; rr += kW) {
-        const bool more = rr + kW < nrows;
-        if (more) load_row(rr + kW, nxt);
-        const float t = s_tall[s_rows[rr]];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const uint32_t r4[4] = {rec[v].x, rec[v].y, rec[v].z, rec[v].w};
+            if (j >= L.out) break;
+            const uint4 r = *reinterpret_cast<const uint4*>(base + j);
+            const uint32_t r4[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const uint32_t p = s_plane[r4[e] & 0xFFFFu];
                 const float c0 = i8lo(p), c1 = i8hi(p);
                 acc[v][e] = fmaf(s_lut[(r4[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[v][e]);
             }
-        }
-        if (more) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) rec[v] = nxt[v];
         }
     }
     stamp(h, 6);
@@ -293,28 +338,60 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     }
 }
 
+__device__ __forceinline__ void rows_of(const DevLayer& L, int c, int P, int& r0, int& r1) {
+    r0 = static_cast<int>(static_cast<long long>(L.in) * c / P);
+    r1 = static_cast<int>(static_cast<long long>(L.in) * (c + 1) / P);
+}
+
 template <int NV>
 __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float s_luts[kMaxHeadLayers][256];
-    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ __align__(8) uint64_t s_bar[2];  // [0] layer-0 staging, [1] row-split prefetch
     const int P = gridDim.x, c = blockIdx.x;
     stamp(h, 0);
-    if (threadIdx.x == 0) mbar_init(&s_bar, 1);
-    for (int l = 0; l < h.nl; ++l) s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];  // one round trip
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
+    __syncthreads();
+    // row-split layers' records of this CTA (contiguous rows) are bulk-copied
+    // now into the tail of shared memory, consumed after the grid barriers
+    unsigned char* s_pref = smem + h.pref_offset;
+    if (threadIdx.x == 0 && h.pref_mask) {
+        uint32_t total = 0;
+        for (int l = 0; l < h.nl; ++l) {
+            if (!(h.pref_mask >> l & 1)) continue;
+            int r0, r1;
+            rows_of(h.L[l], c, P, r0, r1);
+            total += static_cast<uint32_t>(r1 - r0) * h.L[l].out * 4u;
+        }
+        mbar_expect_tx(&s_bar[1], total);
+        uint32_t off = 0;
+        for (int l = 0; l < h.nl; ++l) {
+            if (!(h.pref_mask >> l & 1)) continue;
+            int r0, r1;
+            rows_of(h.L[l], c, P, r0, r1);
+            const uint32_t bytes = static_cast<uint32_t>(r1 - r0) * h.L[l].out * 4u;
+            if (bytes) bulk_g2s(s_pref + off, h.L[l].rec + static_cast<size_t>(r0) * h.L[l].out, bytes, &s_bar[1]);
+            off += bytes;
+        }
+    }
+    for (int l = 0; l < h.nl; ++l) s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];
     __syncthreads();
     stamp(h, 1);
     int* s_m = reinterpret_cast<int*>(smem);  // row-split scratch (after layer 0)
+    uint32_t pref_off = 0;
+    bool pref_ready = false;
     for (int l = 0; l < h.nl; ++l) {
         const DevLayer& L = h.L[l];
         float* part_out = h.part[l & 1];
         const float* s_lut = s_luts[l];
-        __syncthreads();
         if (l == 0 && h.planes0) {
-            planes_layer0<NV>(h, smem, s_lut, &s_bar, part_out);
+            planes_layer0<NV>(h, smem, s_lut, &s_bar[0], part_out);
         } else {
-            const int r0 = static_cast<int>(static_cast<long long>(L.in) * c / P);
-            const int r1 = static_cast<int>(static_cast<long long>(L.in) * (c + 1) / P);
+            int r0, r1;
+            rows_of(L, c, P, r0, r1);
             const int nr = r1 - r0;
             float* s_t = reinterpret_cast<float*>(s_m + nr);
             float* s_acc = s_t + nr;
@@ -329,9 +406,18 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             } else {
                 reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, r0, r1, s_m, s_t, h.err);
             }
+            const uint32_t* s_rec = nullptr;
+            if (h.pref_mask >> l & 1) {
+                if (!pref_ready) {
+                    mbar_wait(&s_bar[1], 0);
+                    pref_ready = true;
+                }
+                s_rec = reinterpret_cast<const uint32_t*>(s_pref + pref_off);
+                pref_off += static_cast<uint32_t>(nr) * L.out * 4u;
+            }
             __syncthreads();
             if (l == 1) stamp(h, 9);
-            rowsplit_layer(L, r0, r1, s_m, s_t, s_lut, s_acc, part_out);
+            rowsplit_layer(L, r0, r1, s_m, s_t, s_rec, s_lut, s_acc, part_out);
         }
         stamp(h, l == 0 ? 7 : 10);
         grid_sync(h.bar);
@@ -364,8 +450,8 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
 
 }  // namespace
 
-// Eligibility: every layer int8 with <= 65536 codebook rows (4-byte records),
-// G-1 <= 32 brackets, and the layer-0 plane + row list in shared memory.
+// Eligibility: every layer int8 with <= 65536-row codebooks (4-byte
+// records), G-1 <= 32 brackets.
 bool head_b1_supported(const DevLayer* L, int nl) {
     if (nl < 1 || nl > kMaxHeadLayers) return false;
     for (int l = 0; l < nl; ++l) {
@@ -374,26 +460,56 @@ bool head_b1_supported(const DevLayer* L, int nl) {
     return true;
 }
 
-size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, bool* planes0, int* nv) {
+// Shared-memory plan: [phase region][prefetched row-split records].  The
+// phase region holds layer 0's plane + staged records (pair-plane layer) or
+// a row-split layer's brackets and per-warp accumulators.  Fills
+// h->planes0 / rec_cap / pref_mask / pref_offset.
+size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* nv) {
     const DevLayer& L0 = L[0];
-    *planes0 = L0.out % 4 == 0 && L0.out <= 1536 && L0.in <= 16 * kT && L0.K % 8 == 0 &&
-               static_cast<size_t>(L0.K) * 2 <= 150 * 1024 && static_cast<long long>(L0.in) * L0.out >= 256LL * 1024;
+    const size_t kBudget = 220 * 1024;
+    h->planes0 = L0.out % 4 == 0 && L0.out <= 1536 && L0.in <= 16 * kT && L0.K % 8 == 0 &&
+                 static_cast<size_t>(L0.K) * 2 <= 144 * 1024 && L0.G - 1 <= 32 &&
+                 static_cast<long long>(L0.in) * L0.out >= 256LL * 1024 &&
+                 num_sms - (L0.G - 1) > 0 && L0.in / (num_sms - (L0.G - 1)) + 2 <= 128;  // s_rows[128]
     const int groups = (L0.out + 127) / 128;
     *nv = groups <= 2 ? 2 : (groups <= 4 ? 4 : (groups <= 8 ? 8 : 12));
-    size_t need = 0;
-    if (*planes0) {
+    // prefetch: row-split layers whose per-CTA record block is small
+    size_t pref = 0;
+    h->pref_mask = 0;
+    for (int l = h->planes0 ? 1 : 0; l < nl; ++l) {
+        const int rows = (L[l].in + num_sms - 1) / num_sms;
+        const size_t b = static_cast<size_t>(rows) * L[l].out * 4;
+        if (L[l].out % 4 == 0 && pref + b <= kPrefetchBytes) {
+            h->pref_mask |= 1 << l;
+            pref += b;
+        }
+    }
+    size_t phase = 0;
+    h->rec_cap = 0;
+    if (h->planes0) {
         const size_t plane = (static_cast<size_t>(L0.K) * 2 + 127) / 128 * 128;
-        const size_t a = plane + static_cast<size_t>(L0.in) * (sizeof(int) + sizeof(float));
-        const size_t b = static_cast<size_t>(kW) * 128 * (*nv) * sizeof(float);
-        need = a > b ? a : b;
+        const size_t red = static_cast<size_t>(kW) * 128 * (*nv) * sizeof(float);
+        const size_t row = static_cast<size_t>(L0.out) * 4;
+        // rows per CTA < in / (P - buckets) + 1
+        const int spare = num_sms - (L0.G - 1) > 0 ? num_sms - (L0.G - 1) : 1;
+        const int want = L0.in / spare + 2;
+        const size_t avail = kBudget > plane + pref ? kBudget - plane - pref : 0;
+        size_t cap = avail / row;
+        if (cap > static_cast<size_t>(want)) cap = want;
+        if (cap > 128) cap = 128;
+        h->rec_cap = static_cast<int>(cap);
+        phase = plane + cap * row;
+        if (red > phase) phase = red;
     }
     for (int l = 0; l < nl; ++l) {
-        if (l == 0 && *planes0) continue;
+        if (l == 0 && h->planes0) continue;
         const int nr = (L[l].in + num_sms - 1) / num_sms + 1;
         const size_t s = static_cast<size_t>(nr) * 8 + static_cast<size_t>(kW) * L[l].out * sizeof(float);
-        if (s > need) need = s;
+        if (s > phase) phase = s;
     }
-    return need;
+    phase = (phase + 127) / 128 * 128;
+    h->pref_offset = static_cast<uint32_t>(phase);
+    return phase + pref;
 }
 
 void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s) {

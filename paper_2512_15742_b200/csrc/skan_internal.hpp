@@ -123,12 +123,18 @@ struct HeadB1Args {
     const double* x;   // [in]
     double* y;         // [out]
     float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
-    unsigned* bar;     // grid barrier {count, generation}
+    unsigned* bar;     // grid barrier {top, generation, 16 sub-counters}
     int* err;
     unsigned long long* timeline;  // optional: [grid][16] %globaltimer stamps per phase
+    int rec_cap;           // layer-0 rows whose records are staged in shared memory
+    unsigned pref_mask;    // row-split layers whose records are prefetched at kernel start
+    unsigned pref_offset;  // byte offset of the prefetch region in dynamic shared memory
 };
+constexpr int kHeadB1BarrierWords = 2 + 16;
 bool head_b1_supported(const DevLayer* L, int nl);
-size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, bool* planes0, int* nv);
+// Shared-memory plan of the batch-1 kernel; fills h->planes0, rec_cap,
+// pref_mask, pref_offset.
+size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* nv);
 void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s);
 
 // Workspace device buffers (one forward stream).
