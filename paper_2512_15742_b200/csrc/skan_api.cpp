@@ -531,9 +531,9 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
         h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan, &h->b1_nv);
         h->b1_plan.nl = nl;
         for (int l = 0; l < nl; ++l) h->b1_plan.L[l] = h->dl[l];
-        if (h->b1_smem <= 227 * 1024) {
+        h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->b1_nv, h->num_sms);
+        if (h->b1_grid > 0) {
             h->b1_ok = true;
-            h->b1_grid = h->num_sms;
         }
     }
     return h.release();

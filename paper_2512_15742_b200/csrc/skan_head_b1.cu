@@ -466,7 +466,7 @@ bool head_b1_supported(const DevLayer* L, int nl) {
 // h->planes0 / rec_cap / pref_mask / pref_offset.
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* nv) {
     const DevLayer& L0 = L[0];
-    const size_t kBudget = 220 * 1024;
+    const size_t kBudget = 204 * 1024;  // dynamic; + ~10.5 KB static + 1 KB reserved <= 227 KB
     h->planes0 = L0.out % 4 == 0 && L0.out <= 1536 && L0.in <= 16 * kT && L0.K % 8 == 0 &&
                  static_cast<size_t>(L0.K) * 2 <= 144 * 1024 && L0.G - 1 <= 32 &&
                  static_cast<long long>(L0.in) * L0.out >= 256LL * 1024 &&
@@ -512,14 +512,31 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* 
     return phase + pref;
 }
 
-void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s) {
-    void (*k)(HeadB1Args);
+static void (*head_b1_kernel(int nv))(HeadB1Args) {
     switch (nv) {
-        case 2: k = k_head_b1<2>; break;
-        case 4: k = k_head_b1<4>; break;
-        case 8: k = k_head_b1<8>; break;
-        default: k = k_head_b1<12>; break;
+        case 2: return k_head_b1<2>;
+        case 4: return k_head_b1<4>;
+        case 8: return k_head_b1<8>;
+        default: return k_head_b1<12>;
     }
+}
+
+int head_b1_max_grid(size_t smem, int nv, int num_sms) {
+    auto k = head_b1_kernel(nv);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kT, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm >= 1 ? num_sms : 0;
+}
+
+void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s) {
+    auto k = head_b1_kernel(nv);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);

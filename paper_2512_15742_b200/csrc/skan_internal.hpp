@@ -136,6 +136,9 @@ bool head_b1_supported(const DevLayer* L, int nl);
 // pref_mask, pref_offset.
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* nv);
 void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s);
+// Grid for which all CTAs are co-resident (one per SM), or 0 if the kernel
+// cannot be resident at this shared-memory size.
+int head_b1_max_grid(size_t smem, int nv, int num_sms);
 
 // Workspace device buffers (one forward stream).
 struct DevScratch {
