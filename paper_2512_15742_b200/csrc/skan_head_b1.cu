@@ -45,30 +45,19 @@ __device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
     }
 }
 
-// Two-level generation grid barrier: CTAs arrive on one of kSub
-// sub-counters; the last of each group arrives on the top counter; the last
-// top arrival resets and bumps the generation.  bar = {top, gen, sub[kSub]}.
-// The CTA barrier orders the CTA's writes before thread 0's gpu-scope fence
-// (cumulativity), as in cooperative_groups::grid_group::sync.
-constexpr int kSub = 16;
+// Generation grid barrier over bar = {count, gen}: one same-address atomic
+// per CTA (L2 serialises ~148 of them in well under a round trip), the last
+// arrival resets the count and bumps the generation.  The CTA barrier
+// orders the CTA's writes before thread 0's gpu-scope fence (cumulativity),
+// as in cooperative_groups::grid_group::sync.
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned* vgen = bar + 1;
         const unsigned gen = *vgen;
-        const int g = blockIdx.x % kSub;
-        const unsigned members = (gridDim.x - g + kSub - 1) / kSub;
-        const unsigned ngroups = gridDim.x < kSub ? gridDim.x : kSub;
         __threadfence();
-        bool release = false;
-        if (atomicAdd(bar + 2 + g, 1u) == members - 1) {
-            bar[2 + g] = 0;
-            if (atomicAdd(bar, 1u) == ngroups - 1) {
-                bar[0] = 0;
-                release = true;
-            }
-        }
-        if (release) {
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            bar[0] = 0;
             __threadfence();
             atomicAdd(bar + 1, 1u);
         } else {
