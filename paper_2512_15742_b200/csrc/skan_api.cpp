@@ -105,8 +105,9 @@ int device_format(const skan_layer_header& h) {
 uint64_t device_bytes(const skan_layer_header& h) {
     const uint64_t e = mul_checked(h.in_dim, h.out_dim);
     const int fmt = device_format(h);
-    uint64_t b = 0;
-    if (fmt == skan::FMT_DENSE) return align_up(mul_checked(mul_checked(e, h.grid_size), 4));
+    // node positions + their integer keys (fast knot selection), every format
+    uint64_t b = 2 * align_up(mul_checked(h.grid_size, 8));
+    if (fmt == skan::FMT_DENSE) return add_checked(b, align_up(mul_checked(mul_checked(e, h.grid_size), 4)));
     const uint64_t kg = mul_checked(h.k, h.grid_size);
     // int8 codebook: rows padded to 16 B (one 128-bit load per row) plus the
     // (c[m], c[m+1]) pair table (one 2-byte gather per edge-sample)
@@ -440,6 +441,22 @@ void upload(skan_head* h, std::vector<Staged>& st) {
         d.cs = s.h.codebook_scale;
         d.bs = s.h.bias_scale;
         const uint64_t begin = cur;
+        {  // node positions exactly as node_position (kan.cpp:21-26) + integer keys
+            const int G = d.G;
+            std::vector<double> node(G);
+            std::vector<long long> key(G);
+            for (int i = 0; i < G; ++i) {
+                node[i] = i == 0 ? d.lo : (i == G - 1 ? d.hi : d.lo + static_cast<double>(i) * d.dx);
+                long long bits;
+                std::memcpy(&bits, &node[i], 8);
+                if (bits == static_cast<long long>(0x8000000000000000ULL)) bits = 0;
+                key[i] = bits ^ ((bits >> 63) & 0x7FFFFFFFFFFFFFFFLL);
+            }
+            d.node = static_cast<const double*>(put(node.data(), node.size() * 8));
+            d.nkey = static_cast<const long long*>(put(key.data(), key.size() * 8));
+            d.lo_f = static_cast<float>(d.lo);
+            d.inv_dx_f = static_cast<float>(1.0 / d.dx);
+        }
         switch (d.fmt) {
             case skan::FMT_DENSE:
                 d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
@@ -614,10 +631,7 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const std::vector<
     a.y = out;
     a.has_next = next != nullptr;
     if (next) {
-        a.nlo = next->lo;
-        a.nhi = next->hi;
-        a.ndx = next->dx;
-        a.nG = next->G;
+        a.N = *next;
         a.bm_out = bm[(l + 1) & 1];
         a.bt_out = bt[(l + 1) & 1];
     }

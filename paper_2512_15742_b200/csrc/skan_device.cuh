@@ -60,6 +60,61 @@ __device__ __forceinline__ bool locate_dev(double lo, double hi, int G, double d
     return clamped;
 }
 
+// ---------------------------------------------------------------------------
+// Division-free knot selection for the fast path.  locate()'s floor-then-
+// correct sequence always ends at the unique i in [0, G-2] with
+// node(i) <= x < node(i+1) over the reference's own node positions
+// (pinned by tests/test_oracle.py::test_bracket_is_the_node_search_the_fast_path_uses),
+// so the bracket index is found with an fp32 estimate and exact comparisons
+// against precomputed node keys -- integer compares, no FP64 division (the
+// FP64 pipe is narrow: one exact locate costs ~2 dependent 160-cycle
+// divisions).  t is then computed as float(x - node(i)) * (1/dx) in fp32,
+// within an ulp of float(locate().t) -- inside the fast path's tolerance;
+// the exact path keeps locate_dev.
+
+// Order-preserving int64 key of a non-NaN double; +0 and -0 share key 0
+// (they compare equal as doubles).
+__device__ __forceinline__ long long dkey(double d) {
+    long long b = __double_as_longlong(d);
+    if (b == static_cast<long long>(0x8000000000000000ULL)) b = 0;
+    return b ^ ((b >> 63) & 0x7FFFFFFFFFFFFFFFLL);
+}
+
+__device__ __forceinline__ bool finite_bits(double d) {
+    return ((__double_as_longlong(d) >> 52) & 0x7FF) != 0x7FF;
+}
+
+// L.nkey[G] node keys, L.node[G] node positions, L.lo_f, L.inv_dx_f.
+__device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
+    if (!finite_bits(x)) {
+        *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
+        m = 0;
+        t = 0.f;
+        return;
+    }
+    const int G = L.G;
+    long long kx = dkey(x);
+    const long long klo = __ldg(L.nkey), khi = __ldg(L.nkey + G - 1);
+    if (kx < klo) {
+        kx = klo;
+        x = L.lo;
+    } else if (kx > khi) {
+        kx = khi;
+        x = L.hi;
+    }
+    int i = __float2int_rd((__double2float_rn(x) - L.lo_f) * L.inv_dx_f);
+    i = i < 0 ? 0 : (i > G - 2 ? G - 2 : i);
+    while (i < G - 2 && kx >= __ldg(L.nkey + i + 1)) ++i;
+    while (i > 0 && kx < __ldg(L.nkey + i)) --i;
+    float tt = 1.f;
+    if (kx < __ldg(L.nkey + i + 1)) {
+        tt = __double2float_rn(x - __ldg(L.node + i)) * L.inv_dx_f;
+        tt = tt < 0.f ? 0.f : (tt > 1.f ? 1.f : tt);
+    }
+    m = i;
+    t = tt;
+}
+
 // locate() for N independent inputs in lock step: the same operations as
 // locate_dev, restructured so the N division chains interleave (ILP)
 // instead of running back to back.  Bitwise identical results.

@@ -95,10 +95,10 @@ __device__ void reduce_rows(const float* prev, int width, int nz, const double* 
         for (int o = C >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (c == 0 && q < n) {
             int m;
-            double t;
-            bracket_of(L.lo, L.hi, L.G, L.dx, v + (bias ? bias[i] : 0.0), err, m, t);
+            float t;
+            fast_locate(L, v + (bias ? bias[i] : 0.0), err, m, t);
             s_m[q] = m;
-            s_t[q] = static_cast<float>(t);
+            s_t[q] = t;
         }
     }
 }
@@ -162,36 +162,19 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     uint32_t* s_rec = reinterpret_cast<uint32_t*>(smem + ((plane_bytes + 127u) & ~127u));
     const uint32_t row_bytes = static_cast<uint32_t>(L.out) * 4u;
 
-    // 1. inputs of this thread (contiguous slice) -> brackets, two lock-step groups of 8
+    // 1. inputs of this thread (contiguous slice) -> brackets (division-free)
     const int per = (L.in + kT - 1) / kT;  // <= 16
     const int i0 = tid * per;
     int mine[16];
     float tmine[16];
+    double xv[16];
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-        double xv[8], tt[8];
-        bool ok[8];
-        int mm[8];
+    for (int q = 0; q < 16; ++q) xv[q] = (q < per && i0 + q < L.in) ? h.x[i0 + q] : 0.0;  // one round trip
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int k = g * 8 + q;
-            ok[q] = k < per && i0 + k < L.in;
-            xv[q] = ok[q] ? h.x[i0 + k] : 0.0;
-        }
-        if (g * 8 < per) {
-            locate_many<8>(L.lo, L.hi, L.G, L.dx, xv, ok, mm, tt, h.err);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                mm[q] = -1;
-                tt[q] = 0.0;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            mine[g * 8 + q] = ok[q] ? mm[q] : -1;
-            tmine[g * 8 + q] = static_cast<float>(tt[q]);
-        }
+    for (int q = 0; q < 16; ++q) {
+        mine[q] = -1;
+        tmine[q] = 0.f;
+        if (q < per && i0 + q < L.in) fast_locate(L, xv[q], h.err, mine[q], tmine[q]);
     }
     stamp(h, 2);
     // 2. histogram: per-warp ballot counts (lane b counts bracket b), then a
@@ -385,13 +368,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             float* s_t = reinterpret_cast<float*>(s_m + nr);
             float* s_acc = s_t + nr;
             if (l == 0) {
-                for (int q = threadIdx.x; q < nr; q += kT) {
-                    int m;
-                    double t;
-                    bracket_of(L.lo, L.hi, L.G, L.dx, h.x[r0 + q], h.err, m, t);
-                    s_m[q] = m;
-                    s_t[q] = static_cast<float>(t);
-                }
+                for (int q = threadIdx.x; q < nr; q += kT) fast_locate(L, h.x[r0 + q], h.err, s_m[q], s_t[q]);
             } else {
                 reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, r0, r1, s_m, s_t, h.err);
             }

@@ -68,6 +68,9 @@ struct DevLayer {
     const uint16_t* pair8;   // int8 pair planes [G-1][K]: c[k][m] | c[k][m+1] << 8 — one 2-byte
                              // gather per edge-sample; plane m is contiguous (smem-stageable)
     int rs;                  // int8 codebook row stride in bytes (G rounded up to 16)
+    const double* node;      // [G] node positions exactly as kan.cpp:21-26 computes them
+    const long long* nkey;   // [G] their order-preserving integer keys (fast locate)
+    float lo_f, inv_dx_f;    // float(lo), float(1/dx): fast locate's estimate and t
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -101,8 +104,7 @@ struct FwdArgs {
     unsigned* counters;     // [jt * st], zero between launches
     double* y;              // [B][out]
     int has_next;
-    double nlo, nhi, ndx;
-    int nG;
+    DevLayer N;             // next layer (its knot grid), valid when has_next
     int* bm_out;            // next layer brackets, input-major [out][B]
     float* bt_out;
     int* err;

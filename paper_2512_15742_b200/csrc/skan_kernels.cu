@@ -20,97 +20,45 @@
 
 #include <cstdint>
 
+#include "skan_device.cuh"
 #include "skan_internal.hpp"
 
 namespace skan {
 namespace {
 
+using namespace dev;
+
 constexpr int kThreads = 128;  // threads per exact-kernel CTA
 constexpr int kIC = 64;        // inputs whose brackets are staged per smem pass (exact kernel)
 
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-// ---------------------------------------------------------------------------
-// Knot selection.  Every double operation is an explicit round-to-nearest
-// intrinsic so nvcc can neither contract lo + i*dx (kan.cpp:25) nor
-// (x - lo)/dx into an FMA: the bracket and t are bitwise the reference's.
-
-__device__ __forceinline__ double node_pos(double lo, double hi, int G, int i, double dx) {
-    if (i == 0) return lo;
-    if (i == G - 1) return hi;
-    return __dadd_rn(lo, __dmul_rn(static_cast<double>(i), dx));  // kan.cpp:21-26
-}
-
-__device__ __forceinline__ bool locate_dev(double lo, double hi, int G, double dx, double x,
-                                           int& idx, double& t) {
-    bool clamped = false;
-    if (x < lo) {
-        x = lo;
-        clamped = true;
-    } else if (x > hi) {
-        x = hi;
-        clamped = true;
-    }
-    int i = static_cast<int>(floor(__ddiv_rn(__dsub_rn(x, lo), dx)));
-    if (i < 0) i = 0;
-    if (i > G - 2) i = G - 2;
-    if (i < G - 2 && x >= node_pos(lo, hi, G, i + 1, dx)) {
-        ++i;
-    } else if (i > 0 && x < node_pos(lo, hi, G, i, dx)) {
-        --i;
-    }
-    double tt;
-    if (x >= node_pos(lo, hi, G, i + 1, dx)) {
-        tt = 1.0;
-    } else {
-        tt = __ddiv_rn(__dsub_rn(x, node_pos(lo, hi, G, i, dx)), dx);
-        if (tt < 0.0) tt = 0.0;
-        if (tt > 1.0) tt = 1.0;
-    }
-    idx = i;
-    t = tt;
-    return clamped;
-}
-
-// locate with the non-finite check (ValueError, kan.cpp:29) folded into err
-__device__ __forceinline__ void bracket_of(double lo, double hi, int G, double dx, double v, int* err,
-                                           int& m, double& t) {
-    m = 0;
-    t = 0.0;
-    if (!isfinite(v)) {
-        *err = 1;
-    } else {
-        locate_dev(lo, hi, G, dx, v, m, t);
-    }
-}
-
 // x is [rows][width] row-major.  Brackets are written in the same layout, or
-// input-major ([width][rows], rows = samples) when `rows_tr` > 0 — the
-// layout the fast-path kernels read (sample-contiguous).
-__global__ void k_locate_input(const double* __restrict__ x, long long n, double lo, double hi,
-                               int G, double dx, int* __restrict__ bm, float* __restrict__ btf,
-                               double* __restrict__ btd, int* __restrict__ err, int width, int rows_tr) {
+// input-major ([width][rows], rows = samples) when `rows_tr` > 0 -- the
+// layout the fast-path kernels read (sample-contiguous).  With btd (exact
+// path) t is locate()'s double; without it (fast path) the division-free
+// fast_locate is used.
+__global__ void k_locate_input(const double* __restrict__ x, long long n, DevLayer L, int* __restrict__ bm,
+                               float* __restrict__ btf, double* __restrict__ btd, int* __restrict__ err,
+                               int width, int rows_tr) {
     pdl_trigger();
     pdl_wait();
     for (long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<long long>(gridDim.x) * blockDim.x) {
         int m;
-        double t;
         long long src = p;
         if (rows_tr > 0) src = (p % rows_tr) * width + p / rows_tr;  // p = i*rows + s
-        bracket_of(lo, hi, G, dx, x[src], err, m, t);
+        if (btd) {
+            double t;
+            bracket_of(L.lo, L.hi, L.G, L.dx, x[src], err, m, t);
+            btf[p] = static_cast<float>(t);
+            btd[p] = t;
+        } else {
+            float t;
+            fast_locate(L, x[src], err, m, t);
+            btf[p] = t;
+        }
         bm[p] = m;
-        btf[p] = static_cast<float>(t);
-        if (btd) btd[p] = t;
     }
 }
-
-// ---------------------------------------------------------------------------
-// Edge decode for the fast kernels.
-
-__device__ __forceinline__ float i8lo(uint32_t p) { return static_cast<float>(static_cast<int8_t>(p & 0xFFu)); }
-__device__ __forceinline__ float i8hi(uint32_t p) { return static_cast<float>(static_cast<int8_t>((p >> 8) & 0xFFu)); }
 
 // Shared finisher: runs in the last CTA of an output tile and reduces the
 // tile's split partials.  C lanes cooperate on one (sample, output) entry
@@ -126,12 +74,12 @@ __device__ __forceinline__ void finish_entry(const FwdArgs& a, size_t p, int j, 
     a.y[p] = v;
     if (a.has_next) {
         int m;
-        double t;
-        bracket_of(a.nlo, a.nhi, a.nG, a.ndx, v, a.err, m, t);
+        float t;
+        fast_locate(a.N, v, a.err, m, t);
         const size_t s = p / a.L.out;
         const size_t q = static_cast<size_t>(j) * a.B + s;  // input-major for the next layer
         a.bm_out[q] = m;
-        a.bt_out[q] = static_cast<float>(t);
+        a.bt_out[q] = t;
     }
 }
 
@@ -215,10 +163,10 @@ __device__ __forceinline__ void reduce_prev_rows(const FwdArgs& a, int r0, int r
                 const int q = base + b, sl = q / R, i = r0 + q % R;
                 if (q >= entries) continue;
                 int m = 0;
-                double t = 0.0;
-                if (sl < nS && i < rend) bracket_of(L.lo, L.hi, L.G, L.dx, v[b] + a.prev_bias_sum[i], a.err, m, t);
+                float t = 0.f;
+                if (sl < nS && i < rend) fast_locate(L, v[b] + a.prev_bias_sum[i], a.err, m, t);
                 s_m[q] = m;
-                s_t[q] = static_cast<float>(t);
+                s_t[q] = t;
             }
         }
     }
@@ -340,9 +288,7 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
         if (sl < nS && i < rend) {
             const size_t p = static_cast<size_t>(s0 + sl) * L.in + i;
             if (a.x) {
-                double td;
-                bracket_of(L.lo, L.hi, L.G, L.dx, a.x[p], a.err, m, td);
-                t = static_cast<float>(td);
+                fast_locate(L, a.x[p], a.err, m, t);
             } else {
                 const size_t pt = static_cast<size_t>(i) * a.B + s0 + sl;  // input-major
                 m = a.bm_in[pt];
@@ -426,10 +372,6 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
 // (largest remainder), rows within a bucket are taken in ascending order,
 // warps take rows round-robin: the fp32 summation order is fixed.  Output:
 // one fp32 partial vector per CTA; the next layer reduces them.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 
 template <int NV>  // 128-output groups per row (out <= 128*NV), 4 outputs per lane per group
 __global__ void __launch_bounds__(256, 1) k_fwd_planes(FwdArgs a) {
@@ -1137,8 +1079,7 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
                          float* btf, double* btd, int* err, cudaStream_t s, bool input_major) {
     const long long n = static_cast<long long>(n_rows) * width;
     if (n == 0) return;
-    k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L.lo, L.hi, L.G, L.dx, bm, btf, btd, err, width,
-                                                    input_major ? n_rows : 0);
+    k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L, bm, btf, btd, err, width, input_major ? n_rows : 0);
 }
 
 void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {

@@ -73,8 +73,8 @@ def test_headline_head_plan():
     # (DESIGN.md "HBM layout"); everything 256 B aligned
     def al(v):
         return (v + 255) // 256 * 256
-    want = sum(al(4 * e) + al(65536 * 16) + al(65536 * 9 * 2) + al(1024) + al(2048) + al(8 * o)
-               for e, o in ((2048 * 1408, 1408), (1408 * 20, 20)))
+    want = sum(2 * al(10 * 8) + al(4 * e) + al(65536 * 16) + al(65536 * 9 * 2) + al(1024) + al(2048) + al(8 * o)
+               for e, o in ((2048 * 1408, 1408), (1408 * 20, 20)))  # node positions + keys first
     assert p.device_total == want
     assert p.device_total < 126e6  # fits the B200 L2
 

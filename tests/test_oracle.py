@@ -87,6 +87,37 @@ def test_locate_port_equals_reference_bitwise():
         assert np.array_equal(a[2], b[2]) and a[3] == b[3] == 0
 
 
+def _dkey(a):
+    """Order-preserving int64 key of a double (+0 and -0 share key 0), as the
+    fast-path device locate compares them (skan_device.cuh: dkey)."""
+    b = np.asarray(a, np.float64).view(np.int64).copy()
+    b[b == np.int64(-0x8000000000000000)] = 0
+    return b ^ ((b >> 63) & np.int64(0x7FFFFFFFFFFFFFFF))
+
+
+def test_bracket_is_the_node_search_the_fast_path_uses():
+    """The fast path finds locate()'s bracket without division: the unique
+    i in [0, G-2] with node(i) <= x < node(i+1) over the reference's own node
+    positions (kan.cpp:21-26), compared as order-preserving integer keys.
+    Pinned against oracle locate on random domains, every node, +-1 ulp
+    neighbours, +-0.0 and clamped inputs."""
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        G = int(rng.choice([2, 3, 4, 5, 7, 10, 16, 33, 64, 128, 1000]))
+        lo, hi = sorted(rng.uniform(-1e3, 1e3, 2)) if trial % 3 else sorted(rng.uniform(-2, 2, 2))
+        if trial % 7 == 0:
+            lo, hi = -1.0, 1.0
+        if hi - lo < 1e-6:
+            hi = lo + 1
+        nodes = np.array([synthetic.node_position(lo, hi, G, i) for i in range(G)])
+        x = np.concatenate([rng.uniform(lo - (hi - lo), hi + (hi - lo), 5000), nodes,
+                            np.nextafter(nodes, -np.inf), np.nextafter(nodes, np.inf), [-0.0, 0.0]])
+        ref_i, _, _, bad = oracle.port_locate_many(lo, hi, G, x)
+        assert bad == 0
+        mine = np.clip(np.searchsorted(_dkey(nodes), _dkey(np.clip(x, lo, hi)), side="right") - 1, 0, G - 2)
+        assert np.array_equal(mine, ref_i)
+
+
 @needs_ref
 def test_gain_decode_port_equals_reference_bitwise():
     rng = np.random.default_rng(2)
