@@ -84,35 +84,50 @@ __device__ __forceinline__ bool finite_bits(double d) {
     return ((__double_as_longlong(d) >> 52) & 0x7FF) != 0x7FF;
 }
 
-// L.nkey[G] node keys, L.node[G] node positions, L.lo_f, L.inv_dx_f.
-__device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
+// key[G] node keys and node[G] node positions (global or shared memory).
+__device__ __forceinline__ void fast_locate_tab(const long long* key, const double* node, int G, float lo_f,
+                                                float inv_dx_f, double x, int* err, int& m, float& t) {
     if (!finite_bits(x)) {
         *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
         m = 0;
         t = 0.f;
         return;
     }
-    const int G = L.G;
     long long kx = dkey(x);
-    const long long klo = __ldg(L.nkey), khi = __ldg(L.nkey + G - 1);
+    const long long klo = key[0], khi = key[G - 1];
     if (kx < klo) {
         kx = klo;
-        x = L.lo;
+        x = node[0];
     } else if (kx > khi) {
         kx = khi;
-        x = L.hi;
+        x = node[G - 1];
     }
-    int i = __float2int_rd((__double2float_rn(x) - L.lo_f) * L.inv_dx_f);
+    int i = __float2int_rd((__double2float_rn(x) - lo_f) * inv_dx_f);
     i = i < 0 ? 0 : (i > G - 2 ? G - 2 : i);
-    while (i < G - 2 && kx >= __ldg(L.nkey + i + 1)) ++i;
-    while (i > 0 && kx < __ldg(L.nkey + i)) --i;
+    while (i < G - 2 && kx >= key[i + 1]) ++i;
+    while (i > 0 && kx < key[i]) --i;
     float tt = 1.f;
-    if (kx < __ldg(L.nkey + i + 1)) {
-        tt = __double2float_rn(x - __ldg(L.node + i)) * L.inv_dx_f;
+    if (kx < key[i + 1]) {
+        tt = __double2float_rn(x - node[i]) * inv_dx_f;
         tt = tt < 0.f ? 0.f : (tt > 1.f ? 1.f : tt);
     }
     m = i;
     t = tt;
+}
+
+__device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
+    fast_locate_tab(L.nkey, L.node, L.G, L.lo_f, L.inv_dx_f, x, err, m, t);
+}
+
+// int8 codebook pair p = c0 | c1 << 8  ->  (c0, c1 - c0) as floats without
+// the quarter-rate I2F pipe: 0x4B000000 | (u ^ 0x80) is the float
+// 2^23 + u^0x80, so subtracting 2^23 + 128 yields the signed value; the
+// difference of two such floats is exact.
+__device__ __forceinline__ void pair_to_f(uint32_t p, float& c0, float& dc) {
+    const float f0 = __int_as_float(static_cast<int>((p & 0xFFu) ^ 0x4B000080u));
+    const float f1 = __int_as_float(static_cast<int>(((p >> 8) & 0xFFu) ^ 0x4B000080u));
+    c0 = f0 - 8388736.0f;
+    dc = f1 - f0;
 }
 
 // locate() for N independent inputs in lock step: the same operations as

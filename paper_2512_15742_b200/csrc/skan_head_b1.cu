@@ -72,8 +72,9 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 // prev[z*width + i] (z < nz): C lanes per row, ascending z per lane, then a
 // fixed butterfly; + bias; then locate with layer L's grid.  All of a
 // thread's loads are issued before any is consumed.
-__device__ void reduce_rows(const float* prev, int width, int nz, const double* bias, const DevLayer& L, int r0,
-                            int r1, int* s_m, float* s_t, int* err) {
+__device__ void reduce_rows(const float* prev, int width, int nz, const double* bias, const DevLayer& L,
+                            const long long* skey, const double* snode, int r0, int r1, int* s_m, float* s_t,
+                            int* err) {
     const int n = r1 - r0;
     int C = 1;
     while (C < 32 && (C * 2) * n <= kT) C <<= 1;
@@ -96,7 +97,7 @@ __device__ void reduce_rows(const float* prev, int width, int nz, const double* 
         if (c == 0 && q < n) {
             int m;
             float t;
-            fast_locate(L, v + (bias ? bias[i] : 0.0), err, m, t);
+            fast_locate_tab(skey, snode, L.G, L.lo_f, L.inv_dx_f, v + (bias ? bias[i] : 0.0), err, m, t);
             s_m[q] = m;
             s_t[q] = t;
         }
@@ -128,8 +129,9 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (j + 32 * e >= L.out) break;
-                const float c0 = i8lo(p[e]), c1 = i8hi(p[e]);
-                acc[j + 32 * e] = fmaf(s_lut[(r[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[j + 32 * e]);
+                float c0, dc;
+                pair_to_f(p[e], c0, dc);
+                acc[j + 32 * e] = fmaf(s_lut[(r[e] >> 16) & 0xFF], fmaf(t, dc, c0), acc[j + 32 * e]);
             }
         }
     }
@@ -146,8 +148,8 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
 // out x 4 B]; rows beyond rec_cap (only for very skewed shapes) read their
 // records from global memory.
 template <int NV>
-__device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const float* s_lut, uint64_t* bar,
-                              float* part_out) {
+__device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const float* s_lut, const long long* skey,
+                              const double* snode, uint64_t* bar, float* part_out) {
     const DevLayer& L = h.L[0];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int GP = L.G - 1;
@@ -174,7 +176,8 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     for (int q = 0; q < 16; ++q) {
         mine[q] = -1;
         tmine[q] = 0.f;
-        if (q < per && i0 + q < L.in) fast_locate(L, xv[q], h.err, mine[q], tmine[q]);
+        if (q < per && i0 + q < L.in)
+            fast_locate_tab(skey, snode, L.G, L.lo_f, L.inv_dx_f, xv[q], h.err, mine[q], tmine[q]);
     }
     stamp(h, 2);
     // 2. histogram: per-warp ballot counts (lane b counts bracket b), then a
@@ -285,9 +288,9 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
             const uint32_t r4[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const uint32_t p = s_plane[r4[e] & 0xFFFFu];
-                const float c0 = i8lo(p), c1 = i8hi(p);
-                acc[v][e] = fmaf(s_lut[(r4[e] >> 16) & 0xFF], fmaf(t, c1 - c0, c0), acc[v][e]);
+                float c0, dc;
+                pair_to_f(s_plane[r4[e] & 0xFFFFu], c0, dc);
+                acc[v][e] = fmaf(s_lut[(r4[e] >> 16) & 0xFF], fmaf(t, dc, c0), acc[v][e]);
             }
         }
     }
@@ -319,6 +322,9 @@ template <int NV>
 __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ float s_luts[kMaxHeadLayers][256];
+    __shared__ long long s_nkey[kMaxHeadLayers][33];  // node keys / positions (G <= 33)
+    __shared__ double s_node[kMaxHeadLayers][33];
+    __shared__ int s_last;
     __shared__ __align__(8) uint64_t s_bar[2];  // [0] layer-0 staging, [1] row-split prefetch
     const int P = gridDim.x, c = blockIdx.x;
     stamp(h, 0);
@@ -349,7 +355,13 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             off += bytes;
         }
     }
-    for (int l = 0; l < h.nl; ++l) s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];
+    for (int l = 0; l < h.nl; ++l) {
+        s_luts[l][threadIdx.x] = h.L[l].lutf[threadIdx.x];
+        if (threadIdx.x < h.L[l].G) {
+            s_nkey[l][threadIdx.x] = h.L[l].nkey[threadIdx.x];
+            s_node[l][threadIdx.x] = h.L[l].node[threadIdx.x];
+        }
+    }
     __syncthreads();
     stamp(h, 1);
     int* s_m = reinterpret_cast<int*>(smem);  // row-split scratch (after layer 0)
@@ -360,7 +372,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
         float* part_out = h.part[l & 1];
         const float* s_lut = s_luts[l];
         if (l == 0 && h.planes0) {
-            planes_layer0<NV>(h, smem, s_lut, &s_bar[0], part_out);
+            planes_layer0<NV>(h, smem, s_lut, s_nkey[0], s_node[0], &s_bar[0], part_out);
         } else {
             int r0, r1;
             rows_of(L, c, P, r0, r1);
@@ -368,9 +380,11 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             float* s_t = reinterpret_cast<float*>(s_m + nr);
             float* s_acc = s_t + nr;
             if (l == 0) {
-                for (int q = threadIdx.x; q < nr; q += kT) fast_locate(L, h.x[r0 + q], h.err, s_m[q], s_t[q]);
+                for (int q = threadIdx.x; q < nr; q += kT)
+                    fast_locate_tab(s_nkey[0], s_node[0], L.G, L.lo_f, L.inv_dx_f, h.x[r0 + q], h.err, s_m[q], s_t[q]);
             } else {
-                reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, r0, r1, s_m, s_t, h.err);
+                reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, s_nkey[l], s_node[l], r0, r1, s_m,
+                            s_t, h.err);
             }
             const uint32_t* s_rec = nullptr;
             if (h.pref_mask >> l & 1) {
@@ -386,16 +400,30 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             rowsplit_layer(L, r0, r1, s_m, s_t, s_rec, s_lut, s_acc, part_out);
         }
         stamp(h, l == 0 ? 7 : 10);
-        grid_sync(h.bar);
-        stamp(h, l == 0 ? 8 : 11);
+        if (l + 1 < h.nl) {
+            grid_sync(h.bar);
+            stamp(h, l == 0 ? 8 : 11);
+        }
     }
-    // final: outputs [c*out/P, (c+1)*out/P) of the last layer, one warp each
+    // the last CTA to finish the last layer reduces its partials: an arrival
+    // counter (bar[2]) instead of a full grid barrier
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(h.bar + 2, 1u) == static_cast<unsigned>(P) - 1;
+        if (s_last) {
+            h.bar[2] = 0;
+            __threadfence();
+        }
+    }
+    __syncthreads();
+    stamp(h, 11);
+    if (!s_last) return;
+    // final (last CTA): every output of the last layer, one warp each
     const DevLayer& L = h.L[h.nl - 1];
     const float* part = h.part[(h.nl - 1) & 1];
-    const int j0 = static_cast<int>(static_cast<long long>(L.out) * c / P);
-    const int j1 = static_cast<int>(static_cast<long long>(L.out) * (c + 1) / P);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int j = j0 + warp; j < j1; j += kW) {
+    for (int j = warp; j < L.out; j += kW) {
         double v = 0.0;
         for (int z0 = lane; z0 < P; z0 += 8 * 32) {  // all loads of a lane issued at once
             float buf[8];
