@@ -221,7 +221,8 @@ struct skan_workspace {
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
     float* b1_part = nullptr;        // 2 x [grid][max_width] partials of the batch-1 kernel
-    unsigned* b1_bar = nullptr;      // its grid barrier
+    unsigned* b1_flags = nullptr;    // its per-CTA barrier flags
+    unsigned b1_epoch = 0;           // epoch base of the next launch
     unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
     std::vector<void*> allocs;
 };
@@ -455,7 +456,8 @@ void upload(skan_head* h, std::vector<Staged>& st) {
             d.node = static_cast<const double*>(put(node.data(), node.size() * 8));
             d.nkey = static_cast<const long long*>(put(key.data(), key.size() * 8));
             d.lo_f = static_cast<float>(d.lo);
-            d.inv_dx_f = static_cast<float>(1.0 / d.dx);
+            d.inv_dx = 1.0 / d.dx;
+            d.inv_dx_f = static_cast<float>(d.inv_dx);
         }
         switch (d.fmt) {
             case skan::FMT_DENSE:
@@ -674,7 +676,9 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
             a.part[0] = ws->b1_part;
             a.part[1] = ws->b1_part + n;
-            a.bar = ws->b1_bar;
+            a.flags = ws->b1_flags;
+            a.epoch = ws->b1_epoch;
+            ws->b1_epoch += skan::kHeadB1EpochStride;
             a.err = d.err;
             a.timeline = ws->b1_timeline;
             skan::launch_head_b1(a, h->b1_grid, h->b1_smem, h->b1_nv, s);
@@ -841,8 +845,8 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         if (h->b1_ok) {
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
-            ws->b1_bar = static_cast<unsigned*>(alloc(skan::kHeadB1BarrierWords * sizeof(unsigned)));
-            skan::cuda_check(cudaMemset(ws->b1_bar, 0, skan::kHeadB1BarrierWords * sizeof(unsigned)), "cudaMemset");
+            ws->b1_flags = static_cast<unsigned*>(alloc(h->b1_grid * sizeof(unsigned)));
+            skan::cuda_check(cudaMemset(ws->b1_flags, 0, h->b1_grid * sizeof(unsigned)), "cudaMemset");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));

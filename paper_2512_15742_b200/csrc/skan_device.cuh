@@ -85,38 +85,41 @@ __device__ __forceinline__ bool finite_bits(double d) {
 }
 
 // key[G] node keys and node[G] node positions (global or shared memory).
-__device__ __forceinline__ void fast_locate_tab(const long long* key, const double* node, int G, float lo_f,
-                                                float inv_dx_f, double x, int* err, int& m, float& t) {
+// Branch-free (no per-lane loops, which diverge and serialise the warp):
+// the estimate floor(float((x-lo)*inv_dx)) is within one bracket of the
+// answer, one select-based step corrects it, and a loop runs only in the
+// (uniform-checked) case that it did not.
+__device__ __forceinline__ void fast_locate_tab(const long long* key, const double* node, int G, double lo,
+                                                double inv_dx, float inv_dx_f, double x, int* err, int& m,
+                                                float& t) {
     if (!finite_bits(x)) {
         *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
-        m = 0;
-        t = 0.f;
-        return;
+        x = node[0];
     }
     long long kx = dkey(x);
     const long long klo = key[0], khi = key[G - 1];
-    if (kx < klo) {
-        kx = klo;
-        x = node[0];
-    } else if (kx > khi) {
-        kx = khi;
-        x = node[G - 1];
+    const bool below = kx < klo, above = kx > khi;
+    kx = below ? klo : (above ? khi : kx);
+    x = below ? node[0] : (above ? node[G - 1] : x);
+    int i = __float2int_rd(__double2float_rn(__dsub_rn(x, lo) * inv_dx));
+    i = min(max(i, 0), G - 2);
+    const bool up = i < G - 2 && kx >= key[i + 1];
+    const bool down = !up && i > 0 && kx < key[i];
+    i += up ? 1 : (down ? -1 : 0);
+    const bool ok = (i == G - 2 || kx < key[i + 1]) && (i == 0 || kx >= key[i]);
+    if (__builtin_expect(!ok, 0)) {  // estimate was off by more than one bracket
+        while (i < G - 2 && kx >= key[i + 1]) ++i;
+        while (i > 0 && kx < key[i]) --i;
     }
-    int i = __float2int_rd((__double2float_rn(x) - lo_f) * inv_dx_f);
-    i = i < 0 ? 0 : (i > G - 2 ? G - 2 : i);
-    while (i < G - 2 && kx >= key[i + 1]) ++i;
-    while (i > 0 && kx < key[i]) --i;
-    float tt = 1.f;
-    if (kx < key[i + 1]) {
-        tt = __double2float_rn(x - node[i]) * inv_dx_f;
-        tt = tt < 0.f ? 0.f : (tt > 1.f ? 1.f : tt);
-    }
+    const bool full = kx >= key[i + 1];  // at or past the upper node: t = 1 exactly
+    float tt = __double2float_rn(x - node[i]) * inv_dx_f;
+    tt = fminf(fmaxf(tt, 0.f), 1.f);
     m = i;
-    t = tt;
+    t = full ? 1.f : tt;
 }
 
 __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
-    fast_locate_tab(L.nkey, L.node, L.G, L.lo_f, L.inv_dx_f, x, err, m, t);
+    fast_locate_tab(L.nkey, L.node, L.G, L.lo, L.inv_dx, L.inv_dx_f, x, err, m, t);
 }
 
 // int8 codebook pair p = c0 | c1 << 8  ->  (c0, c1 - c0) as floats without

@@ -45,25 +45,25 @@ __device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
     }
 }
 
-// Generation grid barrier over bar = {count, gen}: one same-address atomic
-// per CTA (L2 serialises ~148 of them in well under a round trip), the last
-// arrival resets the count and bumps the generation.  The CTA barrier
-// orders the CTA's writes before thread 0's gpu-scope fence (cumulativity),
-// as in cooperative_groups::grid_group::sync.
-__device__ __forceinline__ void grid_sync(unsigned* bar) {
+// Flag grid barrier without atomics: CTA c publishes epoch `target` in its
+// own flag with a gpu-scope release store; thread t of every CTA polls flag
+// t with acquire loads until all CTAs reached the epoch.  (A same-address
+// atomic counter serialises ~148 arrivals in one L2 slice: ~5k cycles.)
+// The CTA barrier before the release makes the whole CTA's writes part of it
+// (cumulativity); the one after the polls makes every peer's writes visible
+// to the whole CTA.  Epochs grow monotonically across launches, compared
+// with wrap-around arithmetic.  Requires gridDim.x <= blockDim.x.
+__device__ __forceinline__ void grid_sync(unsigned* flags, unsigned target) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned* vgen = bar + 1;
-        const unsigned gen = *vgen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*vgen == gen) __nanosleep(16);
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"(target) : "memory");
+    if (threadIdx.x < gridDim.x) {
+        unsigned v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
+            if (static_cast<int>(v - target) >= 0) break;
+            __nanosleep(8);
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -97,7 +97,7 @@ __device__ void reduce_rows(const float* prev, int width, int nz, const double* 
         if (c == 0 && q < n) {
             int m;
             float t;
-            fast_locate_tab(skey, snode, L.G, L.lo_f, L.inv_dx_f, v + (bias ? bias[i] : 0.0), err, m, t);
+            fast_locate_tab(skey, snode, L.G, L.lo, L.inv_dx, L.inv_dx_f, v + (bias ? bias[i] : 0.0), err, m, t);
             s_m[q] = m;
             s_t[q] = t;
         }
@@ -177,7 +177,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
         mine[q] = -1;
         tmine[q] = 0.f;
         if (q < per && i0 + q < L.in)
-            fast_locate_tab(skey, snode, L.G, L.lo_f, L.inv_dx_f, xv[q], h.err, mine[q], tmine[q]);
+            fast_locate_tab(skey, snode, L.G, L.lo, L.inv_dx, L.inv_dx_f, xv[q], h.err, mine[q], tmine[q]);
     }
     stamp(h, 2);
     // 2. histogram: per-warp ballot counts (lane b counts bracket b), then a
@@ -324,7 +324,6 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
     __shared__ float s_luts[kMaxHeadLayers][256];
     __shared__ long long s_nkey[kMaxHeadLayers][33];  // node keys / positions (G <= 33)
     __shared__ double s_node[kMaxHeadLayers][33];
-    __shared__ int s_last;
     __shared__ __align__(8) uint64_t s_bar[2];  // [0] layer-0 staging, [1] row-split prefetch
     const int P = gridDim.x, c = blockIdx.x;
     stamp(h, 0);
@@ -381,7 +380,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
             float* s_acc = s_t + nr;
             if (l == 0) {
                 for (int q = threadIdx.x; q < nr; q += kT)
-                    fast_locate_tab(s_nkey[0], s_node[0], L.G, L.lo_f, L.inv_dx_f, h.x[r0 + q], h.err, s_m[q], s_t[q]);
+                    fast_locate_tab(s_nkey[0], s_node[0], L.G, L.lo, L.inv_dx, L.inv_dx_f, h.x[r0 + q], h.err, s_m[q], s_t[q]);
             } else {
                 reduce_rows(h.part[(l - 1) & 1], L.in, P, h.L[l - 1].bias_sum, L, s_nkey[l], s_node[l], r0, r1, s_m,
                             s_t, h.err);
@@ -401,25 +400,28 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(HeadB1Args h) {
         }
         stamp(h, l == 0 ? 7 : 10);
         if (l + 1 < h.nl) {
-            grid_sync(h.bar);
+            grid_sync(h.flags, h.epoch + l + 1);
             stamp(h, l == 0 ? 8 : 11);
         }
     }
-    // the last CTA to finish the last layer reduces its partials: an arrival
-    // counter (bar[2]) instead of a full grid barrier
+    // the last layer's partials are reduced by CTA 0 alone: every CTA only
+    // publishes its flag; CTA 0 waits for all of them (half a barrier)
+    const unsigned fin = h.epoch + h.nl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(h.bar + 2, 1u) == static_cast<unsigned>(P) - 1;
-        if (s_last) {
-            h.bar[2] = 0;
-            __threadfence();
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(h.flags + blockIdx.x), "r"(fin) : "memory");
+    if (blockIdx.x != 0) return;
+    if (threadIdx.x < P) {
+        unsigned v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(h.flags + threadIdx.x) : "memory");
+            if (static_cast<int>(v - fin) >= 0) break;
+            __nanosleep(8);
         }
     }
     __syncthreads();
     stamp(h, 11);
-    if (!s_last) return;
-    // final (last CTA): every output of the last layer, one warp each
+    // final (CTA 0): every output of the last layer, one warp each
     const DevLayer& L = h.L[h.nl - 1];
     const float* part = h.part[(h.nl - 1) & 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -70,7 +70,8 @@ struct DevLayer {
     int rs;                  // int8 codebook row stride in bytes (G rounded up to 16)
     const double* node;      // [G] node positions exactly as kan.cpp:21-26 computes them
     const long long* nkey;   // [G] their order-preserving integer keys (fast locate)
-    float lo_f, inv_dx_f;    // float(lo), float(1/dx): fast locate's estimate and t
+    double inv_dx;           // 1/dx: fast locate's bracket estimate
+    float lo_f, inv_dx_f;    // float(lo), float(1/dx): fast locate's t
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -125,14 +126,15 @@ struct HeadB1Args {
     const double* x;   // [in]
     double* y;         // [out]
     float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
-    unsigned* bar;     // grid barrier {top, generation, 16 sub-counters}
+    unsigned* flags;   // [grid] per-CTA barrier epochs (monotonic across launches)
+    unsigned epoch;    // this launch's epoch base (barrier k waits for epoch + k + 1)
     int* err;
     unsigned long long* timeline;  // optional: [grid][16] %globaltimer stamps per phase
     int rec_cap;           // layer-0 rows whose records are staged in shared memory
     unsigned pref_mask;    // row-split layers whose records are prefetched at kernel start
     unsigned pref_offset;  // byte offset of the prefetch region in dynamic shared memory
 };
-constexpr int kHeadB1BarrierWords = 2 + 16;
+constexpr unsigned kHeadB1EpochStride = 16;  // >= layers + 1 barriers per launch
 bool head_b1_supported(const DevLayer* L, int nl);
 // Shared-memory plan of the batch-1 kernel; fills h->planes0, rec_cap,
 // pref_mask, pref_offset.

@@ -25,6 +25,7 @@ PHASES = {0: "start", 1: "luts", 2: "locate+hist", 3: "alloc+tma", 4: "rowlist",
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--flush", choices=["write", "write+read", "none"], default="write")
     args = ap.parse_args()
     cn = synthetic.synthetic_head()
     model = hq.build_model(cn)
@@ -35,6 +36,13 @@ def main():
     x = torch.from_numpy(synthetic.synthetic_inputs(1, 2048, seed=1)).cuda()
     y = torch.zeros(20, dtype=torch.float64, device="cuda")
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    flush_r = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+
+    def do_flush():
+        if args.flush != "none":
+            flush.zero_()
+        if args.flush == "write+read":
+            flush_r.sum()
     import time
     for rep in range(args.reps):
         # keep the GPU busy for ~1 s first so SM clocks are at their loaded
@@ -42,11 +50,11 @@ def main():
         t_end = time.perf_counter() + 1.0
         while time.perf_counter() < t_end:
             for _ in range(50):
-                flush.zero_()
+                do_flush()
                 hq.forward_async(model, x, 1, y, ws)
             torch.cuda.synchronize()
-        flush.zero_()
         stamps.zero_()
+        do_flush()
         hq.forward_async(model, x, 1, y, ws)
         torch.cuda.synchronize()
         s = stamps.view(grid, 16).cpu().numpy().astype(np.float64)
