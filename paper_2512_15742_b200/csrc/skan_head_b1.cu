@@ -164,35 +164,27 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     uint32_t* s_rec = reinterpret_cast<uint32_t*>(smem + ((plane_bytes + 127u) & ~127u));
     const uint32_t row_bytes = static_cast<uint32_t>(L.out) * 4u;
 
-    // 1. inputs of this thread (contiguous slice) -> brackets (division-free)
-    const int per = (L.in + kT - 1) / kT;  // <= 16
-    const int i0 = tid * per;
-    int mine[16];
-    float tmine[16];
-    double xv[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) xv[q] = (q < per && i0 + q < L.in) ? h.x[i0 + q] : 0.0;  // one round trip
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        mine[q] = -1;
-        tmine[q] = 0.f;
-        if (q < per && i0 + q < L.in)
-            fast_locate_tab(skey, snode, L.G, L.lo, L.inv_dx, L.inv_dx_f, xv[q], h.err, mine[q], tmine[q]);
-    }
-    stamp(h, 2);
-    // 2. histogram: per-warp ballot counts (lane b counts bracket b), then a
-    //    fixed-order sum over warps -- no atomics
-    int wcnt = 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        if (q >= per) break;
-        for (int b = 0; b < GP; ++b) {
-            const int cb = __popc(__ballot_sync(0xFFFFFFFFu, mine[q] == b));
-            if (lane == b) wcnt += cb;
-        }
-    }
-    s_whist[warp][lane] = wcnt;
+    // Code size matters more than instruction count here: each warp runs this
+    // prologue once, from an instruction cache that the per-call L2 flush
+    // leaves cold, so loops stay rolled (#pragma unroll 1).
+    // 1. inputs staged in the record region (free until the records land),
+    //    brackets of all inputs -> shared memory, integer histogram per warp
+    double* s_x = reinterpret_cast<double*>(s_rec);
+    float* s_tall = reinterpret_cast<float*>(s_x + L.in);
+    uint8_t* s_bm = reinterpret_cast<uint8_t*>(s_tall + L.in);
+#pragma unroll 4
+    for (int i = tid; i < L.in; i += kT) s_x[i] = h.x[i];
+    s_whist[warp][lane] = 0;
     __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < L.in; i += kT) {
+        int m;
+        fast_locate_tab(skey, snode, L.G, L.lo, L.inv_dx, L.inv_dx_f, s_x[i], h.err, m, s_tall[i]);
+        s_bm[i] = static_cast<uint8_t>(m);
+        atomicAdd(&s_whist[warp][m], 1);  // integer counts: order-free, deterministic
+    }
+    __syncthreads();
+    stamp(h, 2);
     if (tid < 32) {
         int s = 0;
 #pragma unroll
@@ -237,11 +229,13 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
             bulk_g2s(smem + off, src + off, min(32768u, plane_bytes - off), bar);
     }
     stamp(h, 3);
-    // 4. my rows: rank within the bucket (exclusive scan of per-thread counts);
-    //    the owning thread issues that row's record bulk copy
+    // 4. my rows: rank within the bucket (thread t scans a contiguous slice;
+    //    exclusive scan of the slice counts), then one record bulk copy per row
+    const int per = (L.in + kT - 1) / kT;
+    const int i0 = min(tid * per, L.in), i1 = min(i0 + per, L.in);
     int cnt = 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) cnt += mine[q] == bucket;
+#pragma unroll 1
+    for (int i = i0; i < i1; ++i) cnt += s_bm[i] == bucket;
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -251,22 +245,21 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     if (lane == 31) s_scan[warp] = incl;
     __syncthreads();
     int rank = incl - cnt;
+#pragma unroll 1
     for (int w = 0; w < warp; ++w) rank += s_scan[w];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        if (mine[q] == bucket) {
-            const int r = rank - lo;
-            if (r >= 0 && r < nrows) {
-                s_rows[r] = i0 + q;
-                s_trow[r] = tmine[q];
-                if (r < rec_rows)
-                    bulk_g2s(s_rec + static_cast<size_t>(r) * L.out, L.rec + static_cast<size_t>(i0 + q) * L.out,
-                             row_bytes, bar);
-            }
-            ++rank;
+#pragma unroll 1
+    for (int i = i0; i < i1; ++i) {
+        if (s_bm[i] != bucket) continue;
+        const int r = rank++ - lo;
+        if (r >= 0 && r < nrows) {
+            s_rows[r] = i;
+            s_trow[r] = s_tall[i];
         }
     }
-    __syncthreads();
+    __syncthreads();  // staging area free: records may land now
+    if (tid < rec_rows)
+        bulk_g2s(s_rec + static_cast<size_t>(tid) * L.out, L.rec + static_cast<size_t>(s_rows[tid]) * L.out,
+                 row_bytes, bar);
     stamp(h, 4);
     if (bucket < GP) mbar_wait(bar, 0);
     stamp(h, 5);
@@ -314,8 +307,8 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
 }
 
 __device__ __forceinline__ void rows_of(const DevLayer& L, int c, int P, int& r0, int& r1) {
-    r0 = static_cast<int>(static_cast<long long>(L.in) * c / P);
-    r1 = static_cast<int>(static_cast<long long>(L.in) * (c + 1) / P);
+    r0 = L.in * c / P;  // 32-bit: in <= 16384, c <= P <= 256 (a 64-bit divide is ~60 instructions)
+    r1 = L.in * (c + 1) / P;
 }
 
 template <int NV>
@@ -494,7 +487,9 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* 
         if (cap > static_cast<size_t>(want)) cap = want;
         if (cap > 128) cap = 128;
         h->rec_cap = static_cast<int>(cap);
-        phase = plane + cap * row;
+        // the record region doubles as the input staging area (x, t, bracket)
+        const size_t staging = static_cast<size_t>(L0.in) * (sizeof(double) + sizeof(float) + 1) + 128;
+        phase = plane + (cap * row > staging ? cap * row : staging);
         if (red > phase) phase = red;
     }
     for (int l = 0; l < nl; ++l) {
