@@ -458,6 +458,11 @@ void upload(skan_head* h, std::vector<Staged>& st) {
             d.lo_f = static_cast<float>(d.lo);
             d.inv_dx = 1.0 / d.dx;
             d.inv_dx_f = static_cast<float>(d.inv_dx);
+            // |q - exact position| <= u*(|lo| + |hi|)/dx from the node roundings
+            // plus ~3u*(G-1) from computing q; 16x margin, floor 1e-9
+            const double u = 0x1.0p-53;
+            d.q_eps = 1e-9 + 16.0 * u * ((std::fabs(d.lo) + std::fabs(d.hi)) / d.dx + 5.0 * G);
+            if (!(d.q_eps < 0.25)) d.q_eps = -1.0;  // pathological domain: always search the nodes
         }
         switch (d.fmt) {
             case skan::FMT_DENSE:

@@ -91,10 +91,24 @@ __device__ __forceinline__ bool finite_bits(double d) {
 // (uniform-checked) case that it did not.
 __device__ __forceinline__ void fast_locate_tab(const long long* key, const double* node, int G, double lo,
                                                 double inv_dx, float inv_dx_f, double x, int* err, int& m,
-                                                float& t) {
+                                                float& t, double q_eps = -1.0) {
     if (!finite_bits(x)) {
         *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
         x = node[0];
+    }
+    if (q_eps >= 0.0) {
+        // common path: q = (x-lo)*inv_dx is within q_eps (host-derived bound
+        // on the rounding of q and of the node positions) of the exact
+        // position, so away from integers floor(q) IS the bracket and
+        // q - floor(q) is t to far below a float ulp; no table loads.
+        const double q = __dmul_rn(__dsub_rn(x, lo), inv_dx);
+        const int i = __double2int_rd(q);
+        const double f = __dsub_rn(q, static_cast<double>(i));
+        if (i >= 0 && i <= G - 2 && f > q_eps && f < 1.0 - q_eps) {
+            m = i;
+            t = __double2float_rn(f);
+            return;
+        }
     }
     long long kx = dkey(x);
     const long long klo = key[0], khi = key[G - 1];
@@ -119,7 +133,7 @@ __device__ __forceinline__ void fast_locate_tab(const long long* key, const doub
 }
 
 __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
-    fast_locate_tab(L.nkey, L.node, L.G, L.lo, L.inv_dx, L.inv_dx_f, x, err, m, t);
+    fast_locate_tab(L.nkey, L.node, L.G, L.lo, L.inv_dx, L.inv_dx_f, x, err, m, t, L.q_eps);
 }
 
 // int8 codebook pair p = c0 | c1 << 8  ->  (c0, c1 - c0) as floats without

@@ -71,6 +71,8 @@ struct DevLayer {
     const double* node;      // [G] node positions exactly as kan.cpp:21-26 computes them
     const long long* nkey;   // [G] their order-preserving integer keys (fast locate)
     double inv_dx;           // 1/dx: fast locate's bracket estimate
+    double q_eps;            // fast locate trusts floor((x-lo)*inv_dx) when its fraction is
+                             // more than q_eps from an integer (< 0: always search)
     float lo_f, inv_dx_f;    // float(lo), float(1/dx): fast locate's t
 };
 
