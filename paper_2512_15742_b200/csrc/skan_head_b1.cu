@@ -161,6 +161,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, const fl
     for (int i = tid; i < L.in; i += kT) s_x[i] = h.x[i];
     s_whist[warp][lane] = 0;
     __syncthreads();
+    stamp(h, 13);
 #pragma unroll 1
     for (int i = tid; i < L.in; i += kT) {
         int m;

@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_15742_b200 as hq  # noqa: E402
 from paper_2512_15742_b200 import _lib, synthetic  # noqa: E402
 
-PHASES = {0: "start", 1: "luts", 2: "locate+hist", 3: "alloc+tma", 4: "rowlist", 5: "plane ready",
+PHASES = {0: "start", 1: "luts", 13: "x staged", 2: "locate+hist", 3: "alloc+tma", 4: "rowlist", 5: "plane ready",
           6: "rows done", 7: "L0 partial", 8: "grid sync 1", 9: "L1 reduce+locate", 10: "L1 rows",
           11: "grid sync 2", 12: "end"}
 

@@ -1,0 +1,56 @@
+"""Latency diagnostics of the cfg2 head on one GPU: CUDA-event time per
+forward at several batch sizes, with L2 flushed (256 MiB write) or warm.
+
+    python tools/diag_latency.py [--reps 200]
+"""
+import argparse
+import os
+import statistics
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_15742_b200 as hq  # noqa: E402
+from paper_2512_15742_b200 import synthetic  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--batches", default="1,2,4,8,16,64,256")
+    args = ap.parse_args()
+    cn = synthetic.synthetic_head()
+    model = hq.build_model(cn)
+    ws = hq.make_workspace(model, 256)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end:
+        flush.zero_()
+    for B in [int(b) for b in args.batches.split(",")]:
+        x = torch.from_numpy(synthetic.synthetic_inputs(B, 2048, seed=1)).cuda()
+        y = torch.zeros(B * 20, dtype=torch.float64, device="cuda")
+        for fl in (True, False):
+            ev = []
+            with torch.cuda.stream(s):
+                for r in range(args.reps + 5):
+                    if fl:
+                        flush.zero_()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(s)
+                    hq.forward_async(model, x, B, y, ws, stream=s.cuda_stream)
+                    b.record(s)
+                    if r >= 5:
+                        ev.append((a, b))
+            s.synchronize()
+            ws.check()
+            t = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+            print(f"B={B:4d} flush={fl!s:5} launches={ws.last_launches()} median {statistics.median(t):8.2f} us "
+                  f"p10 {t[len(t) // 10]:8.2f} p90 {t[9 * len(t) // 10]:8.2f}  -> {B / statistics.median(t) * 1e6:,.0f} samples/s",
+                  flush=True)
+
+
+if __name__ == "__main__":
+    main()
