@@ -201,7 +201,7 @@ struct skan_head {
     int in_dim = 0, out_dim = 0, max_width = 0;
     // batch-1 persistent kernel plan (skan_head_b1.cu)
     bool b1_ok = false;
-    int b1_grid = 0, b1_nv = 0;
+    int b1_grid = 0;
     size_t b1_smem = 0;
     skan::HeadB1Args b1_plan{};  // layers + shared-memory plan; per-call pointers filled at launch
 };
@@ -221,8 +221,8 @@ struct skan_workspace {
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
     float* b1_part = nullptr;        // 2 x [grid][max_width] partials of the batch-1 kernel
-    unsigned* b1_flags = nullptr;    // its per-CTA barrier flags
-    unsigned b1_epoch = 0;           // epoch base of the next launch
+    unsigned* b1_done = nullptr;     // its monotonic last-layer arrival counter
+    unsigned b1_epoch = 0;           // value of *b1_done when the next launch starts
     unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
     std::vector<void*> allocs;
 };
@@ -463,6 +463,16 @@ void upload(skan_head* h, std::vector<Staged>& st) {
             const double u = 0x1.0p-53;
             d.q_eps = 1e-9 + 16.0 * u * ((std::fabs(d.lo) + std::fabs(d.hi)) / d.dx + 5.0 * G);
             if (!(d.q_eps < 0.25)) d.q_eps = -1.0;  // pathological domain: always search the nodes
+            // fp32 bracket estimate (bracket_f32): |qf - (x-lo)/dx| <= 2^-24 * ((2 max|lo|,|hi| +
+            // (hi-lo))/dx + 2(G-1)) from rounding x, lo, 1/dx and two fp32 ops; 4x margin on top of q_eps
+            d.hi_f = static_cast<float>(d.hi);
+            const double uf = 0x1.0p-24;
+            const double amax = std::max(std::fabs(d.lo), std::fabs(d.hi));
+            const double qf_eps = 4.0 * uf * ((2.0 * amax + (d.hi - d.lo)) / d.dx + 2.0 * (G - 1)) + d.q_eps;
+            d.qf_eps = (d.q_eps >= 0.0 && qf_eps < 0.25 && G - 1 < (1 << 21)) ? static_cast<float>(qf_eps) : -1.f;
+            // exp2-form of the int8 gain LUT (fast path): log2(cs) folded into the base
+            d.g_base = static_cast<float>(s.h.gain_log_min + std::log2(s.h.codebook_scale));
+            d.g_step = static_cast<float>(s.h.gain_log_step);
         }
         switch (d.fmt) {
             case skan::FMT_DENSE:
@@ -552,10 +562,10 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
     // co-resident (checked against the occupancy calculator at its smem size)
     const int nl = static_cast<int>(h->dl.size());
     if (skan::head_b1_supported(h->dl.data(), nl)) {
-        h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan, &h->b1_nv);
+        h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan);
         h->b1_plan.nl = nl;
         for (int l = 0; l < nl; ++l) h->b1_plan.L[l] = h->dl[l];
-        h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->b1_nv, h->num_sms);
+        h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->num_sms);
         if (h->b1_grid > 0) {
             h->b1_ok = true;
         }
@@ -681,12 +691,13 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
             a.part[0] = ws->b1_part;
             a.part[1] = ws->b1_part + n;
-            a.flags = ws->b1_flags;
+            a.x_tma = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->in_dim % 2 == 0);
+            a.done = ws->b1_done;
             a.epoch = ws->b1_epoch;
-            ws->b1_epoch += skan::kHeadB1EpochStride;
+            ws->b1_epoch += static_cast<unsigned>(h->b1_grid);  // every CTA arrives once
             a.err = d.err;
             a.timeline = ws->b1_timeline;
-            skan::launch_head_b1(a, h->b1_grid, h->b1_smem, h->b1_nv, s);
+            skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s);
             skan::cuda_check(cudaGetLastError(), "kernel launch");
             return 1;
         }
@@ -850,8 +861,8 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         if (h->b1_ok) {
             const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
-            ws->b1_flags = static_cast<unsigned*>(alloc(h->b1_grid * sizeof(unsigned)));
-            skan::cuda_check(cudaMemset(ws->b1_flags, 0, h->b1_grid * sizeof(unsigned)), "cudaMemset");
+            ws->b1_done = static_cast<unsigned*>(alloc(sizeof(unsigned)));
+            skan::cuda_check(cudaMemset(ws->b1_done, 0, sizeof(unsigned)), "cudaMemset");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));

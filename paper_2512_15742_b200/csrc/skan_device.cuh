@@ -84,56 +84,97 @@ __device__ __forceinline__ bool finite_bits(double d) {
     return ((__double_as_longlong(d) >> 52) & 0x7FF) != 0x7FF;
 }
 
-// key[G] node keys and node[G] node positions (global or shared memory).
-// Branch-free (no per-lane loops, which diverge and serialise the warp):
-// the estimate floor(float((x-lo)*inv_dx)) is within one bracket of the
-// answer, one select-based step corrects it, and a loop runs only in the
-// (uniform-checked) case that it did not.
-__device__ __forceinline__ void fast_locate_tab(const long long* key, const double* node, int G, double lo,
-                                                double inv_dx, float inv_dx_f, double x, int* err, int& m,
-                                                float& t, double q_eps = -1.0) {
-    if (!finite_bits(x)) {
-        *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
-        x = node[0];
-    }
-    if (q_eps >= 0.0) {
-        // common path: q = (x-lo)*inv_dx is within q_eps (host-derived bound
-        // on the rounding of q and of the node positions) of the exact
-        // position, so away from integers floor(q) IS the bracket and
-        // q - floor(q) is t to far below a float ulp; no table loads.
-        const double q = __dmul_rn(__dsub_rn(x, lo), inv_dx);
-        const int i = __double2int_rd(q);
-        const double f = __dsub_rn(q, static_cast<double>(i));
-        if (i >= 0 && i <= G - 2 && f > q_eps && f < 1.0 - q_eps) {
-            m = i;
-            t = __double2float_rn(f);
-            return;
+// The node search for inputs the cheap paths cannot settle (within q_eps of
+// a knot, or pathological domains): locate()'s floor-then-correct sequence
+// ends at the unique i in [0, G-2] with node(i) <= x < node(i+1) over the
+// reference's own node positions (pinned by
+// tests/test_oracle.py::test_bracket_is_the_node_search_the_fast_path_uses),
+// so step from the estimate floor((x-lo)*inv_dx) with exact comparisons
+// against node positions computed exactly as kan.cpp:21-26 does.  Returns
+// (bracket, float t bits) packed in registers.  Out of line: it is rare, and
+// inlining it at every call site multiplies the code a cold instruction
+// cache must fetch.
+static __device__ __noinline__ unsigned long long locate_search(double lo, double hi, int G, double dx,
+                                                                double inv_dx, float inv_dx_f, double x) {
+    int i;
+    float t;
+    if (!(x > lo)) {  // clamped to lo (also NaN, flagged by the caller)
+        i = 0;
+        t = 0.f;
+    } else if (!(x < hi)) {  // clamped to hi: at the last node, t = 1
+        i = G - 2;
+        t = 1.f;
+    } else {
+        i = static_cast<int>(floor(__dmul_rn(__dsub_rn(x, lo), inv_dx)));
+        i = min(max(i, 0), G - 2);
+        while (i < G - 2 && x >= node_pos(lo, hi, G, i + 1, dx)) ++i;
+        while (i > 0 && x < node_pos(lo, hi, G, i, dx)) --i;
+        if (x >= node_pos(lo, hi, G, i + 1, dx)) {
+            t = 1.f;
+        } else {
+            t = __double2float_rn(__dsub_rn(x, node_pos(lo, hi, G, i, dx))) * inv_dx_f;
+            t = fminf(fmaxf(t, 0.f), 1.f);
         }
     }
-    long long kx = dkey(x);
-    const long long klo = key[0], khi = key[G - 1];
-    const bool below = kx < klo, above = kx > khi;
-    kx = below ? klo : (above ? khi : kx);
-    x = below ? node[0] : (above ? node[G - 1] : x);
-    int i = __float2int_rd(__double2float_rn(__dsub_rn(x, lo) * inv_dx));
-    i = min(max(i, 0), G - 2);
-    const bool up = i < G - 2 && kx >= key[i + 1];
-    const bool down = !up && i > 0 && kx < key[i];
-    i += up ? 1 : (down ? -1 : 0);
-    const bool ok = (i == G - 2 || kx < key[i + 1]) && (i == 0 || kx >= key[i]);
-    if (__builtin_expect(!ok, 0)) {  // estimate was off by more than one bracket
-        while (i < G - 2 && kx >= key[i + 1]) ++i;
-        while (i > 0 && kx < key[i]) --i;
+    return static_cast<unsigned>(i) | (static_cast<unsigned long long>(__float_as_uint(t)) << 32);
+}
+
+// Clamped inputs settle without the node tables: x <= lo is clamped to lo
+// (kan.cpp:31-37) -> bracket 0, t = 0 exactly; x >= hi -> bracket G-2,
+// t = 1 exactly (x >= node(G-1) = hi, kan.cpp:49-50).  In-domain inputs
+// whose q = (x-lo)/dx lies more than q_eps (a host-derived bound on the
+// rounding of q and of the node positions) from an integer take
+// floor(q) as the bracket and q - floor(q) as t.  Returns false for the
+// rest (locate_search settles them).  Non-finite x raises the ValueError
+// flag (kan.cpp:29).  Straight-line code: callers locate several inputs
+// with full ILP, then search the rare unsettled ones.
+__device__ __forceinline__ bool locate_easy(double lo, double hi, int G, double inv_dx, double q_eps, double x,
+                                            int* err, int& m, float& t) {
+    if (!finite_bits(x)) *err = 1;  // ValueError("spline evaluated at non-finite x"), kan.cpp:29
+    const bool below = !(x > lo);   // also NaN: any bracket will do once err is set
+    const bool above = !below && !(x < hi);
+    const double q = __dmul_rn(__dsub_rn(x, lo), inv_dx);
+    const int i = __double2int_rd(q);
+    const double f = __dsub_rn(q, static_cast<double>(i));
+    const bool easy = q_eps >= 0.0 && i >= 0 && i <= G - 2 && f > q_eps && f < 1.0 - q_eps;
+    m = below ? 0 : (above ? G - 2 : i);
+    t = below ? 0.f : (above ? 1.f : __double2float_rn(f));
+    return below || above || easy;
+}
+
+// Bracket only, in fp32 (one double->float conversion, no fp64 pipe work):
+// x < lo and x > hi follow exactly from float(x) < float(lo) and
+// float(x) > float(hi) (rounding is monotone); in-domain inputs take
+// floor(q) when q's fraction is more than qf_eps from an integer.  Returns
+// false when undecided (near a knot, at the domain ends, non-finite):
+// callers fall back to the exact fp64 path.
+__device__ __forceinline__ bool bracket_f32(const DevLayer& L, double x, int& m) {
+    if (!finite_bits(x) || !(L.qf_eps >= 0.f)) return false;
+    const float xf = __double2float_rn(x);
+    if (xf < L.lo_f) {
+        m = 0;
+        return true;
     }
-    const bool full = kx >= key[i + 1];  // at or past the upper node: t = 1 exactly
-    float tt = __double2float_rn(x - node[i]) * inv_dx_f;
-    tt = fminf(fmaxf(tt, 0.f), 1.f);
+    if (xf > L.hi_f) {
+        m = L.G - 2;
+        return true;
+    }
+    const float q = (xf - L.lo_f) * L.inv_dx_f;
+    const float r = q + 12582912.0f;  // 1.5 * 2^23: rounds q to the nearest integer
+    const int n = __float_as_int(r) - 0x4B400000;
+    const float fr = q - (r - 12582912.0f);  // exact, in [-0.5, 0.5]
+    const int i = fr < 0.f ? n - 1 : n;
+    const float f = fr < 0.f ? fr + 1.f : fr;
     m = i;
-    t = full ? 1.f : tt;
+    return i >= 0 && i <= L.G - 2 && f > L.qf_eps && f < 1.f - L.qf_eps;
 }
 
 __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {
-    fast_locate_tab(L.nkey, L.node, L.G, L.lo, L.inv_dx, L.inv_dx_f, x, err, m, t, L.q_eps);
+    if (!locate_easy(L.lo, L.hi, L.G, L.inv_dx, L.q_eps, x, err, m, t)) {
+        const unsigned long long r = locate_search(L.lo, L.hi, L.G, L.dx, L.inv_dx, L.inv_dx_f, x);
+        m = static_cast<int>(r & 0xFFFFFFFFu);
+        t = __uint_as_float(static_cast<unsigned>(r >> 32));
+    }
 }
 
 // int8 codebook pair p = c0 | c1 << 8  ->  (c0, c1 - c0) as floats without
@@ -141,10 +182,19 @@ __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* er
 // 2^23 + u^0x80, so subtracting 2^23 + 128 yields the signed value; the
 // difference of two such floats is exact.
 __device__ __forceinline__ void pair_to_f(uint32_t p, float& c0, float& dc) {
-    const float f0 = __int_as_float(static_cast<int>((p & 0xFFu) ^ 0x4B000080u));
-    const float f1 = __int_as_float(static_cast<int>(((p >> 8) & 0xFFu) ^ 0x4B000080u));
+    const uint32_t q = p ^ 0x8080u;
+    const float f0 = __int_as_float(static_cast<int>(__byte_perm(q, 0x4B000000u, 0x7440)));
+    const float f1 = __int_as_float(static_cast<int>(__byte_perm(q, 0x4B000000u, 0x7441)));
     c0 = f0 - 8388736.0f;
     dc = f1 - f0;
+}
+
+// 2^x on the SFU, no range fix-up (arguments here are far from the
+// denormal range or produce a gain that is zeroed anyway)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 // locate() for N independent inputs in lock step: the same operations as
@@ -218,6 +268,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Slice c of P of [base, base+bytes) prefetched into L2 (no shared memory,
+// no completion tracking).  Slices are 16-byte granular.
+__device__ __forceinline__ void prefetch_l2_slice(const void* base, size_t bytes, int c, int P) {
+    const size_t chunk = ((bytes + P - 1) / P + 15) & ~static_cast<size_t>(15);
+    const size_t off = chunk * c;
+    if (off >= bytes) return;
+    const size_t n = (bytes - off < chunk ? bytes - off : chunk) & ~static_cast<size_t>(15);
+    if (n == 0) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(base) + off),
+                 "r"(static_cast<uint32_t>(n))
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -74,6 +74,13 @@ struct DevLayer {
     double q_eps;            // fast locate trusts floor((x-lo)*inv_dx) when its fraction is
                              // more than q_eps from an integer (< 0: always search)
     float lo_f, inv_dx_f;    // float(lo), float(1/dx): fast locate's t
+    float hi_f;              // float(hi)
+    float qf_eps;            // bracket_f32 trusts its fp32 bracket when the fraction of
+                             // (float(x)-lo_f)*inv_dx_f is more than qf_eps from an integer (< 0: never)
+    // fast-path int8 gain, computed instead of looked up:
+    //   float(gain(code) * cs) ~= exp2(g_base + code * g_step), code 127 -> 0
+    // with g_base = log_min + log2(cs) (dequantize_gain_code, quant.cpp:88-91)
+    float g_base, g_step;
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -125,26 +132,26 @@ struct HeadB1Args {
     int nl;
     DevLayer L[kMaxHeadLayers];
     int planes0;       // layer 0 served from shared-memory pair planes
+    int x_tma;         // x may be bulk-copied (16-byte aligned, in0*8 % 16 == 0)
     const double* x;   // [in]
     double* y;         // [out]
     float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
-    unsigned* flags;   // [grid] per-CTA barrier epochs (monotonic across launches)
-    unsigned epoch;    // this launch's epoch base (barrier k waits for epoch + k + 1)
+    unsigned* done;    // monotonic arrival counter of the last layer (last CTA reduces)
+    unsigned epoch;    // value of *done when this launch starts
     int* err;
     unsigned long long* timeline;  // optional: [grid][16] %globaltimer stamps per phase
     int rec_cap;           // layer-0 rows whose records are staged in shared memory
     unsigned pref_mask;    // row-split layers whose records are prefetched at kernel start
     unsigned pref_offset;  // byte offset of the prefetch region in dynamic shared memory
 };
-constexpr unsigned kHeadB1EpochStride = 16;  // >= layers + 1 barriers per launch
 bool head_b1_supported(const DevLayer* L, int nl);
 // Shared-memory plan of the batch-1 kernel; fills h->planes0, rec_cap,
 // pref_mask, pref_offset.
-size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h, int* nv);
-void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, int nv, cudaStream_t s);
+size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h);
+void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s);
 // Grid for which all CTAs are co-resident (one per SM), or 0 if the kernel
 // cannot be resident at this shared-memory size.
-int head_b1_max_grid(size_t smem, int nv, int num_sms);
+int head_b1_max_grid(size_t smem, int num_sms);
 
 // Workspace device buffers (one forward stream).
 struct DevScratch {

@@ -17,9 +17,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_15742_b200 as hq  # noqa: E402
 from paper_2512_15742_b200 import _lib, synthetic  # noqa: E402
 
-PHASES = {0: "start", 1: "luts", 13: "x staged", 2: "locate+hist", 3: "alloc+tma", 4: "rowlist", 5: "plane ready",
-          6: "rows done", 7: "L0 partial", 8: "grid sync 1", 9: "L1 reduce+locate", 10: "L1 rows",
-          11: "grid sync 2", 12: "end"}
+PHASES = {0: "start", 1: "tables", 2: "x ready", 3: "locate+hist", 4: "rowlist+tma", 5: "plane ready",
+          6: "L0 partial", 7: "grid sync 1", 9: "L1 reduce+locate", 10: "L1 rows", 11: "grid sync 2",
+          12: "final start", 13: "end"}
 
 
 def main():
@@ -59,7 +59,11 @@ def main():
         torch.cuda.synchronize()
         s = stamps.view(grid, 16).cpu().numpy().astype(np.float64)
         t0 = s[:, 0].min()
-        print(f"rep {rep}: kernel span {(s[:, 12].max() - t0) / 1e3:.2f} us")
+        print(f"rep {rep}: kernel span {(s[:, 13].max() - t0) / 1e3:.2f} us")
+        last = np.flatnonzero(s[:, 15] > 0)
+        if last.size:
+            r = s[last[0]]
+            print(f"   last CTA {last[0]}: {(r[15] - r[14]) / max(r[13] - r[0], 1) * 1e3:.0f} MHz over its span")
         for p, name in PHASES.items():
             col = s[:, p]
             col = col[col > 0]

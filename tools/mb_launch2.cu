@@ -1,0 +1,103 @@
+// Launch-overhead variants of a kernel shaped like the batch-1 head kernel
+// (148 CTAs x 256 threads): parameter-block size, cooperative attribute,
+// 205 KB dynamic shared memory, PDL; CUDA-event median of 200 launches,
+// after a 256 MiB memset (flush) or back to back.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/mb_launch2.cu -o tools/bin/mb_launch2
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+struct Big {
+    char pad[1800];
+    int* p;
+};
+struct Small {
+    int* p;
+};
+
+template <class A>
+__global__ void k_empty(A a) {
+    extern __shared__ int s[];
+    if (a.p && threadIdx.x == 0 && blockIdx.x == 100000) *a.p = s[0];
+}
+
+template <class A>
+__global__ void k_sync(A a) {
+    cooperative_groups::this_grid().sync();
+    if (a.p && threadIdx.x == 0 && blockIdx.x == 100000) *a.p = 1;
+}
+
+static float* g_flush;
+static size_t g_flush_n = (256u << 20) / 4;
+
+template <class F>
+float time_it(F launch, bool flush, int reps = 200) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    std::vector<float> t;
+    for (int r = 0; r < reps + 10; ++r) {
+        if (flush) cudaMemsetAsync(g_flush, r & 0xFF, g_flush_n * 4, s);
+        cudaEventRecord(a, s);
+        launch(s);
+        cudaEventRecord(b, s);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (r >= 10) t.push_back(ms * 1e3f);
+    }
+    std::sort(t.begin(), t.end());
+    cudaStreamDestroy(s);
+    return t[t.size() / 2];
+}
+
+template <class K, class A>
+void launch_ex(K k, A a, int grid, size_t smem, bool coop, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = coop ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, a);
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaMalloc(&g_flush, g_flush_n * 4);
+    const size_t big_smem = 205 * 1024;
+    cudaFuncSetAttribute(k_empty<Small>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
+    cudaFuncSetAttribute(k_empty<Big>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
+    cudaFuncSetAttribute(k_sync<Big>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
+    for (int i = 0; i < 2000; ++i) cudaMemsetAsync(g_flush, 0, g_flush_n * 4);
+    cudaDeviceSynchronize();
+    Small sm{nullptr};
+    Big bg{};
+    bg.p = nullptr;
+    for (int fl = 0; fl < 2; ++fl) {
+        const bool f = fl == 1;
+        printf("--- flush=%d\n", fl);
+        printf("small params, 0 smem          %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Small>, sm, sms, 0, false, s); }, f));
+        printf("1.8 KB params, 0 smem         %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Big>, bg, sms, 0, false, s); }, f));
+        printf("1.8 KB params, 205 KB smem    %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Big>, bg, sms, big_smem, false, s); }, f));
+        printf("  + cooperative attr          %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Big>, bg, sms, big_smem, true, s); }, f));
+        printf("  + cooperative + grid.sync   %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_sync<Big>, bg, sms, big_smem, true, s); }, f));
+        printf("  two launches back to back   %7.2f us\n", time_it([&](cudaStream_t s) {
+                   launch_ex(k_empty<Big>, bg, sms, big_smem, false, s);
+                   launch_ex(k_empty<Big>, bg, sms, big_smem, false, s);
+               }, f));
+    }
+    cudaError_t e = cudaDeviceSynchronize();
+    printf("status %s\n", cudaGetErrorString(e));
+    return 0;
+}
