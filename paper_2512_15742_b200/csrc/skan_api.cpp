@@ -565,6 +565,9 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
         h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan);
         h->b1_plan.nl = nl;
         for (int l = 0; l < nl; ++l) h->b1_plan.L[l] = h->dl[l];
+        const DevLayer& L0 = h->dl[0];
+        for (int i = 0; i < L0.G && i < 33; ++i)  // node_position, kan.cpp:21-26
+            h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
         h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->num_sms);
         if (h->b1_grid > 0) {
             h->b1_ok = true;

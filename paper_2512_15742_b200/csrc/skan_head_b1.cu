@@ -157,6 +157,27 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
     }
 }
 
+// floor(a / b) for 0 <= a < 2^24, b >= 1: correctly rounded fp32 quotient,
+// one integer fix-up each way (no 32-bit integer division sequence)
+__device__ __forceinline__ int idiv_small(int a, int b) {
+    int q = static_cast<int>(__fdiv_rn(static_cast<float>(a), static_cast<float>(b)));
+    if ((q + 1) * b <= a) ++q;
+    if (q * b > a) --q;
+    return q;
+}
+
+// Exact bracket of an in-domain (or clamped) x from a bracket estimate
+// within one of the answer, by double comparisons against the reference's
+// node positions (kan.cpp:21-58: the unique i with node(i) <= x < node(i+1)).
+__device__ __forceinline__ int bracket_exact(const double* node, const DevLayer& L, double x, int est) {
+    if (!(x > L.lo)) return 0;
+    if (!(x < L.hi)) return L.G - 2;
+    int i = min(max(est, 0), L.G - 2);
+    if (x < node[i]) --i;
+    else if (x >= node[i + 1]) ++i;
+    return i;
+}
+
 // Pair-plane layer 0.  Shared memory: [plane K*2 B][records rec_cap rows x
 // out x 4 B]; x, t and brackets of all inputs are staged in the record
 // region first (free until the records land).  Rows beyond rec_cap (only
@@ -187,23 +208,34 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
         __syncthreads();
     }
     stamp(h, 2);
-    // 1. brackets of all inputs, input i by thread i % kT: fp32 estimate,
-    //    exact fp64 locate only where it is undecided (t is computed later,
-    //    for this CTA's rows only)
+    // 1. brackets of all inputs, input i by thread i % kT: fp32 estimate; the
+    //    undecided (near a knot, at the domain ends) settle by exact double
+    //    comparisons against the node table; t comes later, for this CTA's
+    //    rows only
     {
         int m[kMaxPer];
         unsigned hard = 0;
 #pragma unroll
         for (int q = 0; q < kMaxPer; ++q) {
             const int i = tid + q * kT;
+            m[q] = -1;
             if (i < L.in && !bracket_f32(L, s_x[i], m[q])) hard |= 1u << q;
         }
 #pragma unroll 1
         for (; hard; hard &= hard - 1) {
             const int q = __ffs(hard) - 1;
+            int est = -1;
+#pragma unroll
+            for (int u = 0; u < kMaxPer; ++u)
+                if (u == q) est = m[u];
+            const double x = s_x[tid + q * kT];
             int mm;
-            float tt;
-            fast_locate(L, s_x[tid + q * kT], h.err, mm, tt);
+            if (!finite_bits(x) || !(L.qf_eps >= 0.f)) {
+                float tt;
+                fast_locate(L, x, h.err, mm, tt);
+            } else {
+                mm = bracket_exact(h.node0, L, x, est);
+            }
 #pragma unroll
             for (int u = 0; u < kMaxPer; ++u)
                 if (u == q) m[u] = mm;
@@ -238,7 +270,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
         const int P = gridDim.x;
         const int n = lane < GP ? s_cnt[lane] : 0;
         const int nonempty = __popc(__ballot_sync(0xFFFFFFFFu, n > 0));
-        const int alloc = n > 0 ? 1 + (P - nonempty) * n / L.in : 0;
+        const int alloc = n > 0 ? 1 + idiv_small((P - nonempty) * n, L.in) : 0;
         int incl = alloc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -249,7 +281,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
         const bool mine = c >= incl - alloc && c < incl;
         if (mine) {  // at most one lane
             const int q = c - (incl - alloc);
-            const int lo = n * q / alloc, hi = n * (q + 1) / alloc;
+            const int lo = idiv_small(n * q, alloc), hi = idiv_small(n * (q + 1), alloc);
             s_bucket = lane;
             s_lo = lo;
             s_hi = hi;
@@ -305,11 +337,14 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
         for (uint32_t mk = hits[u]; mk; mk &= mk - 1) {
             const int i = (tid * wpt + u) * 4 + (__ffs(mk) - 1) / 8;
             if (rank >= 0 && rank < nrows) {
-                int mm;
-                float tt;
-                fast_locate(L, s_x[i], h.err, mm, tt);  // exact bracket, t for this row
+                // t of this row (fast path: float(x - node(m)) / dx, t = 1 at or past the upper node)
+                const double x = s_x[i];
+                float t;
+                if (!(x > L.lo)) t = 0.f;
+                else if (!(x < L.hi) || x >= h.node0[bucket + 1]) t = 1.f;
+                else t = fminf(fmaxf(__double2float_rn(__dsub_rn(x, h.node0[bucket])) * L.inv_dx_f, 0.f), 1.f);
                 s_rows[rank] = i;
-                s_trow[rank] = tt;
+                s_trow[rank] = t;
             }
             ++rank;
         }

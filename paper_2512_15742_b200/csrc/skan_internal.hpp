@@ -143,6 +143,7 @@ struct HeadB1Args {
     int rec_cap;           // layer-0 rows whose records are staged in shared memory
     unsigned pref_mask;    // row-split layers whose records are prefetched at kernel start
     unsigned pref_offset;  // byte offset of the prefetch region in dynamic shared memory
+    double node0[33];      // layer 0's node positions (kan.cpp:21-26), G <= 33
 };
 bool head_b1_supported(const DevLayer* L, int nl);
 // Shared-memory plan of the batch-1 kernel; fills h->planes0, rec_cap,

@@ -31,7 +31,7 @@ def main():
     model = hq.build_model(cn)
     ws = hq.make_workspace(model, 1)
     grid = _lib.lib().skan_head_b1_grid(model.handle)
-    stamps = torch.zeros(grid * 16, dtype=torch.int64, device="cuda")
+    stamps = torch.zeros(2 * grid * 16, dtype=torch.int64, device="cuda")
     _lib.check(_lib.lib().skan_debug_b1_timeline(ws.handle, stamps.data_ptr()))
     x = torch.from_numpy(synthetic.synthetic_inputs(1, 2048, seed=1)).cuda()
     y = torch.zeros(20, dtype=torch.float64, device="cuda")
@@ -57,7 +57,8 @@ def main():
         do_flush()
         hq.forward_async(model, x, 1, y, ws)
         torch.cuda.synchronize()
-        s = stamps.view(grid, 16).cpu().numpy().astype(np.float64)
+        both = stamps.view(2, grid, 16).cpu().numpy().astype(np.float64)
+        s, cs = both[0], both[1]
         t0 = s[:, 0].min()
         print(f"rep {rep}: kernel span {(s[:, 13].max() - t0) / 1e3:.2f} us")
         last = np.flatnonzero(s[:, 15] > 0)
@@ -71,6 +72,11 @@ def main():
                 continue
             rel = (col - t0) / 1e3
             print(f"   {p:2d} {name:18s} min {rel.min():7.2f}  med {np.median(rel):7.2f}  max {rel.max():7.2f}")
+        used = [k for k in range(16) if (cs[:, k] > 0).all()]
+        if len(used) > 1:
+            d = np.diff(cs[:, used], axis=1)
+            print("   clock64 deltas between fine stamps (cycles, median over CTAs):",
+                  {f"{a}->{b}": int(np.median(d[:, q])) for q, (a, b) in enumerate(zip(used[:-1], used[1:]))})
 
 
 if __name__ == "__main__":
