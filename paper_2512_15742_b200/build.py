@@ -39,6 +39,36 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+
+
+REF_INCLUDE = "/root/reference/proj/include"
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_lutham_b200.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "bin", "test_lutham_b200")
+
+
+def build_cpp_tests(force: bool = False) -> str | None:
+    """Compile the C++ drop-in parity test (tests/cpp) against the reference
+    headers and the reference library in oracle/_ref (the checker).  Only
+    possible where /root/reference exists; the binary travels to the GPU box
+    with the snapshot.  Returns the binary path, or None if unbuildable here."""
+    ref_so = os.path.join(ROOT, "oracle", "_ref", "libholoquant_ref.so")
+    if not (os.path.isdir(REF_INCLUDE) and os.path.exists(ref_so)):
+        return CPP_TEST_BIN if os.path.exists(CPP_TEST_BIN) else None
+    deps = [CPP_TEST_SRC, os.path.join(ROOT, "include", "holoquant", "lutham_b200.hpp"),
+            os.path.join(ROOT, "include", "skan.h"), OUT, ref_so]
+    if (not force and os.path.exists(CPP_TEST_BIN)
+            and all(os.path.getmtime(d) <= os.path.getmtime(CPP_TEST_BIN) for d in deps)):
+        return CPP_TEST_BIN
+    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I" + REF_INCLUDE, "-I" + os.path.join(ROOT, "include"),
+           CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+           "-L" + os.path.dirname(ref_so), "-lholoquant_ref", "-L" + HERE, "-lskan",
+           "-Wl,-rpath,$ORIGIN/../../../oracle/_ref", "-Wl,-rpath,$ORIGIN/../../../paper_2512_15742_b200",
+           "-lpthread"]
+    subprocess.run(cmd, check=True)
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     build_library(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(OUT)

@@ -715,13 +715,23 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
     return launches;
 }
 
-void check_forward_args(const skan_head* h, const skan_workspace* ws, int batch) {
+// Validation in compressed_forward's order (lutham.cpp:821-834): model,
+// batch, spans (checked by the caller in between), then the workspace.
+void check_head_batch(const skan_head* h, int batch) {
     if (!h) raise(SKAN_SHAPE_ERROR, "model has no layers");
     if (batch < 0) raise(SKAN_SHAPE_ERROR, "batch must be nonnegative");
+}
+
+void check_workspace_for(const skan_head* h, const skan_workspace* ws) {
     if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
     if (ws->width < h->max_width)
         raise(SKAN_CONTRACT_ERROR, "workspace is smaller than the model's widest layer");
     if (ws->device != h->device) raise(SKAN_CONTRACT_ERROR, "workspace lives on another device");
+}
+
+void check_forward_args(const skan_head* h, const skan_workspace* ws, int batch) {
+    check_head_batch(h, batch);
+    check_workspace_for(h, ws);
 }
 
 }  // namespace
@@ -895,12 +905,13 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
                          uint64_t n_inputs, int batch, double* outputs, uint64_t n_outputs,
                          int mode, unsigned ptr_flags, void* stream) {
     return guarded([&] {
-        check_forward_args(h, ws, batch);
+        check_head_batch(h, batch);
         const uint64_t in = static_cast<uint64_t>(h->in_dim), out = static_cast<uint64_t>(h->out_dim);
         if (n_inputs != in * static_cast<uint64_t>(batch))
             raise(SKAN_SHAPE_ERROR, "input buffer does not match batch * input_dim");
         if (n_outputs != out * static_cast<uint64_t>(batch))
             raise(SKAN_SHAPE_ERROR, "output buffer does not match batch * output_dim");
+        check_workspace_for(h, ws);
         if (mode != SKAN_MODE_FAST && mode != SKAN_MODE_EXACT) raise(SKAN_CONTRACT_ERROR, "unknown mode");
         const bool exact = mode == SKAN_MODE_EXACT;
         const bool host = (ptr_flags & SKAN_PTR_DEVICE) == 0;

@@ -20,11 +20,25 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--batches", default="1,2,4,8,16,64,256")
+    ap.add_argument("--flush-with", choices=["torch", "memset"], default="torch",
+                    help="L2 flush: a torch fill kernel, or cudaMemsetAsync")
     args = ap.parse_args()
     cn = synthetic.synthetic_head()
     model = hq.build_model(cn)
     ws = hq.make_workspace(model, 256)
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    if args.flush_with == "memset":
+        import ctypes
+        import glob
+        rt = ctypes.CDLL(sorted(glob.glob("/usr/local/cuda/lib64/libcudart.so.12*"))[0])
+        rt.cudaMemsetAsync.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p]
+
+        class _F:
+            def zero_(self):
+                rt.cudaMemsetAsync(flush.data_ptr(), 0, flush.numel() * 4, torch.cuda.current_stream().cuda_stream)
+        flusher = _F()
+    else:
+        flusher = flush
     s = torch.cuda.Stream()
     t_end = time.perf_counter() + 1.0
     while time.perf_counter() < t_end:
@@ -37,7 +51,7 @@ def main():
             with torch.cuda.stream(s):
                 for r in range(args.reps + 5):
                     if fl:
-                        flush.zero_()
+                        flusher.zero_()
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record(s)
                     hq.forward_async(model, x, B, y, ws, stream=s.cuda_stream)

@@ -11,7 +11,7 @@
 #include <vector>
 
 struct Big {
-    char pad[1800];
+    char pad[2100];
     int* p;
 };
 struct Small {
@@ -32,6 +32,11 @@ __global__ void k_sync(A a) {
 
 static float* g_flush;
 static size_t g_flush_n = (256u << 20) / 4;
+static bool g_kernel_flush = false;
+
+__global__ void k_fill(float* p, size_t n, float v) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) p[i] = v;
+}
 
 template <class F>
 float time_it(F launch, bool flush, int reps = 200) {
@@ -42,7 +47,10 @@ float time_it(F launch, bool flush, int reps = 200) {
     cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
     std::vector<float> t;
     for (int r = 0; r < reps + 10; ++r) {
-        if (flush) cudaMemsetAsync(g_flush, r & 0xFF, g_flush_n * 4, s);
+        if (flush) {
+            if (g_kernel_flush) k_fill<<<148 * 8, 256, 0, s>>>(g_flush, g_flush_n, float(r));
+            else cudaMemsetAsync(g_flush, r & 0xFF, g_flush_n * 4, s);
+        }
         cudaEventRecord(a, s);
         launch(s);
         cudaEventRecord(b, s);
@@ -60,7 +68,7 @@ template <class K, class A>
 void launch_ex(K k, A a, int grid, size_t smem, bool coop, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(384);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -75,7 +83,7 @@ int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaMalloc(&g_flush, g_flush_n * 4);
-    const size_t big_smem = 205 * 1024;
+    const size_t big_smem = 218 * 1024;
     cudaFuncSetAttribute(k_empty<Small>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
     cudaFuncSetAttribute(k_empty<Big>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
     cudaFuncSetAttribute(k_sync<Big>, cudaFuncAttributeMaxDynamicSharedMemorySize, big_smem);
@@ -84,9 +92,10 @@ int main() {
     Small sm{nullptr};
     Big bg{};
     bg.p = nullptr;
-    for (int fl = 0; fl < 2; ++fl) {
-        const bool f = fl == 1;
-        printf("--- flush=%d\n", fl);
+    for (int fl = 0; fl < 3; ++fl) {
+        const bool f = fl >= 1;
+        g_kernel_flush = fl == 2;
+        printf("--- flush=%s\n", fl == 0 ? "none" : (fl == 1 ? "memset" : "fill kernel"));
         printf("small params, 0 smem          %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Small>, sm, sms, 0, false, s); }, f));
         printf("1.8 KB params, 0 smem         %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Big>, bg, sms, 0, false, s); }, f));
         printf("1.8 KB params, 205 KB smem    %7.2f us\n", time_it([&](cudaStream_t s) { launch_ex(k_empty<Big>, bg, sms, big_smem, false, s); }, f));
