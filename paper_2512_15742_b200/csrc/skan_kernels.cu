@@ -548,39 +548,40 @@ size_t planes_smem(const DevLayer& L, int nv) {
 
 // ---------------------------------------------------------------------------
 // k_fwd_large: samples in lanes.  CTA = 8 warps = 4 sample-warps (128
-// samples) x 2 output-warps (16 outputs each) -> tile 128 samples x 32
+// samples) x 2 output-warps (VJ outputs each) -> tile 128 samples x 2*VJ
 // outputs, over a split of the input rows processed in chunks of IC rows.
 // Per chunk every edge of the tile is decoded ONCE (record + 16-byte padded
 // codebook row) into shared memory as gained pairs (g*c[m], g*(c[m+1]-c[m])),
-// m = 0..G-2; a thread then evaluates its 16 outputs for its sample with one
+// m = 0..G-2; a thread then evaluates its VJ outputs for its sample with one
 // broadcast LDS.64 per edge-sample (lanes of a warp hit <= G-1 distinct
-// pairs of one edge: one wavefront).  Staging of chunk c+1 is prefetched into
-// registers while chunk c is computed.  int8 tables, G <= 16.
+// pairs of one edge) at an immediate offset when G is a compile-time
+// constant (GPT > 0).  A row's bracket and t arrive as one 8-byte word.
+// Staging of chunk c+1 is prefetched into registers while chunk c is
+// computed.  int8 tables, G <= 16.
 
 constexpr int kLgSW = 4;                // sample-warps
 constexpr int kLgJW = 2;                // output-warps
-constexpr int kLgVJ = 16;               // outputs per thread
 constexpr int kLgS = 32 * kLgSW;        // samples per CTA
-constexpr int kLgJ = kLgJW * kLgVJ;     // outputs per CTA
 
-template <int FMT, int EPT>  // EPT: staged edges per thread per chunk
+template <int FMT, int EPT, int GPT, int VJ>  // EPT: staged edges per thread per chunk; GPT: G-1 or 0
 __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
-    constexpr int IC = EPT * 256 / kLgJ;  // input rows per chunk
+    constexpr int kJ = kLgJW * VJ;       // outputs per CTA
+    constexpr int IC = EPT * 256 / kJ;   // input rows per chunk
     extern __shared__ __align__(128) unsigned char smem[];
     const DevLayer& L = a.L;
-    const int G = L.G, GP = G - 1;
-    // layout: pairs[2][IC][kLgJ][GP] float2 | m[2][IC][kLgS] int | t[2][IC][kLgS] float | lut[256]
+    const int G = L.G;
+    const int GP = GPT > 0 ? GPT : G - 1;
+    // layout: pairs[2][IC][kJ][GP] float2 | mt[2][IC][kLgS] {m, t} | lut[256]
     float2* s_pair = reinterpret_cast<float2*>(smem);
-    const size_t pair_buf = static_cast<size_t>(IC) * kLgJ * GP;
-    int* s_m = reinterpret_cast<int*>(s_pair + 2 * pair_buf);
-    float* s_t = reinterpret_cast<float*>(s_m + 2 * IC * kLgS);
-    float* s_lut = s_t + 2 * IC * kLgS;
+    const size_t pair_buf = static_cast<size_t>(IC) * kJ * GP;
+    int2* s_mt = reinterpret_cast<int2*>(s_pair + 2 * pair_buf);
+    float* s_lut = reinterpret_cast<float*>(s_mt + 2 * IC * kLgS);
     __shared__ int s_last;
     pdl_trigger();
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int sw = warp % kLgSW, jw = warp / kLgSW;
-    const int jbase = blockIdx.x * kLgJ;
+    const int jbase = blockIdx.x * kJ;
     const int s0 = blockIdx.z * kLgS;
     const int nS = min(kLgS, a.B - s0);
     const int r0 = blockIdx.y * a.rows_per_cta;
@@ -596,7 +597,7 @@ __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
         ok = 0;
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
-            const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
+            const int q = tid + 256 * u, il = q / kJ, jl = q % kJ;
             const int i = r0 + c * IC + il, j = jbase + jl;
             if (i < rend && j < L.out) {
                 ok |= 1u << u;
@@ -624,8 +625,8 @@ __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
         float2* dst = s_pair + buf * pair_buf;
 #pragma unroll
         for (int u = 0; u < EPT; ++u) {
-            const int q = tid + 256 * u, il = q / kLgJ, jl = q % kLgJ;
-            float2* d = dst + (static_cast<size_t>(il) * kLgJ + jl) * GP;
+            const int q = tid + 256 * u, il = q / kJ, jl = q % kJ;
+            float2* d = dst + (static_cast<size_t>(il) * kJ + jl) * GP;
             float g = 0.f;  // absent edges stage zeros
             if (ok & (1u << u)) {
                 int gc;
@@ -659,14 +660,13 @@ __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
                 m = a.bm_in[p];
                 t = a.bt_in[p];
             }
-            s_m[(buf * IC + il) * kLgS + sl] = m;
-            s_t[(buf * IC + il) * kLgS + sl] = t;
+            s_mt[(buf * IC + il) * kLgS + sl] = make_int2(m, __float_as_int(t));
         }
     };
 
-    float acc[kLgVJ];
+    float acc[VJ];
 #pragma unroll
-    for (int v = 0; v < kLgVJ; ++v) acc[v] = 0.f;
+    for (int v = 0; v < VJ; ++v) acc[v] = 0.f;
     const int sl = sw * 32 + lane;
 
     if (nchunks > 0) {
@@ -681,20 +681,21 @@ __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
     } else {
         pdl_wait();
     }
+#pragma unroll 1
     for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
         const bool more = c + 1 < nchunks;
         if (more) load_rows();  // rows of chunk c+1 fly while chunk c is computed
-        const float2* P = s_pair + buf * pair_buf;
-        const int* M = s_m + buf * IC * kLgS;
-        const float* T = s_t + buf * IC * kLgS;
+        const float2* P = s_pair + buf * pair_buf + static_cast<size_t>(jw * VJ) * GP;
+        const int2* MT = s_mt + buf * IC * kLgS + sl;
         const int nrow = min(IC, rend - (r0 + c * IC));
+#pragma unroll 2
         for (int il = 0; il < nrow; ++il) {
-            const int m = M[il * kLgS + sl];
-            const float t = T[il * kLgS + sl];
-            const float2* e = P + (static_cast<size_t>(il) * kLgJ + jw * kLgVJ) * GP + m;
+            const int2 mt = MT[il * kLgS];
+            const float t = __int_as_float(mt.y);
+            const float2* e = P + static_cast<size_t>(il) * kJ * GP + mt.x;
 #pragma unroll
-            for (int v = 0; v < kLgVJ; ++v) {
+            for (int v = 0; v < VJ; ++v) {
                 const float2 p = e[v * GP];
                 acc[v] += fmaf(t, p.y, p.x);
             }
@@ -710,13 +711,13 @@ __global__ void __launch_bounds__(256) k_fwd_large(FwdArgs a) {
     const size_t plane = static_cast<size_t>(a.B) * L.out;
     if (sl < nS) {
 #pragma unroll
-        for (int v = 0; v < kLgVJ; ++v) {
-            const int j = jbase + jw * kLgVJ + v;
+        for (int v = 0; v < VJ; ++v) {
+            const int j = jbase + jw * VJ + v;
             if (j < L.out) a.partial[blockIdx.y * plane + static_cast<size_t>(s0 + sl) * L.out + j] = acc[v];
         }
     }
     if (!arrive_last(a.counters + blockIdx.x * gridDim.z + blockIdx.z, gridDim.y, &s_last)) return;
-    finish_tile(a, gridDim.y, s0, nS, jbase, min(kLgJ, L.out - jbase));
+    finish_tile(a, gridDim.y, s0, nS, jbase, min(kJ, L.out - jbase));
 }
 
 // ---------------------------------------------------------------------------
@@ -991,14 +992,25 @@ void dispatch_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
     }
 }
 
-size_t large_smem(int G, int ept) {
-    const size_t ic = static_cast<size_t>(ept) * 256 / kLgJ;
-    return 2 * ic * kLgJ * (G - 1) * sizeof(float2) + 2 * ic * kLgS * (sizeof(int) + sizeof(float)) +
-           256 * sizeof(float);
+size_t large_smem(int G, int ept, int vj) {
+    const size_t kj = static_cast<size_t>(kLgJW) * vj;
+    const size_t ic = static_cast<size_t>(ept) * 256 / kj;
+    return 2 * ic * kj * (G - 1) * sizeof(float2) + 2 * ic * kLgS * sizeof(int2) + 256 * sizeof(float);
 }
 
 // Shared-memory budget of one large-batch CTA: two fit per SM.
 constexpr size_t kLgSmemBudget = 110 * 1024;
+
+template <int FMT, int EPT, int VJ>
+void (*large_kernel_g(int G))(FwdArgs) {
+    return G == 10 ? k_fwd_large<FMT, EPT, 9, VJ> : k_fwd_large<FMT, EPT, 0, VJ>;
+}
+
+template <int FMT>
+void (*large_kernel(int G, int ept, int vj))(FwdArgs) {
+    if (vj == 32) return ept == 2 ? large_kernel_g<FMT, 2, 32>(G) : large_kernel_g<FMT, 1, 32>(G);
+    return ept == 2 ? large_kernel_g<FMT, 2, 16>(G) : large_kernel_g<FMT, 1, 16>(G);
+}
 
 }  // namespace
 
@@ -1032,26 +1044,26 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
     }
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {
-        // samples in lanes: tile 128 samples x 32 outputs x split of the rows
+        // samples in lanes: tile 128 samples x (32 or 64) outputs x split of the rows
         c.kind = 1;
-        int ept = 4;
-        while (ept > 1 && large_smem(L.G, ept) > kLgSmemBudget) ept >>= 1;
+        c.tj = 32;                        // outputs per CTA (64 measured slower: more staging conflicts)
+        c.spt = c.tj / kLgJW;             // outputs per thread (VJ)
+        int ept = 2;
+        while (ept > 1 && large_smem(L.G, ept, c.spt) > kLgSmemBudget) ept >>= 1;
         c.vj = ept;
-        c.ic = ept * 256 / kLgJ;
-        c.jt = (L.out + kLgJ - 1) / kLgJ;
+        c.ic = ept * 256 / c.tj;
+        c.jt = (L.out + c.tj - 1) / c.tj;
         c.st = (B + kLgS - 1) / kLgS;
         const long long base = static_cast<long long>(c.jt) * c.st;
         long long ns = (2LL * sms + base - 1) / base;  // ~2 CTAs per SM, one wave
-        if (ns > 16) ns = 16;                          // bounds the finisher's partial traffic
+        if (ns > 16) ns = 16;                          // bounds the finisher's work (last CTA per tile)
         const long long maxns = (L.in + c.ic - 1) / c.ic;
         ns = ns < 1 ? 1 : (ns > maxns ? maxns : ns);
         const int chunks = static_cast<int>((L.in + c.ic - 1) / c.ic);
         const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
         c.ichunk = per * c.ic;
         c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
-        c.smem = large_smem(L.G, ept);
-        c.tj = kLgJ;
-        c.spt = 0;
+        c.smem = large_smem(L.G, ept, c.spt);
         return c;
     }
     // rows in warps: 8 warps x rw rows, 32*vj outputs, S samples
@@ -1096,11 +1108,8 @@ void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_
         return;
     }
     if (c.kind == 1) {
-        void (*k)(FwdArgs);
-        const bool r32 = a.L.fmt == FMT_I8_R32;
-        if (c.vj == 4) k = r32 ? k_fwd_large<FMT_I8_R32, 4> : k_fwd_large<FMT_I8_WIDE, 4>;
-        else if (c.vj == 2) k = r32 ? k_fwd_large<FMT_I8_R32, 2> : k_fwd_large<FMT_I8_WIDE, 2>;
-        else k = r32 ? k_fwd_large<FMT_I8_R32, 1> : k_fwd_large<FMT_I8_WIDE, 1>;
+        void (*k)(FwdArgs) = a.L.fmt == FMT_I8_R32 ? large_kernel<FMT_I8_R32>(a.L.G, c.vj, c.spt)
+                                                    : large_kernel<FMT_I8_WIDE>(a.L.G, c.vj, c.spt);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
         launch_ex(k, dim3(c.jt, c.nsplit, c.st), dim3(256), c.smem, pdl, s, a);
         return;
