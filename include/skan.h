@@ -255,6 +255,13 @@ skan_status skan_debug_b1_timeline(skan_workspace* ws, unsigned long long* d_sta
 /* Grid size of the persistent batch-1 kernel for head (0 if not eligible). */
 int skan_head_b1_grid(const skan_head* head);
 
+/* Self-test of the tensor-core building blocks (no reference counterpart):
+ * D[128][N] = A[128][K] * B[K][N] (row-major f32, device pointers) on
+ * tcgen05 kind::tf32 with `passes` = 1 (plain tf32) or 3 (split-precision
+ * 3xTF32).  N in [16, 256] step 16, K in [8, 64] step 8. */
+skan_status skan_debug_gemm_tf32(const float* d_a, const float* d_b, float* d_d, int n, int k, int passes,
+                                 void* stream);
+
 /* ---- single-edge primitive (lutham.cpp:730-755) ----------------------- */
 
 /* Batched pli_lookup over n independent (row, g, b, x) tuples on the GPU:

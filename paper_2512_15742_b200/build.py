@@ -11,8 +11,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("skan_kernels.cu", "skan_head_b1.cu", "skan_api.cpp", "skan_format.cpp")]
-HEADERS = [os.path.join(CSRC, "skan_internal.hpp"), os.path.join(CSRC, "skan_device.cuh"), os.path.join(ROOT, "include", "skan.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("skan_kernels.cu", "skan_head_b1.cu", "skan_gemm.cu", "skan_api.cpp",
+                                           "skan_format.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("skan_internal.hpp", "skan_device.cuh", "skan_tc.cuh")] + [
+    os.path.join(ROOT, "include", "skan.h")]
 OUT = os.path.join(HERE, "libskan.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -657,7 +657,7 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const std::vector<
     }
     a.err = d.err;
     skan::launch_fwd_fast(a, c, chained, s);
-    return launches + 1;
+    return launches + (c.kind == 4 ? 2 : 1);  // the tensor-core GEMM is followed by its split reduction
 }
 
 // Enqueue one chunk (B <= ws->max_batch) on `s`; x/y are device pointers.

@@ -1,0 +1,486 @@
+// tcgen05 kind::tf32 GEMM, three-pass split precision ("3xTF32"):
+//     A*B ~= A_hi*B_hi + A_hi*B_lo + A_lo*B_hi
+// with x_hi = the tensor core's own tf32 truncation of x and x_lo = x - x_hi
+// (exact in f32), accumulated in f32 in TMEM: ~2^-21 relative per product,
+// inside the fast path's 1e-5 (L1-scaled) bar where a single tf32 pass
+// (~2^-11) is not.
+//
+// k_debug_gemm is the self-test of the building blocks in skan_tc.cuh: one
+// CTA, 128 x N (N <= 256) x K (K <= 64) from row-major f32 A [128][K] and
+// B [K][N] staged by plain threads into the canonical K-major layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "skan_internal.hpp"
+#include "skan_tc.cuh"
+
+namespace skan {
+namespace {
+
+__global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ D, int N, int K, int passes) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_tmem;
+    constexpr int M = 128;
+    unsigned char* a_hi = smem;
+    unsigned char* a_lo = a_hi + M * K * 4;
+    unsigned char* b_hi = a_lo + M * K * 4;
+    unsigned char* b_lo = b_hi + N * K * 4;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int q = tid; q < M * K; q += 128) {
+        const int r = q / K, k = q % K;
+        const float x = A[q];
+        *reinterpret_cast<float*>(a_hi + tc::kmajor_off(r, k, M)) = x;
+        *reinterpret_cast<float*>(a_lo + tc::kmajor_off(r, k, M)) = tc::tf32_lo(x);
+    }
+    for (int q = tid; q < N * K; q += 128) {
+        const int k = q / N, n = q % N;
+        const float x = B[q];
+        *reinterpret_cast<float*>(b_hi + tc::kmajor_off(n, k, N)) = x;
+        *reinterpret_cast<float*>(b_lo + tc::kmajor_off(n, k, N)) = tc::tf32_lo(x);
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_proxy_async();
+    if (warp == 0) tc::tmem_alloc<256>(&s_tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    if (tid == 0) {
+        const uint32_t idesc = tc::idesc_tf32(M, N);
+        const uint32_t lbo_a = (M / 8) * 128, lbo_b = (N / 8) * 128;
+        for (int s = 0; s < K / 8; ++s) {
+            const uint32_t oa = s * 2 * lbo_a, ob = s * 2 * lbo_b;
+            const uint64_t ah = tc::make_desc(tc::smem_addr(a_hi) + oa, lbo_a, 128);
+            const uint64_t al = tc::make_desc(tc::smem_addr(a_lo) + oa, lbo_a, 128);
+            const uint64_t bh = tc::make_desc(tc::smem_addr(b_hi) + ob, lbo_b, 128);
+            const uint64_t bl = tc::make_desc(tc::smem_addr(b_lo) + ob, lbo_b, 128);
+            tc::mma_tf32(tmem, ah, bh, idesc, s > 0);
+            if (passes >= 3) {
+                tc::mma_tf32(tmem, ah, bl, idesc, true);
+                tc::mma_tf32(tmem, al, bh, idesc, true);
+            }
+        }
+        tc::mma_commit(&s_bar);
+    }
+    __syncwarp();
+    // wait for the MMAs
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(tc::smem_addr(&s_bar))
+            : "memory");
+    }
+    tc::fence_after_sync();
+    const int row = warp * 32 + lane;
+    for (int c = 0; c < N; c += 8) {
+        float v[8];
+        tc::tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) D[row * N + c + q] = v[q];
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<256>(tmem);
+}
+
+}  // namespace
+}  // namespace skan
+
+extern "C" skan_status skan_debug_gemm_tf32(const float* dA, const float* dB, float* dD, int N, int K, int passes,
+                                            void* stream) {
+    if (N < 8 || N > 256 || N % 16 || K < 8 || K > 64 || K % 8)
+        return skan::set_error(SKAN_SHAPE_ERROR, "debug gemm: N in [16,256] step 16, K in [8,64] step 8", 0,
+                               SKAN_FAULT_NONE);
+    const size_t smem = static_cast<size_t>(2 * 128 * K + 2 * N * K) * 4;
+    cudaFuncSetAttribute(skan::k_debug_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    skan::k_debug_gemm<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K, passes);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return skan::set_error(SKAN_CUDA_ERROR, cudaGetErrorString(e), 0, SKAN_FAULT_NONE);
+    return SKAN_OK;
+}
+
+// ===========================================================================
+// K4: a fast-path layer as a tensor-core GEMM, used at large batch.
+//
+// The reference's per-edge interpolation, bias included (lutham.cpp:810:
+// (g c0 + b)(1-t) + (g c1 + b) t), is a contraction over the knot basis:
+//     y[b][j] = sum_i sum_m  A[b][i*G+m] * W[i*G+m][j]
+//     A[b][i*G+m] = hat weight of knot m at x_bi: 1-t at the bracket, t at
+//                   the next knot, 0 elsewhere (kan.cpp:28-58 brackets)
+//     W[i*G+m][j] = g_ij * c_kij[m] + b_ij  (the reconstructed per-edge grid,
+//                   to_dense_network, lutham.cpp:304), or the dense grid
+// so a layer is Y[B x out] = A[B x in*G] * W[in*G x out].  Each CTA owns a
+// 128-sample x 128-output tile and a split of the inputs; per chunk of IC
+// inputs its 256 threads write A (from the brackets) and W (decoded from the
+// compressed records + codebook, or read from the dense grid) into shared
+// memory in the canonical K-major layout, split into tf32 hi/lo, and one
+// thread issues 3 x (IC*G/8) tcgen05.mma (3xTF32) into a TMEM accumulator;
+// the next chunk is generated while the tensor core runs (two stages,
+// mbarrier-tracked).  Split partials are reduced in fixed order (f64) by
+// k_split_reduce, which also locates the next layer's inputs.
+// ===========================================================================
+
+#include "skan_device.cuh"
+
+namespace skan {
+namespace {
+
+using namespace dev;
+
+constexpr int kGmM = 128;  // samples per tile (MMA M)
+constexpr int kGmN = 128;  // outputs per tile (MMA N, TMEM columns)
+constexpr int kGmT = 512;  // 4 knot groups x 128 output columns (W), 128 samples x 4 inputs (A)
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(tc::smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// Per-thread staging of one edge (i, j), loaded one chunk ahead: I8 the
+// 16-byte codebook row plus gain and bias already decoded; F32 the row
+// index, gain and bias; DENSE nothing (the grid is read when written).
+struct EdgeRaw {
+    uint4 row;
+    uint32_t k;
+    float g, b;
+};
+
+template <int FMT>
+__device__ __forceinline__ void edge_load(const DevLayer& L, const float* s_lut, size_t e, EdgeRaw& r) {
+    if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
+        uint32_t k, gc;
+        int bc;
+        if constexpr (FMT == FMT_I8_R32) {
+            const uint32_t rec = __ldg(L.rec + e);
+            k = rec & 0xFFFFu;
+            gc = (rec >> 16) & 0xFFu;
+            bc = static_cast<int8_t>(rec >> 24);
+        } else {
+            k = L.idx ? __ldg(L.idx + e) : 0u;
+            const uint32_t gb = __ldg(L.gb + e);
+            gc = gb & 0xFFu;
+            bc = static_cast<int8_t>(gb >> 8);
+        }
+        r.row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
+        r.g = s_lut[gc];  // float(gain(code) * codebook scale)
+        r.b = static_cast<float>(static_cast<double>(bc) * L.bs);
+    } else if constexpr (FMT == FMT_F32) {
+        r.k = L.idx ? __ldg(L.idx + e) : 0u;
+        r.g = __ldg(L.gain + e);
+        r.b = __ldg(L.bias + e);
+    }
+}
+
+// W value of a staged edge at knot m (fast-path decode); int8 codes become
+// floats through the 2^23 + (u ^ 0x80) bit pattern (no I2F).
+template <int FMT>
+__device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, size_t e, int m) {
+    if constexpr (FMT == FMT_DENSE) {
+        return __ldg(L.cb32 + e * static_cast<size_t>(L.G) + m);
+    } else if constexpr (FMT == FMT_F32) {
+        return fmaf(r.g, __ldg(L.cb32 + static_cast<size_t>(r.k) * L.G + m), r.b);
+    } else {
+        const uint32_t w = m < 4 ? r.row.x : (m < 8 ? r.row.y : (m < 12 ? r.row.z : r.row.w));
+        const float code = __int_as_float(static_cast<int>(((w >> (8 * (m & 3))) & 0xFFu) ^ 0x4B000080u)) - 8388736.0f;
+        return fmaf(r.g, code, r.b);
+    }
+}
+
+// Chunk K order: k = m * IC + il (knot-major), so the IC inputs of one
+// edge column at one knot are contiguous 4-float groups of the K-major
+// tile: W is written with 16-byte stores.  IC is 4 (G even) or 8 (G odd).
+// Thread t: W for output column t % 128 at knots t/128, t/128 + 4, ...;
+// A for sample t % 128 at input t / 128 (and + 4 when IC = 8).
+template <int FMT, int IC>
+__global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ uint32_t s_tmem;
+    __shared__ float s_lut[256];
+    const DevLayer& L = a.L;
+    const int G = L.G, KC = IC * G;
+    const uint32_t tile = kGmM * KC * 4;    // kGmM == kGmN: A and W tiles have one size
+    const uint32_t stage_bytes = 4 * tile;  // [A_hi][A_lo][W_hi][W_lo]
+    constexpr uint32_t kLbo = (kGmM / 8) * 128;
+    constexpr int kAU = IC * kGmM / kGmT;  // A slots per thread (1 or 2)
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * kGmM;
+    const int nS = min(kGmM, a.B - s0), nJ = min(kGmN, L.out - j0);
+    const int r0 = blockIdx.y * a.rows_per_cta, rend = min(L.in, r0 + a.rows_per_cta);
+    const int nchunks = rend > r0 ? (rend - r0 + IC - 1) / IC : 0;
+    pdl_trigger();
+    if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
+        if (tid < 256) s_lut[tid] = L.lutf[tid];
+    }
+    // the A tiles are sparse (2 of G weights per sample and input): zero both
+    // stages once, then write and clear only the nonzeros
+    for (uint32_t q = tid * 16; q < 2 * stage_bytes; q += kGmT * 16) {
+        const uint32_t st = q / stage_bytes, o = q % stage_bytes;
+        if (o < 2 * tile) *reinterpret_cast<uint4*>(smem + st * stage_bytes + o) = make_uint4(0, 0, 0, 0);
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tc::tmem_alloc<kGmN>(&s_tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    const uint32_t idesc = tc::idesc_tf32(kGmM, kGmN);
+
+    const int rl = tid & (kGmM - 1), grp = tid >> 7;  // grp in 0..3
+    const uint32_t rbase = tc::kmajor_off(rl, 0, kGmM);  // row part of the offset
+    EdgeRaw er[IC];
+    unsigned evalid = 0;
+    int bm[kAU];
+    float bt[kAU];
+    uint32_t aoff0[kAU], aoff1[kAU];  // nonzero A offsets written into stage 0 / 1 (cleared on reuse)
+#pragma unroll
+    for (int u = 0; u < kAU; ++u) aoff0[u] = aoff1[u] = 0xFFFFFFFFu;
+    auto load_chunk = [&](int c) {
+        const int ib = r0 + c * IC;
+        evalid = 0;
+#pragma unroll
+        for (int il = 0; il < IC; ++il) {
+            const int i = ib + il;
+            if (rl < nJ && i < rend) {
+                evalid |= 1u << il;
+                edge_load<FMT>(L, s_lut, static_cast<size_t>(i) * L.out + j0 + rl, er[il]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kAU; ++u) {
+            const int i = ib + grp + 4 * u;
+            bm[u] = -2;
+            bt[u] = 0.f;
+            if (rl < nS && i < rend) {
+                const size_t p = static_cast<size_t>(i) * a.B + s0 + rl;
+                bm[u] = a.bm_in[p];
+                bt[u] = a.bt_in[p];
+            }
+        }
+    };
+    pdl_wait();  // brackets come from the previous kernel
+    if (nchunks > 0) {
+        __syncthreads();  // s_lut visible to edge_load
+        load_chunk(0);
+    }
+#pragma unroll 1
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        unsigned char* st = smem + buf * stage_bytes;
+        if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);  // chunk c-2's MMAs released it
+        const int ib = r0 + c * IC;
+        // W: this thread's knots, the IC inputs' values as 16-byte groups
+#pragma unroll 1
+        for (int m = grp; m < G; m += 4) {
+#pragma unroll
+            for (int h = 0; h < IC / 4; ++h) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int il = 4 * h + q;
+                    v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], static_cast<size_t>(ib + il) * L.out + j0 + rl, m)
+                                              : 0.f;
+                }
+                const uint32_t o = (m * (IC / 4) + h) * kLbo + rbase;
+                *reinterpret_cast<float4*>(st + 2 * tile + o) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4*>(st + 3 * tile + o) =
+                    make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]), tc::tf32_lo(v[2]), tc::tf32_lo(v[3]));
+            }
+        }
+        // A: clear the two weights chunk c-2 left, write this chunk's
+#pragma unroll
+        for (int u = 0; u < kAU; ++u) {
+            const int il = grp + 4 * u;
+            uint32_t& ao = buf ? aoff1[u] : aoff0[u];
+            if (ao != 0xFFFFFFFFu) {
+                const uint32_t o0 = ao & 0xFFFFu, o1 = ao >> 16;
+                *reinterpret_cast<float*>(st + o0) = 0.f;
+                *reinterpret_cast<float*>(st + tile + o0) = 0.f;
+                *reinterpret_cast<float*>(st + o1) = 0.f;
+                *reinterpret_cast<float*>(st + tile + o1) = 0.f;
+                ao = 0xFFFFFFFFu;
+            }
+            if (bm[u] >= 0) {
+                const int k0 = bm[u] * IC + il, k1 = k0 + IC;
+                const uint32_t o0 = rbase + (k0 >> 2) * kLbo + (k0 & 3) * 4;
+                const uint32_t o1 = rbase + (k1 >> 2) * kLbo + (k1 & 3) * 4;
+                const float w0 = 1.f - bt[u], w1 = bt[u];
+                *reinterpret_cast<float*>(st + o0) = w0;
+                *reinterpret_cast<float*>(st + tile + o0) = tc::tf32_lo(w0);
+                *reinterpret_cast<float*>(st + o1) = w1;
+                *reinterpret_cast<float*>(st + tile + o1) = tc::tf32_lo(w1);
+                ao = o0 | (o1 << 16);
+            }
+        }
+        if (c + 1 < nchunks) load_chunk(c + 1);  // next chunk's tables fly while this one multiplies
+        tc::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after_sync();
+            const uint32_t base = tc::smem_addr(st);
+#pragma unroll 1
+            for (int s = 0; s < KC / 8; ++s) {
+                const uint32_t o = s * 2 * kLbo;
+                const uint64_t ah = tc::make_desc(base + o, kLbo, 128);
+                const uint64_t al = tc::make_desc(base + tile + o, kLbo, 128);
+                const uint64_t wh = tc::make_desc(base + 2 * tile + o, kLbo, 128);
+                const uint64_t wl = tc::make_desc(base + 3 * tile + o, kLbo, 128);
+                tc::mma_tf32(tmem, ah, wh, idesc, c > 0 || s > 0);
+                tc::mma_tf32(tmem, ah, wl, idesc, true);
+                tc::mma_tf32(tmem, al, wh, idesc, true);
+            }
+            tc::mma_commit(&s_bar[buf]);
+        }
+    }
+    if (nchunks > 0) mbar_wait_parity(&s_bar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+    tc::fence_after_sync();
+    // epilogue: warp w reads TMEM lanes (w%4)*32.. (its samples), columns (w/4)*32..+32
+    const int q4 = warp & 3, cq = warp >> 2;
+    const int row = q4 * 32 + lane;
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    float* dst = a.partial + blockIdx.y * plane + static_cast<size_t>(s0 + row) * L.out + j0;
+#pragma unroll 1
+    for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+        float v[8];
+        if (nchunks > 0) {
+            tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = 0.f;
+        }
+        if (row < nS) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (c8 + u < nJ) dst[c8 + u] = v[u];
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<kGmN>(tmem);
+}
+
+// Fixed-order (ascending split) f64 reduction of the split partials, one
+// thread per (sample, output); + bias sums when the layer's bias was not
+// folded into W; y; next layer's bracket (input-major).
+__global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
+    pdl_trigger();
+    pdl_wait();
+    const DevLayer& L = a.L;
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(p % L.out);
+        double v = 0.0;
+        for (int z = 0; z < nsplit; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+        if (add_bias && L.bias_sum) v += L.bias_sum[j];
+        a.y[p] = v;
+        if (a.has_next) {
+            int m;
+            float t;
+            fast_locate(a.N, v, a.err, m, t);
+            const size_t q = static_cast<size_t>(j) * a.B + p / L.out;
+            a.bm_out[q] = m;
+            a.bt_out[q] = t;
+        }
+    }
+}
+
+template <typename K, typename... Args>
+void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+}  // namespace
+
+// Inputs per chunk: IC*G must be a multiple of the tf32 MMA K (8), and IC
+// a multiple of 4 (16-byte W groups): 4 for even G, 8 for odd G.
+int gemm_ic(int G) { return G % 2 == 0 ? 4 : 8; }
+
+size_t gemm_smem(int G) {
+    const size_t kc = static_cast<size_t>(gemm_ic(G)) * G;
+    return 2 * (2 * kGmM * kc * 4 + 2 * kGmN * kc * 4);
+}
+
+bool gemm_supported(const DevLayer& L) {
+    const int ic = gemm_ic(L.G);
+    return ic > 0 && L.G <= 16 && gemm_smem(L.G) <= 200 * 1024 &&
+           (L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32 || L.fmt == FMT_DENSE);
+}
+
+LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
+    LaunchCfg c{};
+    c.kind = 4;
+    c.ic = gemm_ic(L.G);
+    c.jt = (L.out + kGmN - 1) / kGmN;
+    c.st = (B + kGmM - 1) / kGmM;
+    c.tj = kGmN;
+    const int sms = num_sms > 0 ? num_sms : 148;
+    // one CTA per SM: the fewest input splits whose waves are >= 90% full
+    const long long base = static_cast<long long>(c.jt) * c.st;
+    const long long maxns = std::max<long long>(1, std::min<long long>(64, (L.in + c.ic - 1) / c.ic));
+    long long ns = 1;
+    double best = 0.0;
+    for (long long k = 1; k <= maxns; ++k) {
+        const long long ctas = base * k, waves = (ctas + sms - 1) / sms;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * sms);
+        if (eff > best + 1e-9) {
+            best = eff;
+            ns = k;
+        }
+        if (eff >= 0.9) break;
+    }
+    const int chunks = (L.in + c.ic - 1) / c.ic;
+    const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
+    c.ichunk = per * c.ic;
+    c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
+    c.smem = gemm_smem(L.G);
+    return c;
+}
+
+void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    void (*k)(FwdArgs);
+    const bool i4 = c.ic == 4;
+    switch (a.L.fmt) {
+        case FMT_I8_R32: k = i4 ? k_layer_gemm<FMT_I8_R32, 4> : k_layer_gemm<FMT_I8_R32, 8>; break;
+        case FMT_I8_WIDE: k = i4 ? k_layer_gemm<FMT_I8_WIDE, 4> : k_layer_gemm<FMT_I8_WIDE, 8>; break;
+        case FMT_F32: k = i4 ? k_layer_gemm<FMT_F32, 4> : k_layer_gemm<FMT_F32, 8>; break;
+        default: k = i4 ? k_layer_gemm<FMT_DENSE, 4> : k_layer_gemm<FMT_DENSE, 8>; break;
+    }
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+    launch_pdl(k, dim3(c.jt, c.nsplit, c.st), dim3(kGmT), c.smem, pdl, s, a);
+    // bias: folded into W for compressed layers; dense layers have none
+    const long long n = static_cast<long long>(a.B) * a.L.out;
+    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+    launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+}
+
+}  // namespace skan

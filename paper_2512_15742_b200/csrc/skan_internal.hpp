@@ -91,7 +91,8 @@ struct LaunchCfg {
     int nsplit;  // i-splits (fast path); 1 in exact mode
     int ichunk;  // inputs per split
     int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes
-                 // (large batch), 2 = pair planes in shared memory (batch 1)
+                 // (large batch), 2 = pair planes in shared memory (batch 1), 4 = tensor-core
+                 // GEMM over the knot basis (large batch, wide layers; skan_gemm.cu)
     int vj;      // outputs per lane (small kernel)
     int rw;      // rows per warp (small kernel)
     int ic;      // inputs per staged chunk (large kernel)
@@ -182,6 +183,13 @@ void launch_pli_lookup(const double* cb, int k, int G, const int* rows, const do
                        int* err, cudaStream_t s);
 void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint32_t* out,
                            cudaStream_t s);
+
+// Tensor-core layer GEMM (skan_gemm.cu), kind 4 of LaunchCfg: two launches
+// (the GEMM over input splits, then the fixed-order split reduction).
+constexpr int kGemmMinBatch = 64;  // smallest batch routed to the tensor-core layer GEMM
+bool gemm_supported(const DevLayer& L);
+LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms);
+void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);
 
 // Record a thread-local error for skan_last_error and return its status.
 skan_status set_error(skan_status s, const std::string& msg, uint64_t offset, int fault);

@@ -1042,6 +1042,7 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         c.ichunk = L.in;
         return c;
     }
+    if (B >= kGemmMinBatch && L.out >= 64 && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {
         // samples in lanes: tile 128 samples x (32 or 64) outputs x split of the rows
@@ -1095,6 +1096,10 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
 }
 
 void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    if (c.kind == 4) {
+        launch_layer_gemm(a, c, pdl, s);
+        return;
+    }
     if (c.kind == 2) {
         void (*k)(FwdArgs);
         switch (c.vj) {
