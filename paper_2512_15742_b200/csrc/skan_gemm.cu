@@ -152,46 +152,36 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
 }
 
 // Per-thread staging of one edge (i, j), loaded one chunk ahead: I8 the
-// 16-byte codebook row plus gain and bias already decoded; F32 the row
-// index, gain and bias; DENSE nothing (the grid is read when written).
+// 16-byte codebook row plus gain and bias already decoded (the record that
+// names the row is loaded one chunk earlier still, so the row load never
+// waits on it); F32 the row index, gain and bias; DENSE the grid values at
+// the thread's knots.
 struct EdgeRaw {
     uint4 row;
     uint32_t k;
     float g, b;
+    float v[4];
 };
 
+// record word of an int8 edge: (row, gain code, bias code)
 template <int FMT>
-__device__ __forceinline__ void edge_load(const DevLayer& L, const float* s_lut, size_t e, EdgeRaw& r) {
-    if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
-        uint32_t k, gc;
-        int bc;
-        if constexpr (FMT == FMT_I8_R32) {
-            const uint32_t rec = __ldg(L.rec + e);
-            k = rec & 0xFFFFu;
-            gc = (rec >> 16) & 0xFFu;
-            bc = static_cast<int8_t>(rec >> 24);
-        } else {
-            k = L.idx ? __ldg(L.idx + e) : 0u;
-            const uint32_t gb = __ldg(L.gb + e);
-            gc = gb & 0xFFu;
-            bc = static_cast<int8_t>(gb >> 8);
-        }
-        r.row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
-        r.g = s_lut[gc];  // float(gain(code) * codebook scale)
-        r.b = static_cast<float>(static_cast<double>(bc) * L.bs);
-    } else if constexpr (FMT == FMT_F32) {
-        r.k = L.idx ? __ldg(L.idx + e) : 0u;
-        r.g = __ldg(L.gain + e);
-        r.b = __ldg(L.bias + e);
+__device__ __forceinline__ uint32_t rec_load(const DevLayer& L, size_t e, uint32_t& k) {
+    if constexpr (FMT == FMT_I8_R32) {
+        const uint32_t r = __ldg(L.rec + e);
+        k = r & 0xFFFFu;
+        return r >> 16;  // gain code | bias code << 8
+    } else {
+        k = L.idx ? __ldg(L.idx + e) : 0u;
+        return __ldg(L.gb + e);
     }
 }
 
-// W value of a staged edge at knot m (fast-path decode); int8 codes become
-// floats through the 2^23 + (u ^ 0x80) bit pattern (no I2F).
+// W value of a staged edge at its u-th knot m (fast-path decode); int8
+// codes become floats through the 2^23 + (u ^ 0x80) bit pattern (no I2F).
 template <int FMT>
-__device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, size_t e, int m) {
+__device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int m, int u) {
     if constexpr (FMT == FMT_DENSE) {
-        return __ldg(L.cb32 + e * static_cast<size_t>(L.G) + m);
+        return r.v[u];
     } else if constexpr (FMT == FMT_F32) {
         return fmaf(r.g, __ldg(L.cb32 + static_cast<size_t>(r.k) * L.G + m), r.b);
     } else {
@@ -248,21 +238,57 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     const int rl = tid & (kGmM - 1), grp = tid >> 7;  // grp in 0..3
     const uint32_t rbase = tc::kmajor_off(rl, 0, kGmM);  // row part of the offset
     EdgeRaw er[IC];
-    unsigned evalid = 0;
+    unsigned evalid = 0;   // edges of the staged chunk inside the layer
+    uint32_t recn[IC], kn[IC];  // I8: records of the chunk after the staged one
+    unsigned nvalid = 0;
     int bm[kAU];
     float bt[kAU];
     uint32_t aoff0[kAU], aoff1[kAU];  // nonzero A offsets written into stage 0 / 1 (cleared on reuse)
 #pragma unroll
     for (int u = 0; u < kAU; ++u) aoff0[u] = aoff1[u] = 0xFFFFFFFFu;
-    auto load_chunk = [&](int c) {
+    constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
+    auto load_recs = [&](int c) {  // I8 records of chunk c
         const int ib = r0 + c * IC;
-        evalid = 0;
+        nvalid = 0;
 #pragma unroll
         for (int il = 0; il < IC; ++il) {
             const int i = ib + il;
             if (rl < nJ && i < rend) {
+                nvalid |= 1u << il;
+                recn[il] = rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, kn[il]);
+            }
+        }
+    };
+    auto load_chunk = [&](int c) {  // stage chunk c's edge data and brackets into registers
+        const int ib = r0 + c * IC;
+        if constexpr (kI8) {
+            evalid = nvalid;
+#pragma unroll
+            for (int il = 0; il < IC; ++il) {
+                if (!(evalid >> il & 1)) continue;
+                er[il].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(kn[il]) * L.rs));
+                er[il].g = s_lut[recn[il] & 0xFFu];  // float(gain(code) * codebook scale)
+                er[il].b = static_cast<float>(static_cast<double>(static_cast<int8_t>(recn[il] >> 8)) * L.bs);
+            }
+        } else {
+            evalid = 0;
+#pragma unroll
+            for (int il = 0; il < IC; ++il) {
+                const int i = ib + il;
+                if (!(rl < nJ && i < rend)) continue;
                 evalid |= 1u << il;
-                edge_load<FMT>(L, s_lut, static_cast<size_t>(i) * L.out + j0 + rl, er[il]);
+                const size_t e = static_cast<size_t>(i) * L.out + j0 + rl;
+                if constexpr (FMT == FMT_F32) {
+                    er[il].k = L.idx ? __ldg(L.idx + e) : 0u;
+                    er[il].g = __ldg(L.gain + e);
+                    er[il].b = __ldg(L.bias + e);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int m = grp + 4 * u;
+                        er[il].v[u] = m < G ? __ldg(L.cb32 + e * static_cast<size_t>(G) + m) : 0.f;
+                    }
+                }
             }
         }
 #pragma unroll
@@ -276,10 +302,14 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                 bt[u] = a.bt_in[p];
             }
         }
+        if constexpr (kI8) {
+            if (c + 1 < nchunks) load_recs(c + 1);
+        }
     };
     pdl_wait();  // brackets come from the previous kernel
     if (nchunks > 0) {
-        __syncthreads();  // s_lut visible to edge_load
+        __syncthreads();  // s_lut visible
+        if constexpr (kI8) load_recs(0);
         load_chunk(0);
     }
 #pragma unroll 1
@@ -287,18 +317,18 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         const int buf = c & 1;
         unsigned char* st = smem + buf * stage_bytes;
         if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);  // chunk c-2's MMAs released it
-        const int ib = r0 + c * IC;
         // W: this thread's knots, the IC inputs' values as 16-byte groups
-#pragma unroll 1
-        for (int m = grp; m < G; m += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int m = grp + 4 * u;
+            if (m >= G) break;
 #pragma unroll
             for (int h = 0; h < IC / 4; ++h) {
                 float v[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int il = 4 * h + q;
-                    v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], static_cast<size_t>(ib + il) * L.out + j0 + rl, m)
-                                              : 0.f;
+                    v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], m, u) : 0.f;
                 }
                 const uint32_t o = (m * (IC / 4) + h) * kLbo + rbase;
                 *reinterpret_cast<float4*>(st + 2 * tile + o) = make_float4(v[0], v[1], v[2], v[3]);
@@ -390,7 +420,15 @@ __global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int j = static_cast<int>(p % L.out);
         double v = 0.0;
-        for (int z = 0; z < nsplit; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+        int z = 0;
+        for (; z + 4 <= nsplit; z += 4) {  // four loads in flight, summed in split order
+            float f[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) f[u] = __ldcg(a.partial + (z + u) * plane + p);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
+        }
+        for (; z < nsplit; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
         if (add_bias && L.bias_sum) v += L.bias_sum[j];
         a.y[p] = v;
         if (a.has_next) {
