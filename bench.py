@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--mode", choices=["fast", "exact"], default="fast")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1/cfg4/cfg5 side measurements")
     return ap.parse_args()
 
 
@@ -292,6 +293,65 @@ def main():
     ms256 = sync_max(statistics.mean(t256))
     edges = model.edge_count()
 
+    # ---- the other BASELINE.json configs on this GPU (side measurements) ---
+    def event_us(fn, reps):
+        """median CUDA-event time (us) of fn on `stream`, L2 flushed before each call"""
+        ev = []
+        with torch.cuda.stream(stream):
+            for r in range(reps + 3):
+                flush.zero_()
+                a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                fn()
+                b0.record(stream)
+                if r >= 3:
+                    ev.append((a0, b0))
+            stream.synchronize()
+        return statistics.median(x.elapsed_time(y) * 1e3 for x, y in ev)
+
+    extra = {}
+    if not args.no_extra and rank == 0:
+        # cfg1: single 256->256 layer, K=256, G=10, int8, batch 1
+        m1 = hq.build_model(synthetic.synthetic_head(dims=(256, 256), k=256, grid=G, int8=True, seed=1), device=local)
+        w1 = hq.make_workspace(m1, 1)
+        x1 = torch.from_numpy(synthetic.synthetic_inputs(1, 256, seed=1)).to(dev)
+        y1 = torch.zeros(256, dtype=torch.float64, device=dev)
+        us1 = event_us(lambda: _lib.check(L.skan_forward_async(m1.handle, w1.handle, x1.data_ptr(), 1, y1.data_ptr(),
+                                                               mode, s_ptr)), max(20, args.steps))
+        p1 = m1.plan()
+        extra["cfg1"] = {"workload": "single layer 256->256, K=256, G=10, int8, batch 1", "latency_us": us1,
+                         "samples_per_s": 1e6 / us1, "launches": w1.last_launches(),
+                         "achieved_gbs": (p1.payload_total + (256 + 256) * 8) / us1 / 1e3}
+        del m1, w1
+        # cfg5 per GPU: 32 heads over 8 GPUs = 4 cfg2 heads on one shared batch of 256
+        heads = [model] + [hq.build_model(synthetic.synthetic_head(dims=DIMS, k=K, grid=G, int8=True, seed=2026 + 7 * h),
+                                          device=local) for h in range(1, 4)]
+        hws = [ws] + [hq.make_workspace(h, 256) for h in heads[1:]]
+        ys5 = [torch.zeros(256 * DIMS[-1], dtype=torch.float64, device=dev) for _ in heads]
+        x5 = torch.from_numpy(synthetic.synthetic_inputs(256, DIMS[0], seed=777)).to(dev)
+        us5 = event_us(lambda: hq.forward_multi(heads, hws, x5, 256, ys5, mode=args.mode, stream=s_ptr), 5)
+        extra["cfg5"] = {"workload": "4 compressed cfg2 heads (the per-GPU share of 32 heads on 8 GPUs), one shared "
+                                     "feature batch of 256", "us_per_step": us5,
+                         "head_samples_per_s": 4 * 256 / us5 * 1e6}
+        del heads[1:], hws[1:]
+        # cfg4: uncompressed dense-spline head, f32 grids, batch 64 (the DRAM-bound comparison path)
+        dl = synthetic.dense_runtime_head()
+        dm = hq.upload(dl, device=local)
+        del dl
+        dws = hq.make_workspace(dm, 64)
+        x4 = torch.from_numpy(synthetic.synthetic_inputs(64, DIMS[0], seed=6)).to(dev)
+        y4 = torch.zeros(64 * DIMS[-1], dtype=torch.float64, device=dev)
+        us4 = event_us(lambda: _lib.check(L.skan_forward_async(dm.handle, dws.handle, x4.data_ptr(), 64, y4.data_ptr(),
+                                                               mode, s_ptr)), 5)
+        p4 = dm.plan()
+        b4 = p4.payload_total + 64 * (DIMS[0] + DIMS[-1]) * 8
+        extra["cfg4"] = {"workload": "dense {2048,13664,20} f32 grids (1,130,286,080 B), batch 64", "us_per_step": us4,
+                         "samples_per_s": 64 / us4 * 1e6, "launches": dws.last_launches(),
+                         "roofline": {"bound": "hbm", "achieved": b4 / us4 / 1e3, "peak": pk.get("hbm_gbs"),
+                                      "unit": "GB/s", "frac": b4 / us4 / 1e3 / pk.get("hbm_gbs", 6537.0),
+                                      "algorithmic_bytes": b4}}
+        del dm, dws
+
     # ---- e2e through the public API with host buffers ---------------------
     x_host = torch.from_numpy(x_np.copy()).pin_memory()
     y_host = torch.zeros(B * DIMS[-1], dtype=torch.float64).pin_memory()
@@ -349,6 +409,7 @@ def main():
                     "h2d_bytes_per_step": int(xh.nbytes), "d2h_bytes_per_step": int(yh.nbytes),
                     "ms_per_step": e2e_s * 1e3, "path": "skan_forward(SKAN_PTR_HOST) from pinned host memory"},
             "clocks": clk.summary(),
+            "configs": extra,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu

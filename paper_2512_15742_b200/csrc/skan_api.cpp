@@ -569,7 +569,10 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
         for (int i = 0; i < L0.G && i < 33; ++i)  // node_position, kan.cpp:21-26
             h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
         h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->num_sms);
-        if (h->b1_grid > 0) {
+        // the persistent kernel pays for its cooperative launch and grid
+        // barriers only on heads whose first layer is wide enough for the
+        // pair-plane scheme; small heads take the multi-kernel path
+        if (h->b1_grid > 0 && h->b1_plan.planes0) {
             h->b1_ok = true;
         }
     }
