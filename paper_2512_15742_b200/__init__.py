@@ -5,9 +5,10 @@ path behind the reference's own operator API (see lutham.py, include/skan.h).
 """
 from .errors import (ContractError, CudaError, FormatError, FormatFault, HoloquantError, PlanError,
                      ShapeError, ValueError)
-from .lutham import (MODE_EXACT, MODE_FAST, Codebook, CompressedLayer, CompressedNetwork, Int8Tables,
+from .lutham import (MODE_EXACT, MODE_FAST, BenchConfig, BenchRow, Codebook, CompressedLayer, CompressedNetwork, Int8Tables,
                      KanLayer, KanNetwork, LayerHeader, LayerPlan, MemoryPlan, Model, ModelHeader,
-                     RuntimeLayer, Workspace, build_dense_model, build_model, compressed_forward,
+                     RuntimeLayer, Workspace, bench_csv, bench_iso_latency, bench_model, build_dense_model,
+                     build_model, compressed_forward,
                      deserialize, forward_async, forward_multi, index_bits, kFlagInt8, load_model,
                      locate, make_workspace, pli_lookup, plan_memory, unpack_indices, upload)
 

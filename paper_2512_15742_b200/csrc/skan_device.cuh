@@ -149,24 +149,18 @@ __device__ __forceinline__ bool locate_easy(double lo, double hi, int G, double 
 // false when undecided (near a knot, at the domain ends, non-finite):
 // callers fall back to the exact fp64 path.
 __device__ __forceinline__ bool bracket_f32(const DevLayer& L, double x, int& m) {
-    if (!finite_bits(x) || !(L.qf_eps >= 0.f)) return false;
+    // branch-free (callers unroll several inputs for ILP)
     const float xf = __double2float_rn(x);
-    if (xf < L.lo_f) {
-        m = 0;
-        return true;
-    }
-    if (xf > L.hi_f) {
-        m = L.G - 2;
-        return true;
-    }
+    const bool below = xf < L.lo_f, above = xf > L.hi_f;
     const float q = (xf - L.lo_f) * L.inv_dx_f;
     const float r = q + 12582912.0f;  // 1.5 * 2^23: rounds q to the nearest integer
     const int n = __float_as_int(r) - 0x4B400000;
     const float fr = q - (r - 12582912.0f);  // exact, in [-0.5, 0.5]
     const int i = fr < 0.f ? n - 1 : n;
     const float f = fr < 0.f ? fr + 1.f : fr;
-    m = i;
-    return i >= 0 && i <= L.G - 2 && f > L.qf_eps && f < 1.f - L.qf_eps;
+    const bool inside = i >= 0 && i <= L.G - 2 && f > L.qf_eps && f < 1.f - L.qf_eps;
+    m = below ? 0 : (above ? L.G - 2 : i);
+    return finite_bits(x) && L.qf_eps >= 0.f && (below || above || inside);
 }
 
 __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* err, int& m, float& t) {

@@ -157,10 +157,10 @@ __device__ void rowsplit_layer(const DevLayer& L, int r0, int r1, const int* s_m
     }
 }
 
-// floor(a / b) for 0 <= a < 2^24, b >= 1: correctly rounded fp32 quotient,
-// one integer fix-up each way (no 32-bit integer division sequence)
+// floor(a / b) for 0 <= a < 2^24, 1 <= b < 2^24: fp32 reciprocal estimate
+// (off by at most one), one integer fix-up each way (no division sequence)
 __device__ __forceinline__ int idiv_small(int a, int b) {
-    int q = static_cast<int>(__fdiv_rn(static_cast<float>(a), static_cast<float>(b)));
+    int q = static_cast<int>(static_cast<float>(a) * __frcp_rn(static_cast<float>(b)));
     if ((q + 1) * b <= a) ++q;
     if (q * b > a) --q;
     return q;
@@ -287,9 +287,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
             s_hi = hi;
             const int rec_rows = min(min(hi - lo, kMaxRows), h.rec_cap);
             mbar_expect_tx(bar, plane_bytes + static_cast<uint32_t>(rec_rows) * row_bytes);
-            const char* src = reinterpret_cast<const char*>(L.pair8 + static_cast<size_t>(lane) * L.K);
-            for (uint32_t off = 0; off < plane_bytes; off += 32768u)
-                bulk_g2s(smem + off, src + off, min(32768u, plane_bytes - off), bar);
+            bulk_g2s(smem, L.pair8 + static_cast<size_t>(lane) * L.K, plane_bytes, bar);  // the whole plane
         }
         if (__ballot_sync(0xFFFFFFFFu, mine) == 0 && lane == 0) {  // spare CTA: no rows
             s_bucket = GP;

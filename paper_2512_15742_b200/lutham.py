@@ -515,3 +515,111 @@ def unpack_indices(d_bytes, count: int, bits: int):
     _lib.check(_lib.lib().skan_unpack_indices(d_bytes.data_ptr(), d_bytes.numel(), int(count), int(bits),
                                               out.data_ptr(), s))
     return out[:count]
+
+
+# ---------------------------------------------------------------------------
+# benchmarking (lutham.hpp:160-183, lutham.cpp:852-951) on the device
+
+class _MT19937_64:
+    """std::mt19937_64 (the reference's bench input generator, lutham.cpp:875)."""
+
+    def __init__(self, seed: int):
+        self.mt = [0] * 312
+        self.mt[0] = seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & 0xFFFFFFFFFFFFFFFF
+        self.i = 312
+
+    def _twist(self):
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.i = 0
+
+    def __call__(self) -> int:
+        if self.i >= 312:
+            self._twist()
+        y = self.mt[self.i]
+        self.i += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEDA60000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & 0xFFFFFFFFFFFFFFFF
+
+
+@dataclass
+class BenchConfig:
+    """lutham.hpp:160-165."""
+    batch: int = 64
+    repeats: int = 101
+    warmup: int = 10
+    seed: int = 12345
+
+
+@dataclass
+class BenchRow:
+    """lutham.hpp:167-172 (microseconds per sample)."""
+    grid_size: int = 0
+    median_us: float = 0.0
+    p25_us: float = 0.0
+    p75_us: float = 0.0
+
+
+def _percentile(sorted_v, q: float) -> float:
+    """lutham.cpp:857-861: nearest-rank on the sorted samples."""
+    n = len(sorted_v)
+    return sorted_v[int(round(q * (n - 1)))]
+
+
+def bench_model(model: Model, config: BenchConfig = BenchConfig(), mode="fast") -> BenchRow:
+    """bench_model (lutham.cpp:866-902) on the device: the same inputs
+    (U(lo, hi) of the first layer's domain from mt19937_64(seed)), warmup,
+    repeats of the synchronous host-buffer compressed_forward timed with a
+    steady clock, microseconds per sample, median / p25 / p75."""
+    import time
+    if config.batch < 1 or config.repeats < 1 or config.warmup < 0:
+        raise ShapeError("bench needs batch >= 1, repeats >= 1, warmup >= 0")
+    lo, hi = model.layers[0].domain_lo, model.layers[0].domain_hi
+    rng = _MT19937_64(config.seed)
+    n = config.batch * model.input_dim()
+    x = np.array([lo + (rng() >> 11) * 2.0 ** -53 * (hi - lo) for _ in range(n)], dtype=np.float64)
+    y = np.zeros(config.batch * model.output_dim())
+    ws = make_workspace(model, max_batch=config.batch)
+    for _ in range(config.warmup):
+        compressed_forward(model, x, config.batch, y, ws, mode=mode)
+    samples = []
+    for _ in range(config.repeats):
+        t0 = time.perf_counter()
+        compressed_forward(model, x, config.batch, y, ws, mode=mode)
+        samples.append((time.perf_counter() - t0) * 1e6 / config.batch)
+    samples.sort()
+    return BenchRow(model.layers[0].grid_size, _percentile(samples, 0.5), _percentile(samples, 0.25),
+                    _percentile(samples, 0.75))
+
+
+def bench_iso_latency(models: Sequence[Model], config: BenchConfig = BenchConfig(), mode="fast") -> List[BenchRow]:
+    """bench_iso_latency (lutham.cpp:904-926): models identical apart from G."""
+    if not models:
+        raise ShapeError("bench needs at least one model")
+    ref = models[0].layers
+    for m in models:
+        if len(m.layers) != len(ref):
+            raise ShapeError("bench models must share topology apart from grid size")
+        for a, b in zip(m.layers, ref):
+            if (a.in_dim, a.out_dim, a.k, a.flags, a.domain_lo, a.domain_hi) != (
+                    b.in_dim, b.out_dim, b.k, b.flags, b.domain_lo, b.domain_hi):
+                raise ShapeError("bench models must share topology apart from grid size")
+    return [bench_model(m, config, mode) for m in models]
+
+
+def bench_csv(rows: Sequence[BenchRow]) -> str:
+    """bench_csv (lutham.cpp:938-951): the same header and %.17g fields."""
+    out = "G,median_us,p25_us,p75_us\n"
+    for r in rows:
+        out += f"{r.grid_size},{r.median_us:.17g},{r.p25_us:.17g},{r.p75_us:.17g}\n"
+    return out
