@@ -383,10 +383,7 @@ __device__ void planes_layer0(const HeadB1Args& h, unsigned char* smem, uint64_t
 
 __global__ void __launch_bounds__(kT, 1) k_head_b1(const __grid_constant__ HeadB1Args hp) {
     extern __shared__ __align__(128) unsigned char smem[];
-    // The parameter block is read from shared memory after the first
-    // barrier: one parallel copy instead of a constant-cache miss on every
-    // field a phase touches for the first time.
-    __shared__ __align__(16) HeadB1Args h;
+    const HeadB1Args& h = hp;  // parameters straight from the constant bank
     // bias sums: layer 0's of this CTA's layer-1 rows, later the last layer's
     __shared__ double s_bias[kT];
     __shared__ __align__(8) uint64_t s_bar[3];  // [0] layer-0 plane+records, [1] row-split prefetch, [2] x
@@ -440,12 +437,6 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(const __grid_constant__ HeadB
             prefetch_l2_slice(L.pair8, static_cast<size_t>(L.K) * (L.G - 1) * 2, c, P);
         else
             prefetch_l2_slice(L.rec, static_cast<size_t>(L.in) * L.out * 4, c, P);
-    }
-    {  // parameter block -> shared memory
-        const int n = static_cast<int>(sizeof(HeadB1Args) / 4);
-        const int* src = reinterpret_cast<const int*>(&hp);
-        int* dst = reinterpret_cast<int*>(&h);
-        for (int q = threadIdx.x; q < n; q += kT) dst[q] = src[q];
     }
     // bias sums needed late (layer-1 row reduction, final reduction) are
     // loaded into registers now; the loads complete off the critical path
