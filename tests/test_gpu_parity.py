@@ -396,3 +396,32 @@ def test_unpack_indices_bitexact(torch_cuda):
     # KAT test_lutham.cpp:39-40
     got = hq.unpack_indices(torch.tensor([0xff, 0x03, 0x10, 0x20], dtype=torch.uint8, device="cuda"), 3, 10)
     assert got.cpu().tolist() == [1023, 0, 513]
+
+
+# ---------------------------------------------------------------------------
+# tensor-core layer GEMM (skan_gemm.cu): every table format, even and odd G,
+# batches that fill and do not fill a 128-sample tile
+
+@pytest.mark.parametrize("batch", [64, 200])
+def test_fast_mode_tensor_core_gemm_formats(torch_cuda, batch):
+    rng = np.random.default_rng(300 + batch)
+    cases = [
+        ("int8 u16 G=10", oracle.ref_build(synthetic.CompressedNetwork(
+            [synthetic.crafted_layer(96, 150, 10, 300, 1, int8=True)])).tables()),
+        ("int8 u32 K>65536 G=6", oracle.ref_build(synthetic.CompressedNetwork(
+            [synthetic.crafted_layer(20, 70, 6, 70000, 2, int8=True)])).tables()),
+        ("f32 G=5 (odd: 8 inputs per chunk)", oracle.ref_build(synthetic.CompressedNetwork(
+            [synthetic.crafted_layer(33, 40, 5, 50, 3, int8=False)])).tables()),
+        ("dense G=12", oracle.ref_random([24, 130, 17], 12, 0.4, 4, 0, False).tables()),
+        ("int8 two layers", [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(
+            synthetic.synthetic_head(dims=(128, 96, 24), k=512, grid=10, int8=True, seed=5))]),
+    ]
+    for name, tables in cases:
+        x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+        want, _ = oracle.port_forward(tables, x, batch)
+        model = _upload(tables)
+        got, ws = _gpu_forward(model, x, batch, "fast", max_batch=256)
+        assert ws.last_launches() >= 2, name
+        assert_close(got, want, l1_scale(tables, x, batch))
+        again, _ = _gpu_forward(model, x, batch, "fast", max_batch=256)
+        assert np.array_equal(_bits(got), _bits(again)), name  # fixed-order split reduction

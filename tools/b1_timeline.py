@@ -77,6 +77,8 @@ def main():
             d = np.diff(cs[:, used], axis=1)
             print("   clock64 deltas between fine stamps (cycles, median over CTAs):",
                   {f"{a}->{b}": int(np.median(d[:, q])) for q, (a, b) in enumerate(zip(used[:-1], used[1:]))})
+            print("   clock64 of each fine stamp after slot", used[0], "(cycles, median over CTAs):",
+                  {k: int(np.median(cs[:, k] - cs[:, used[0]])) for k in used[1:]})
 
 
 if __name__ == "__main__":
