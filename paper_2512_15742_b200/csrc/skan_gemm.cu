@@ -163,16 +163,16 @@ struct EdgeRaw {
     float v[4];
 };
 
-// record word of an int8 edge: (row, gain code, bias code)
+// record word of an int8 edge: (row, gain code, bias code); WIDE also the
+// u32 row index.  Only the loads are issued here: nothing consumes them
+// until the next chunk.
 template <int FMT>
-__device__ __forceinline__ uint32_t rec_load(const DevLayer& L, size_t e, uint32_t& k) {
+__device__ __forceinline__ void rec_load(const DevLayer& L, size_t e, uint32_t& rec, uint32_t& k) {
     if constexpr (FMT == FMT_I8_R32) {
-        const uint32_t r = __ldg(L.rec + e);
-        k = r & 0xFFFFu;
-        return r >> 16;  // gain code | bias code << 8
+        rec = __ldg(L.rec + e);
     } else {
         k = L.idx ? __ldg(L.idx + e) : 0u;
-        return __ldg(L.gb + e);
+        rec = __ldg(L.gb + e);
     }
 }
 
@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll
     for (int u = 0; u < kAU; ++u) aoff0[u] = aoff1[u] = 0xFFFFFFFFu;
     constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
+    const float bs_f = static_cast<float>(L.bs);
     auto load_recs = [&](int c) {  // I8 records of chunk c
         const int ib = r0 + c * IC;
         nvalid = 0;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             const int i = ib + il;
             if (rl < nJ && i < rend) {
                 nvalid |= 1u << il;
-                recn[il] = rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, kn[il]);
+                rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, recn[il], kn[il]);
             }
         }
     };
@@ -266,9 +267,12 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll
             for (int il = 0; il < IC; ++il) {
                 if (!(evalid >> il & 1)) continue;
-                er[il].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(kn[il]) * L.rs));
-                er[il].g = s_lut[recn[il] & 0xFFu];  // float(gain(code) * codebook scale)
-                er[il].b = static_cast<float>(static_cast<double>(static_cast<int8_t>(recn[il] >> 8)) * L.bs);
+                const uint32_t r = recn[il];
+                const uint32_t k = FMT == FMT_I8_R32 ? (r & 0xFFFFu) : kn[il];
+                const uint32_t gb = FMT == FMT_I8_R32 ? (r >> 16) : r;  // gain code | bias code << 8
+                er[il].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
+                er[il].g = s_lut[gb & 0xFFu];  // float(gain(code) * codebook scale)
+                er[il].b = static_cast<float>(static_cast<int8_t>((gb >> 8) & 0xFFu)) * bs_f;
             }
         } else {
             evalid = 0;
@@ -398,9 +402,14 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             for (int u = 0; u < 8; ++u) v[u] = 0.f;
         }
         if (row < nS) {
+            if (c8 + 8 <= nJ && (L.out & 3) == 0) {
+                *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
+                *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (c8 + u < nJ) dst[c8 + u] = v[u];
+                for (int u = 0; u < 8; ++u)
+                    if (c8 + u < nJ) dst[c8 + u] = v[u];
+            }
         }
     }
     tc::fence_before_sync();
