@@ -417,17 +417,30 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     if (warp == 0) tc::tmem_free<kGmN>(tmem);
 }
 
+__device__ __forceinline__ void reduce_finish(const FwdArgs& a, size_t p, double v, int add_bias) {
+    const DevLayer& L = a.L;
+    const int j = static_cast<int>(p % L.out);
+    if (add_bias && L.bias_sum) v += L.bias_sum[j];
+    a.y[p] = v;
+    if (a.has_next) {
+        int m;
+        float t;
+        fast_locate(a.N, v, a.err, m, t);
+        const size_t q = static_cast<size_t>(j) * a.B + p / L.out;
+        a.bm_out[q] = m;
+        a.bt_out[q] = t;
+    }
+}
+
 // Fixed-order (ascending split) f64 reduction of the split partials, one
 // thread per (sample, output); + bias sums when the layer's bias was not
 // folded into W; y; next layer's bracket (input-major).
 __global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
     pdl_trigger();
     pdl_wait();
-    const DevLayer& L = a.L;
-    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    const size_t plane = static_cast<size_t>(a.B) * a.L.out;
     for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(p % L.out);
         double v = 0.0;
         int z = 0;
         for (; z + 4 <= nsplit; z += 4) {  // four loads in flight, summed in split order
@@ -438,16 +451,24 @@ __global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
             for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
         }
         for (; z < nsplit; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
-        if (add_bias && L.bias_sum) v += L.bias_sum[j];
-        a.y[p] = v;
-        if (a.has_next) {
-            int m;
-            float t;
-            fast_locate(a.N, v, a.err, m, t);
-            const size_t q = static_cast<size_t>(j) * a.B + p / L.out;
-            a.bm_out[q] = m;
-            a.bt_out[q] = t;
-        }
+        reduce_finish(a, p, v, add_bias);
+    }
+}
+
+// Many splits, few entries (narrow layers): one warp per entry, lane l sums
+// splits l, l+32, ... in order, then a fixed butterfly.
+__global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t plane = static_cast<size_t>(a.B) * a.L.out;
+    const int lane = threadIdx.x & 31;
+    for (size_t p = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / 32; p < plane;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
+        double v = 0.0;
+        for (int z = lane; z < nsplit; z += 32) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) reduce_finish(a, p, v, add_bias);
     }
 }
 
@@ -526,8 +547,13 @@ void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStrea
     launch_pdl(k, dim3(c.jt, c.nsplit, c.st), dim3(kGmT), c.smem, pdl, s, a);
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
-    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
-    launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+    if (c.nsplit >= 16 && n < 148LL * 256) {
+        const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
+        launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+    } else {
+        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+        launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+    }
 }
 
 }  // namespace skan
