@@ -138,7 +138,8 @@ using namespace dev;
 
 constexpr int kGmM = 128;  // samples per tile (MMA M)
 constexpr int kGmN = 128;  // outputs per tile (MMA N, TMEM columns)
-constexpr int kGmT = 512;  // 4 knot groups x 128 output columns (W), 128 samples x 4 inputs (A)
+constexpr int kGmP = 512;        // producers: 4 knot groups x 128 output columns (W), 128 samples x 4 inputs (A)
+constexpr int kGmT = kGmP + 32;  // + one warp that issues the tensor-core MMAs
 
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
     uint32_t done = 0;
@@ -199,7 +200,8 @@ __device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int
 template <int FMT, int IC>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t s_bar[2];   // stage free: committed by the MMA warp
+    __shared__ __align__(8) uint64_t s_full[2];  // stage written: every producer arrives
     __shared__ uint32_t s_tmem;
     __shared__ float s_lut[256];
     const DevLayer& L = a.L;
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     const uint32_t tile = kGmM * KC * 4;    // kGmM == kGmN: A and W tiles have one size
     const uint32_t stage_bytes = 4 * tile;  // [A_hi][A_lo][W_hi][W_lo]
     constexpr uint32_t kLbo = (kGmM / 8) * 128;
-    constexpr int kAU = IC * kGmM / kGmT;  // A slots per thread (1 or 2)
+    constexpr int kAU = IC * kGmM / kGmP;  // A slots per producer (1 or 2)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * kGmM;
     const int nS = min(kGmM, a.B - s0), nJ = min(kGmN, L.out - j0);
@@ -226,6 +228,8 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[0])), "r"(kGmP));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[1])), "r"(kGmP));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tc::tmem_alloc<kGmN>(&s_tmem);
@@ -311,84 +315,96 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         }
     };
     pdl_wait();  // brackets come from the previous kernel
-    if (nchunks > 0) {
-        __syncthreads();  // s_lut visible
-        if constexpr (kI8) load_recs(0);
-        load_chunk(0);
-    }
+    __syncthreads();  // s_lut visible
+    if (tid < kGmP) {
+        // producers: write stage c as soon as the MMAs of chunk c-2 released it
+        if (nchunks > 0) {
+            if constexpr (kI8) load_recs(0);
+            load_chunk(0);
+        }
 #pragma unroll 1
-    for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        unsigned char* st = smem + buf * stage_bytes;
-        if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);  // chunk c-2's MMAs released it
-        // W: this thread's knots, the IC inputs' values as 16-byte groups
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            unsigned char* st = smem + buf * stage_bytes;
+            if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);
+            // W: this thread's knots, the IC inputs' values as 16-byte groups
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int m = grp + 4 * u;
-            if (m >= G) break;
+            for (int u = 0; u < 4; ++u) {
+                const int m = grp + 4 * u;
+                if (m >= G) break;
 #pragma unroll
-            for (int h = 0; h < IC / 4; ++h) {
-                float v[4];
+                for (int h = 0; h < IC / 4; ++h) {
+                    float v[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int il = 4 * h + q;
-                    v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], m, u) : 0.f;
+                    for (int q = 0; q < 4; ++q) {
+                        const int il = 4 * h + q;
+                        v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], m, u) : 0.f;
+                    }
+                    const uint32_t o = (m * (IC / 4) + h) * kLbo + rbase;
+                    *reinterpret_cast<float4*>(st + 2 * tile + o) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4*>(st + 3 * tile + o) =
+                        make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]), tc::tf32_lo(v[2]), tc::tf32_lo(v[3]));
                 }
-                const uint32_t o = (m * (IC / 4) + h) * kLbo + rbase;
-                *reinterpret_cast<float4*>(st + 2 * tile + o) = make_float4(v[0], v[1], v[2], v[3]);
-                *reinterpret_cast<float4*>(st + 3 * tile + o) =
-                    make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]), tc::tf32_lo(v[2]), tc::tf32_lo(v[3]));
             }
-        }
-        // A: clear the two weights chunk c-2 left, write this chunk's
+            // A: clear the two weights chunk c-2 left, write this chunk's
 #pragma unroll
-        for (int u = 0; u < kAU; ++u) {
-            const int il = grp + 4 * u;
-            uint32_t& ao = buf ? aoff1[u] : aoff0[u];
-            if (ao != 0xFFFFFFFFu) {
-                const uint32_t o0 = ao & 0xFFFFu, o1 = ao >> 16;
-                *reinterpret_cast<float*>(st + o0) = 0.f;
-                *reinterpret_cast<float*>(st + tile + o0) = 0.f;
-                *reinterpret_cast<float*>(st + o1) = 0.f;
-                *reinterpret_cast<float*>(st + tile + o1) = 0.f;
-                ao = 0xFFFFFFFFu;
+            for (int u = 0; u < kAU; ++u) {
+                const int il = grp + 4 * u;
+                uint32_t& ao = buf ? aoff1[u] : aoff0[u];
+                if (ao != 0xFFFFFFFFu) {
+                    const uint32_t o0 = ao & 0xFFFFu, o1 = ao >> 16;
+                    *reinterpret_cast<float*>(st + o0) = 0.f;
+                    *reinterpret_cast<float*>(st + tile + o0) = 0.f;
+                    *reinterpret_cast<float*>(st + o1) = 0.f;
+                    *reinterpret_cast<float*>(st + tile + o1) = 0.f;
+                    ao = 0xFFFFFFFFu;
+                }
+                if (bm[u] >= 0) {
+                    const int k0 = bm[u] * IC + il, k1 = k0 + IC;
+                    const uint32_t o0 = rbase + (k0 >> 2) * kLbo + (k0 & 3) * 4;
+                    const uint32_t o1 = rbase + (k1 >> 2) * kLbo + (k1 & 3) * 4;
+                    const float w0 = 1.f - bt[u], w1 = bt[u];
+                    *reinterpret_cast<float*>(st + o0) = w0;
+                    *reinterpret_cast<float*>(st + tile + o0) = tc::tf32_lo(w0);
+                    *reinterpret_cast<float*>(st + o1) = w1;
+                    *reinterpret_cast<float*>(st + tile + o1) = tc::tf32_lo(w1);
+                    ao = o0 | (o1 << 16);
+                }
             }
-            if (bm[u] >= 0) {
-                const int k0 = bm[u] * IC + il, k1 = k0 + IC;
-                const uint32_t o0 = rbase + (k0 >> 2) * kLbo + (k0 & 3) * 4;
-                const uint32_t o1 = rbase + (k1 >> 2) * kLbo + (k1 & 3) * 4;
-                const float w0 = 1.f - bt[u], w1 = bt[u];
-                *reinterpret_cast<float*>(st + o0) = w0;
-                *reinterpret_cast<float*>(st + tile + o0) = tc::tf32_lo(w0);
-                *reinterpret_cast<float*>(st + o1) = w1;
-                *reinterpret_cast<float*>(st + tile + o1) = tc::tf32_lo(w1);
-                ao = o0 | (o1 << 16);
-            }
+            if (c + 1 < nchunks) load_chunk(c + 1);  // next chunk's tables fly while this one multiplies
+            tc::fence_proxy_async();                 // this thread's stage writes -> the tensor core
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[buf])) : "memory");
         }
-        if (c + 1 < nchunks) load_chunk(c + 1);  // next chunk's tables fly while this one multiplies
-        tc::fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
-            tc::fence_after_sync();
-            const uint32_t base = tc::smem_addr(st);
+    } else {
+        // the MMA warp: one lane issues 3 x (KC/8) tcgen05.mma per chunk, in order
 #pragma unroll 1
-            for (int s = 0; s < KC / 8; ++s) {
-                const uint32_t o = s * 2 * kLbo;
-                const uint64_t ah = tc::make_desc(base + o, kLbo, 128);
-                const uint64_t al = tc::make_desc(base + tile + o, kLbo, 128);
-                const uint64_t wh = tc::make_desc(base + 2 * tile + o, kLbo, 128);
-                const uint64_t wl = tc::make_desc(base + 3 * tile + o, kLbo, 128);
-                tc::mma_tf32(tmem, ah, wh, idesc, c > 0 || s > 0);
-                tc::mma_tf32(tmem, ah, wl, idesc, true);
-                tc::mma_tf32(tmem, al, wh, idesc, true);
+        for (int c = 0; c < nchunks; ++c) {
+            const int buf = c & 1;
+            mbar_wait_parity(&s_full[buf], (c >> 1) & 1);
+            if (lane == 0) {
+                tc::fence_after_sync();
+                const uint32_t base = tc::smem_addr(smem + buf * stage_bytes);
+#pragma unroll 1
+                for (int s = 0; s < KC / 8; ++s) {
+                    const uint32_t o = s * 2 * kLbo;
+                    const uint64_t ah = tc::make_desc(base + o, kLbo, 128);
+                    const uint64_t al = tc::make_desc(base + tile + o, kLbo, 128);
+                    const uint64_t wh = tc::make_desc(base + 2 * tile + o, kLbo, 128);
+                    const uint64_t wl = tc::make_desc(base + 3 * tile + o, kLbo, 128);
+                    tc::mma_tf32(tmem, ah, wh, idesc, c > 0 || s > 0);
+                    tc::mma_tf32(tmem, ah, wl, idesc, true);
+                    tc::mma_tf32(tmem, al, wh, idesc, true);
+                }
+                tc::mma_commit(&s_bar[buf]);
             }
-            tc::mma_commit(&s_bar[buf]);
+            __syncwarp();
         }
     }
     if (nchunks > 0) mbar_wait_parity(&s_bar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
     tc::fence_after_sync();
-    // epilogue: warp w reads TMEM lanes (w%4)*32.. (its samples), columns (w/4)*32..+32
+    // epilogue: producer warp w reads TMEM lanes (w%4)*32.. (its samples), columns (w/4)*32..+32
     const int q4 = warp & 3, cq = warp >> 2;
+    if (warp < kGmP / 32) {
     const int row = q4 * 32 + lane;
     const size_t plane = static_cast<size_t>(a.B) * L.out;
     float* dst = a.partial + blockIdx.y * plane + static_cast<size_t>(s0 + row) * L.out + j0;
@@ -411,6 +427,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                     if (c8 + u < nJ) dst[c8 + u] = v[u];
             }
         }
+    }
     }
     tc::fence_before_sync();
     __syncthreads();
