@@ -213,10 +213,9 @@ inline DeviceHead upload(const Model& model, int device = 0) {
     return DeviceHead(h);
 }
 
-// build_model (lutham.cpp:214-271) straight to the device: same validation
-// (ContractError on K < 1, size mismatch, index >= K, negative gain) and the
-// same f32 / int8 conversion.
-inline DeviceHead build_device_model(const CompressedNetwork& cn, int device = 0) {
+namespace b200_detail {
+// CompressedLayer (+ Int8Tables) views for skan_head_create / skan_head_swap
+inline std::vector<skan_layer_desc> compressed_descs(const CompressedNetwork& cn) {
     if (cn.layers.empty()) throw ShapeError("model has no layers");
     std::vector<skan_layer_desc> d(cn.layers.size());
     for (std::size_t l = 0; l < cn.layers.size(); ++l) {
@@ -233,22 +232,22 @@ inline DeviceHead build_device_model(const CompressedNetwork& cn, int device = 0
         h.k = static_cast<std::uint32_t>(cl.codebook.k);
         h.domain_lo = cl.domain_lo;
         h.domain_hi = cl.domain_hi;
-        x.header = b200_detail::to_c(h);
+        x.header = to_c(h);
         if (cl.codebook.grid_size != cl.grid_size) throw ContractError("codebook does not match layer grid size");
-        x.codebook = b200_detail::ptr(cl.codebook.entries);
+        x.codebook = ptr(cl.codebook.entries);
         x.n_codebook = cl.codebook.entries.size();
-        x.indices = b200_detail::ptr(cl.indices);
-        x.gains = b200_detail::ptr(cl.gains);
-        x.biases = b200_detail::ptr(cl.biases);
+        x.indices = ptr(cl.indices);
+        x.gains = ptr(cl.gains);
+        x.biases = ptr(cl.biases);
         x.n_indices = cl.indices.size();
         x.n_gains = cl.gains.size();
         x.n_biases = cl.biases.size();
         if (cl.int8) {
             const Int8Tables& t = *cl.int8;
             x.has_int8 = 1;
-            x.codebook_codes = b200_detail::ptr(t.codebook_codes);
-            x.gain_codes = b200_detail::ptr(t.gain_codes);
-            x.bias_codes = b200_detail::ptr(t.bias_codes);
+            x.codebook_codes = ptr(t.codebook_codes);
+            x.gain_codes = ptr(t.gain_codes);
+            x.bias_codes = ptr(t.bias_codes);
             x.n_codebook_codes = t.codebook_codes.size();
             x.n_gain_codes = t.gain_codes.size();
             x.n_bias_codes = t.bias_codes.size();
@@ -258,9 +257,25 @@ inline DeviceHead build_device_model(const CompressedNetwork& cn, int device = 0
             x.bias_scale = t.bias_params.scale;
         }
     }
+    return d;
+}
+}  // namespace b200_detail
+
+// build_model (lutham.cpp:214-271) straight to the device: same validation
+// (ContractError on K < 1, size mismatch, index >= K, negative gain) and the
+// same f32 / int8 conversion.
+inline DeviceHead build_device_model(const CompressedNetwork& cn, int device = 0) {
+    const std::vector<skan_layer_desc> d = b200_detail::compressed_descs(cn);
     skan_head* h = nullptr;
     b200_detail::check(skan_head_create(d.data(), static_cast<int>(d.size()), device, &h));
     return DeviceHead(h);
+}
+
+// Hot swap: refill `head` in place with a network of the same shapes
+// (skan_head_swap); its workspaces stay valid.  Ordered on `stream`.
+inline void swap_device_model(DeviceHead& head, const CompressedNetwork& cn, void* stream = nullptr) {
+    const std::vector<skan_layer_desc> d = b200_detail::compressed_descs(cn);
+    b200_detail::check(skan_head_swap(head.get(), d.data(), static_cast<int>(d.size()), stream));
 }
 
 // build_dense_model (lutham.cpp:177-195) straight to the device.

@@ -179,6 +179,15 @@ skan_status skan_head_load_file(const char* path, int device, skan_head** out);
 
 skan_status skan_head_destroy(skan_head* head);
 
+/* Hot swap (no reference counterpart; the reference reloads a Model,
+ * lutham.cpp:715-724): replace every table of `head` in place with the
+ * layers described (validated like skan_head_create), keeping its device
+ * allocation, plan and workspaces.  The new layers must match the old ones
+ * in shape, grid size, K and format.  The copy is ordered on `stream`
+ * (cudaStream_t) and complete on return; forwards on other streams must not
+ * overlap it. */
+skan_status skan_head_swap(skan_head* head, const skan_layer_desc* layers, int n_layers, void* stream);
+
 /* Model::input_dim/output_dim/max_width (lutham.cpp:160-175), layer count
  * and per-layer headers (Model::header, lutham.cpp:154). */
 int skan_head_num_layers(const skan_head* head);

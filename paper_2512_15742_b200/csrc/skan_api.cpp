@@ -414,11 +414,19 @@ Staged stage_runtime(const skan_layer_desc& d, int l) {
 
 // Copy the staged layers into one device allocation (sub-buffers 256-B
 // aligned) and fill the kernel-side DevLayer views.
-void upload(skan_head* h, std::vector<Staged>& st) {
+// With `swap` the head's existing allocation is refilled (hot swap: same
+// plan), ordered on `stream`; otherwise it is allocated here.
+void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream_t stream = nullptr) {
     uint64_t total = 0;
     for (const auto& lp : h->lplan) total = add_checked(total, lp.device_bytes);
-    h->dbytes = total;
-    skan::cuda_check(cudaMalloc(&h->dmem, std::max<uint64_t>(total, 256)), "cudaMalloc(head)");
+    if (swap) {
+        if (total != h->dbytes) raise(SKAN_CONTRACT_ERROR, "hot swap needs a head with the same memory plan");
+        h->dl.clear();
+        h->headers.clear();
+    } else {
+        h->dbytes = total;
+        skan::cuda_check(cudaMalloc(&h->dmem, std::max<uint64_t>(total, 256)), "cudaMalloc(head)");
+    }
     std::vector<uint8_t> host(total, 0);
     uint64_t cur = 0;
     auto put = [&](const void* src, uint64_t bytes) -> void* {
@@ -519,14 +527,15 @@ void upload(skan_head* h, std::vector<Staged>& st) {
         h->dl.push_back(d);
         h->headers.push_back(s.h);
     }
-    skan::cuda_check(cudaMemcpy(h->dmem, host.data(), total, cudaMemcpyHostToDevice), "upload head");
+    if (swap) {
+        skan::cuda_check(cudaMemcpyAsync(h->dmem, host.data(), total, cudaMemcpyHostToDevice, stream), "swap head");
+        skan::cuda_check(cudaStreamSynchronize(stream), "swap head");  // host image is freed on return
+    } else {
+        skan::cuda_check(cudaMemcpy(h->dmem, host.data(), total, cudaMemcpyHostToDevice), "upload head");
+    }
 }
 
-skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
-    if (n <= 0 || !layers) raise(SKAN_SHAPE_ERROR, "model has no layers");
-    int ndev = 0;
-    skan::cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    if (device < 0 || device >= ndev) raise(SKAN_CONTRACT_ERROR, "no such CUDA device");
+std::vector<Staged> stage_all(const skan_layer_desc* layers, int n) {
     std::vector<Staged> st;
     st.reserve(n);
     for (int l = 0; l < n; ++l) {
@@ -541,6 +550,24 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
             raise(SKAN_SHAPE_ERROR, "layer " + std::to_string(l - 1) + " out_dim does not match layer " +
                                         std::to_string(l) + " in_dim");
     }
+    return st;
+}
+
+// Kernel-side copies of the layer views for the persistent batch-1 plan.
+void refresh_b1_layers(skan_head* h) {
+    const int nl = static_cast<int>(h->dl.size());
+    for (int l = 0; l < nl && l < skan::kMaxHeadLayers; ++l) h->b1_plan.L[l] = h->dl[l];
+    const DevLayer& L0 = h->dl[0];
+    for (int i = 0; i < L0.G && i < 33; ++i)  // node_position, kan.cpp:21-26
+        h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
+}
+
+skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
+    if (n <= 0 || !layers) raise(SKAN_SHAPE_ERROR, "model has no layers");
+    int ndev = 0;
+    skan::cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) raise(SKAN_CONTRACT_ERROR, "no such CUDA device");
+    std::vector<Staged> st = stage_all(layers, n);
     auto h = std::make_unique<skan_head>();
     h->device = device;
     std::vector<skan_layer_header> hs;
@@ -564,10 +591,7 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
     if (skan::head_b1_supported(h->dl.data(), nl)) {
         h->b1_smem = skan::head_b1_smem(h->dl.data(), nl, h->num_sms, &h->b1_plan);
         h->b1_plan.nl = nl;
-        for (int l = 0; l < nl; ++l) h->b1_plan.L[l] = h->dl[l];
-        const DevLayer& L0 = h->dl[0];
-        for (int i = 0; i < L0.G && i < 33; ++i)  // node_position, kan.cpp:21-26
-            h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
+        refresh_b1_layers(h.get());
         h->b1_grid = skan::head_b1_max_grid(h->b1_smem, h->num_sms);
         // the persistent kernel pays for its cooperative launch and grid
         // barriers only on heads whose first layer is wide enough for the
@@ -782,6 +806,30 @@ skan_status skan_head_create(const skan_layer_desc* layers, int n, int device, s
     return guarded([&] {
         if (!out) raise(SKAN_CONTRACT_ERROR, "null output handle");
         *out = create_head(layers, n, device);
+    });
+}
+
+skan_status skan_head_swap(skan_head* h, const skan_layer_desc* layers, int n, void* stream) {
+    return guarded([&] {
+        if (!h) raise(SKAN_CONTRACT_ERROR, "null head");
+        if (n != static_cast<int>(h->headers.size()) || !layers)
+            raise(SKAN_CONTRACT_ERROR, "hot swap needs the same number of layers");
+        std::vector<Staged> st = stage_all(layers, n);
+        for (int l = 0; l < n; ++l) {
+            const skan_layer_header &a = st[l].h, &b = h->headers[l];
+            if (a.in_dim != b.in_dim || a.out_dim != b.out_dim || a.grid_size != b.grid_size || a.k != b.k ||
+                (a.flags & SKAN_FLAG_INT8) != (b.flags & SKAN_FLAG_INT8))
+                raise(SKAN_CONTRACT_ERROR, "hot swap needs the same layer shapes, grid sizes, K and formats");
+        }
+        std::vector<skan_layer_header> hs;
+        for (auto& x : st) hs.push_back(x.h);
+        std::vector<skan_layer_plan> lp(n);
+        const skan_memory_plan tot = plan(hs.data(), n, lp.data());
+        DeviceGuard g(h->device);
+        h->lplan = lp;
+        h->totals = tot;
+        upload(h, st, /*swap=*/true, static_cast<cudaStream_t>(stream));
+        if (h->b1_ok) refresh_b1_layers(h);
     });
 }
 

@@ -219,14 +219,17 @@ class Model:
     def __init__(self, handle: C.c_void_p, keepalive=None):
         self._h = handle
         self._keep = keepalive  # host arrays only needed during creation
-        L = _lib.lib()
-        n = L.skan_head_num_layers(handle)
-        self.layers: List[LayerHeader] = []
-        for l in range(n):
-            hc = _lib.LayerHeaderC()
-            _lib.check(L.skan_head_layer_header(handle, l, C.byref(hc)))
-            self.layers.append(LayerHeader.from_c(hc))
+        self.layers: List[LayerHeader] = self._refresh_layers()
         self._keep = None
+
+    def _refresh_layers(self) -> List[LayerHeader]:
+        L = _lib.lib()
+        out = []
+        for l in range(L.skan_head_num_layers(self._h)):
+            hc = _lib.LayerHeaderC()
+            _lib.check(L.skan_head_layer_header(self._h, l, C.byref(hc)))
+            out.append(LayerHeader.from_c(hc))
+        return out
 
     @property
     def handle(self) -> C.c_void_p:
@@ -287,6 +290,11 @@ def build_model(cn: CompressedNetwork, device: int = 0) -> Model:
     """build_model (lutham.cpp:214-271), validated the same way, uploaded to `device`."""
     if not cn.layers:
         raise ShapeError("model has no layers")
+    descs, keep = _compressed_descs(cn)
+    return _create(descs, device, keep)
+
+
+def _compressed_descs(cn: CompressedNetwork):
     descs, keep = [], []
     for cl in cn.layers:
         d = _lib.LayerDescC()
@@ -314,7 +322,19 @@ def build_model(cn: CompressedNetwork, device: int = 0) -> Model:
             d.codebook_scale, d.gain_log_min = t.codebook_scale, t.gain_log_min
             d.gain_log_step, d.bias_scale = t.gain_log_step, t.bias_scale
         descs.append(d)
-    return _create(descs, device, keep)
+    return descs, keep
+
+
+def swap_model(model: Model, cn: CompressedNetwork, stream=None) -> None:
+    """Hot swap (skan_head_swap): refill a resident head in place from a
+    CompressedNetwork of the same shapes; workspaces stay valid."""
+    if not cn.layers:
+        raise ShapeError("model has no layers")
+    descs, keep = _compressed_descs(cn)
+    arr = (_lib.LayerDescC * len(descs))(*descs)
+    _lib.check(_lib.lib().skan_head_swap(model.handle, arr, len(descs), stream))
+    model.layers = model._refresh_layers()
+    del keep
 
 
 def build_dense_model(net: KanNetwork, device: int = 0) -> Model:

@@ -280,6 +280,18 @@ TEST_GPU("errors, batch 0 and interp_ops follow compressed_forward (lutham.cpp:8
     CHECK_THROWS_AS(build_device_model(bad), ContractError);
 }
 
+TEST_GPU("swap_device_model: a resident head refilled in place forwards like the new model") {
+    const CompressedNetwork a = head({64, 48, 5}, 10, 256, true, 31), b = head({64, 48, 5}, 10, 256, true, 32);
+    DeviceHead dev = build_device_model(a);
+    DeviceWorkspace ws = make_workspace(dev, 8);
+    swap_device_model(dev, b);
+    const std::vector<double> x = inputs(4, 64, 5);
+    std::vector<double> y(4 * 5);
+    compressed_forward(dev, x, 4, y, ws, DeviceMode::Exact);
+    CHECK(bitwise_equal(y, ref_forward(build_model(b), x, 4)));
+    CHECK_THROWS_AS(swap_device_model(dev, head({64, 40, 5}, 10, 256, true, 33)), ContractError);
+}
+
 TEST_GPU("cfg2 head {2048,1408,20} K=65536 int8: batch 1 fast within tolerance, exact bitwise") {
     const CompressedNetwork cn = head({2048, 1408, 20}, 10, 65536, true, 2026);
     const Model model = build_model(cn);

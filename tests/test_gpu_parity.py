@@ -425,3 +425,29 @@ def test_fast_mode_tensor_core_gemm_formats(torch_cuda, batch):
         assert_close(got, want, l1_scale(tables, x, batch))
         again, _ = _gpu_forward(model, x, batch, "fast", max_batch=256)
         assert np.array_equal(_bits(got), _bits(again)), name  # fixed-order split reduction
+
+
+def test_hot_swap_refills_a_resident_head(torch_cuda):
+    """skan_head_swap: a head (batch-1 persistent path and the multi-kernel
+    path) refilled in place serves the new tables bitwise in exact mode and
+    within tolerance in fast mode; shape changes are a ContractError."""
+    dims = (512, 512, 8)
+    a = synthetic.synthetic_head(dims=dims, k=4096, grid=10, int8=True, seed=1)
+    b = synthetic.synthetic_head(dims=dims, k=4096, grid=10, int8=True, seed=2)
+    tb = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(b)]
+    model = hq.build_model(a)
+    ws = hq.make_workspace(model, max_batch=8)
+    x = synthetic.synthetic_inputs(3, 512, seed=4)
+    want, _ = oracle.port_forward(tb, x, 3)
+    hq.swap_model(model, b)
+    y = np.zeros(3 * 8)
+    hq.compressed_forward(model, x, 3, y, ws, mode="exact")
+    assert np.array_equal(_bits(y), _bits(want))
+    for batch in (1, 3):
+        xb = x[:batch * 512]
+        wb, _ = oracle.port_forward(tb, xb, batch)
+        yb = np.zeros(batch * 8)
+        hq.compressed_forward(model, xb, batch, yb, ws, mode="fast")
+        assert_close(yb, wb, l1_scale(tb, xb, batch))
+    with pytest.raises(hq.ContractError):
+        hq.swap_model(model, synthetic.synthetic_head(dims=(512, 500, 8), k=4096, grid=10, int8=True, seed=3))
