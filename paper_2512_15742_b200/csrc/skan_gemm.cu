@@ -20,11 +20,10 @@ namespace skan {
 namespace {
 
 __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__ A, const float* __restrict__ B,
-                                                      float* __restrict__ D, int N, int K, int passes) {
+                                                      float* __restrict__ D, int N, int K, int passes, int M) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_tmem;
-    constexpr int M = 128;
     unsigned char* a_hi = smem;
     unsigned char* a_lo = a_hi + M * K * 4;
     unsigned char* b_hi = a_lo + M * K * 4;
@@ -80,7 +79,7 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
             : "memory");
     }
     tc::fence_after_sync();
-    const int row = warp * 32 + lane;
+    const int row = warp * 32 + lane;  // TMEM lane (== row for M = 128; raw lanes are dumped for M = 64)
     for (int c = 0; c < N; c += 8) {
         float v[8];
         tc::tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
@@ -97,12 +96,15 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
 
 extern "C" skan_status skan_debug_gemm_tf32(const float* dA, const float* dB, float* dD, int N, int K, int passes,
                                             void* stream) {
+    // passes >= 100: M = 64 variant (passes - 100), D receives the raw 128 TMEM lanes
+    const int M = passes >= 100 ? 64 : 128;
+    if (passes >= 100) passes -= 100;
     if (N < 8 || N > 256 || N % 16 || K < 8 || K > 64 || K % 8)
         return skan::set_error(SKAN_SHAPE_ERROR, "debug gemm: N in [16,256] step 16, K in [8,64] step 8", 0,
                                SKAN_FAULT_NONE);
     const size_t smem = static_cast<size_t>(2 * 128 * K + 2 * N * K) * 4;
     cudaFuncSetAttribute(skan::k_debug_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    skan::k_debug_gemm<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K, passes);
+    skan::k_debug_gemm<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K, passes, M);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return skan::set_error(SKAN_CUDA_ERROR, cudaGetErrorString(e), 0, SKAN_FAULT_NONE);
     return SKAN_OK;
@@ -140,6 +142,7 @@ constexpr int kGmM = 128;  // samples per tile (MMA M)
 constexpr int kGmN = 128;  // outputs per tile (MMA N, TMEM columns)
 constexpr int kGmP = 512;        // producers: 4 knot groups x 128 output columns (W), 128 samples x 4 inputs (A)
 constexpr int kGmT = kGmP + 32;  // + one warp that issues the tensor-core MMAs
+constexpr int kStg = 3;          // DENSE: grid-slab staging slots (TMA bulk copies, 3 chunks ahead)
 
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
     uint32_t done = 0;
@@ -197,22 +200,28 @@ __device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int
 // tile: W is written with 16-byte stores.  IC is 4 (G even) or 8 (G odd).
 // Thread t: W for output column t % 128 at knots t/128, t/128 + 4, ...;
 // A for sample t % 128 at input t / 128 (and + 4 when IC = 8).
-template <int FMT, int IC>
+template <int FMT, int IC, int MT>  // MT: samples per tile (MMA M = 64 or 128)
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[2];   // stage free: committed by the MMA warp
     __shared__ __align__(8) uint64_t s_full[2];  // stage written: every producer arrives
+    __shared__ __align__(8) uint64_t s_stg[kStg];  // DENSE: grid slab of chunk c landed in staging slot c % kStg
     __shared__ uint32_t s_tmem;
     __shared__ float s_lut[256];
     const DevLayer& L = a.L;
     const int G = L.G, KC = IC * G;
-    const uint32_t tile = kGmM * KC * 4;    // kGmM == kGmN: A and W tiles have one size
-    const uint32_t stage_bytes = 4 * tile;  // [A_hi][A_lo][W_hi][W_lo]
-    constexpr uint32_t kLbo = (kGmM / 8) * 128;
-    constexpr int kAU = IC * kGmM / kGmP;  // A slots per producer (1 or 2)
+    const uint32_t tile_a = MT * KC * 4, tile_w = kGmN * KC * 4;
+    const uint32_t stage_bytes = 2 * tile_a + 2 * tile_w;  // [A_hi][A_lo][W_hi][W_lo]
+    constexpr uint32_t kLboA = (MT / 8) * 128, kLboW = (kGmN / 8) * 128;
+    constexpr int kAU = (IC * MT + kGmP - 1) / kGmP;  // A slots per producer (1 or 2)
+    // DENSE: the grid slab of a chunk (IC inputs x 128 columns x G floats) is
+    // bulk-copied into a staging ring behind the two operand stages
+    const bool stg = FMT == FMT_DENSE && a.tma_w;
+    const uint32_t slab = kGmN * static_cast<uint32_t>(G) * 4;  // bytes per input row of the slab
+    unsigned char* s_slab = smem + 2 * stage_bytes;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * kGmM;
-    const int nS = min(kGmM, a.B - s0), nJ = min(kGmN, L.out - j0);
+    const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * MT;
+    const int nS = min(MT, a.B - s0), nJ = min(kGmN, L.out - j0);
     const int r0 = blockIdx.y * a.rows_per_cta, rend = min(L.in, r0 + a.rows_per_cta);
     const int nchunks = rend > r0 ? (rend - r0 + IC - 1) / IC : 0;
     pdl_trigger();
@@ -223,13 +232,14 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     // stages once, then write and clear only the nonzeros
     for (uint32_t q = tid * 16; q < 2 * stage_bytes; q += kGmT * 16) {
         const uint32_t st = q / stage_bytes, o = q % stage_bytes;
-        if (o < 2 * tile) *reinterpret_cast<uint4*>(smem + st * stage_bytes + o) = make_uint4(0, 0, 0, 0);
+        if (o < 2 * tile_a) *reinterpret_cast<uint4*>(smem + st * stage_bytes + o) = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[1])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[0])), "r"(kGmP));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[1])), "r"(kGmP));
+        for (int q = 0; q < kStg; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_stg[q])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tc::tmem_alloc<kGmN>(&s_tmem);
@@ -237,10 +247,10 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
-    const uint32_t idesc = tc::idesc_tf32(kGmM, kGmN);
+    const uint32_t idesc = tc::idesc_tf32(MT, kGmN);
 
-    const int rl = tid & (kGmM - 1), grp = tid >> 7;  // grp in 0..3
-    const uint32_t rbase = tc::kmajor_off(rl, 0, kGmM);  // row part of the offset
+    const int rl = tid & (kGmN - 1), grp = tid >> 7;  // W: output column, knot group 0..3
+    const uint32_t rbase = tc::kmajor_off(rl, 0, kGmN);  // row part of the W offset
     EdgeRaw er[IC];
     unsigned evalid = 0;   // edges of the staged chunk inside the layer
     uint32_t recn[IC], kn[IC];  // I8: records of the chunk after the staged one
@@ -290,7 +300,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                     er[il].k = L.idx ? __ldg(L.idx + e) : 0u;
                     er[il].g = __ldg(L.gain + e);
                     er[il].b = __ldg(L.bias + e);
-                } else {
+                } else if (!stg) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int m = grp + 4 * u;
@@ -301,11 +311,11 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < kAU; ++u) {
-            const int i = ib + grp + 4 * u;
+            const int q = tid + kGmP * u, ra = q % MT, ila = q / MT, i = ib + ila;
             bm[u] = -2;
             bt[u] = 0.f;
-            if (rl < nS && i < rend) {
-                const size_t p = static_cast<size_t>(i) * a.B + s0 + rl;
+            if (ila < IC && ra < nS && i < rend) {
+                const size_t p = static_cast<size_t>(i) * a.B + s0 + ra;
                 bm[u] = a.bm_in[p];
                 bt[u] = a.bt_in[p];
             }
@@ -327,6 +337,13 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             const int buf = c & 1;
             unsigned char* st = smem + buf * stage_bytes;
             if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);
+            const float* slabf = nullptr;
+            if constexpr (FMT == FMT_DENSE) {
+                if (stg) {
+                    mbar_wait_parity(&s_stg[c % kStg], (c / kStg) & 1);
+                    slabf = reinterpret_cast<const float*>(s_slab + (c % kStg) * IC * slab);
+                }
+            }
             // W: this thread's knots, the IC inputs' values as 16-byte groups
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -338,36 +355,43 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int il = 4 * h + q;
+                        if constexpr (FMT == FMT_DENSE) {
+                            if (stg) {
+                                v[q] = (evalid >> il & 1) ? slabf[(il * kGmN + rl) * G + m] : 0.f;
+                                continue;
+                            }
+                        }
                         v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], m, u) : 0.f;
                     }
-                    const uint32_t o = (m * (IC / 4) + h) * kLbo + rbase;
-                    *reinterpret_cast<float4*>(st + 2 * tile + o) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(st + 3 * tile + o) =
+                    const uint32_t o = (m * (IC / 4) + h) * kLboW + rbase;
+                    *reinterpret_cast<float4*>(st + 2 * tile_a + o) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4*>(st + 2 * tile_a + tile_w + o) =
                         make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]), tc::tf32_lo(v[2]), tc::tf32_lo(v[3]));
                 }
             }
             // A: clear the two weights chunk c-2 left, write this chunk's
 #pragma unroll
             for (int u = 0; u < kAU; ++u) {
-                const int il = grp + 4 * u;
+                const int qa = tid + kGmP * u, ra = qa % MT, il = qa / MT;
+                const uint32_t rbase_a = tc::kmajor_off(ra, 0, MT);
                 uint32_t& ao = buf ? aoff1[u] : aoff0[u];
                 if (ao != 0xFFFFFFFFu) {
                     const uint32_t o0 = ao & 0xFFFFu, o1 = ao >> 16;
                     *reinterpret_cast<float*>(st + o0) = 0.f;
-                    *reinterpret_cast<float*>(st + tile + o0) = 0.f;
+                    *reinterpret_cast<float*>(st + tile_a + o0) = 0.f;
                     *reinterpret_cast<float*>(st + o1) = 0.f;
-                    *reinterpret_cast<float*>(st + tile + o1) = 0.f;
+                    *reinterpret_cast<float*>(st + tile_a + o1) = 0.f;
                     ao = 0xFFFFFFFFu;
                 }
                 if (bm[u] >= 0) {
                     const int k0 = bm[u] * IC + il, k1 = k0 + IC;
-                    const uint32_t o0 = rbase + (k0 >> 2) * kLbo + (k0 & 3) * 4;
-                    const uint32_t o1 = rbase + (k1 >> 2) * kLbo + (k1 & 3) * 4;
+                    const uint32_t o0 = rbase_a + (k0 >> 2) * kLboA + (k0 & 3) * 4;
+                    const uint32_t o1 = rbase_a + (k1 >> 2) * kLboA + (k1 & 3) * 4;
                     const float w0 = 1.f - bt[u], w1 = bt[u];
                     *reinterpret_cast<float*>(st + o0) = w0;
-                    *reinterpret_cast<float*>(st + tile + o0) = tc::tf32_lo(w0);
+                    *reinterpret_cast<float*>(st + tile_a + o0) = tc::tf32_lo(w0);
                     *reinterpret_cast<float*>(st + o1) = w1;
-                    *reinterpret_cast<float*>(st + tile + o1) = tc::tf32_lo(w1);
+                    *reinterpret_cast<float*>(st + tile_a + o1) = tc::tf32_lo(w1);
                     ao = o0 | (o1 << 16);
                 }
             }
@@ -376,21 +400,40 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[buf])) : "memory");
         }
     } else {
-        // the MMA warp: one lane issues 3 x (KC/8) tcgen05.mma per chunk, in order
+        // the MMA warp: one lane issues 3 x (KC/8) tcgen05.mma per chunk, in
+        // order (and, for dense layers, the grid-slab bulk copies kStg chunks ahead)
+        auto issue_slab = [&](int c) {
+            if constexpr (FMT == FMT_DENSE) {
+                if (!stg || c >= nchunks) return;
+                const int ib = r0 + c * IC;
+                const uint32_t bytes = static_cast<uint32_t>(nJ) * G * 4;
+                int nv = 0;
+                for (int il = 0; il < IC; ++il) nv += ib + il < rend;
+                uint64_t* bar = &s_stg[c % kStg];
+                mbar_expect_tx(bar, nv * bytes);
+                unsigned char* dst = s_slab + (c % kStg) * IC * slab;
+                for (int il = 0; il < IC; ++il)
+                    if (ib + il < rend)
+                        bulk_g2s(dst + il * slab, L.cb32 + (static_cast<size_t>(ib + il) * L.out + j0) * G, bytes, bar);
+            }
+        };
+        if (lane == 0)
+            for (int c = 0; c < kStg; ++c) issue_slab(c);
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
             const int buf = c & 1;
             mbar_wait_parity(&s_full[buf], (c >> 1) & 1);
             if (lane == 0) {
+                issue_slab(c + kStg);  // the producers are done with chunk c's slab
                 tc::fence_after_sync();
                 const uint32_t base = tc::smem_addr(smem + buf * stage_bytes);
 #pragma unroll 1
                 for (int s = 0; s < KC / 8; ++s) {
-                    const uint32_t o = s * 2 * kLbo;
-                    const uint64_t ah = tc::make_desc(base + o, kLbo, 128);
-                    const uint64_t al = tc::make_desc(base + tile + o, kLbo, 128);
-                    const uint64_t wh = tc::make_desc(base + 2 * tile + o, kLbo, 128);
-                    const uint64_t wl = tc::make_desc(base + 3 * tile + o, kLbo, 128);
+                    const uint32_t oa = s * 2 * kLboA, ow = s * 2 * kLboW;
+                    const uint64_t ah = tc::make_desc(base + oa, kLboA, 128);
+                    const uint64_t al = tc::make_desc(base + tile_a + oa, kLboA, 128);
+                    const uint64_t wh = tc::make_desc(base + 2 * tile_a + ow, kLboW, 128);
+                    const uint64_t wl = tc::make_desc(base + 2 * tile_a + tile_w + ow, kLboW, 128);
                     tc::mma_tf32(tmem, ah, wh, idesc, c > 0 || s > 0);
                     tc::mma_tf32(tmem, ah, wl, idesc, true);
                     tc::mma_tf32(tmem, al, wh, idesc, true);
@@ -405,9 +448,10 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     // epilogue: producer warp w reads TMEM lanes (w%4)*32.. (its samples), columns (w/4)*32..+32
     const int q4 = warp & 3, cq = warp >> 2;
     if (warp < kGmP / 32) {
-    const int row = q4 * 32 + lane;
+    // M = 128: sample r in TMEM lane r; M = 64: sample r in lane (r/16)*32 + r%16
+    const int row = MT == 128 ? q4 * 32 + lane : (lane < 16 ? q4 * 16 + lane : MT);
     const size_t plane = static_cast<size_t>(a.B) * L.out;
-    float* dst = a.partial + blockIdx.y * plane + static_cast<size_t>(s0 + row) * L.out + j0;
+    float* dst = a.partial + blockIdx.y * plane + static_cast<size_t>(s0 + min(row, MT - 1)) * L.out + j0;
 #pragma unroll 1
     for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
         float v[8];
@@ -510,14 +554,14 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStre
 // a multiple of 4 (16-byte W groups): 4 for even G, 8 for odd G.
 int gemm_ic(int G) { return G % 2 == 0 ? 4 : 8; }
 
-size_t gemm_smem(int G) {
+size_t gemm_smem(int G, bool dense, int mt = kGmM) {
     const size_t kc = static_cast<size_t>(gemm_ic(G)) * G;
-    return 2 * (2 * kGmM * kc * 4 + 2 * kGmN * kc * 4);
+    return 2 * (2 * static_cast<size_t>(mt) * kc * 4 + 2 * kGmN * kc * 4) + (dense ? kStg * kc * kGmN * 4 : 0);
 }
 
 bool gemm_supported(const DevLayer& L) {
     const int ic = gemm_ic(L.G);
-    return ic > 0 && L.G <= 16 && gemm_smem(L.G) <= 200 * 1024 &&
+    return ic > 0 && L.G <= 16 && gemm_smem(L.G, L.fmt == FMT_DENSE) <= 222 * 1024 &&
            (L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32 || L.fmt == FMT_DENSE);
 }
 
@@ -526,7 +570,8 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     c.kind = 4;
     c.ic = gemm_ic(L.G);
     c.jt = (L.out + kGmN - 1) / kGmN;
-    c.st = (B + kGmM - 1) / kGmM;
+    c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: the M = 64 MMA when the batch fits it
+    c.st = (B + c.spt - 1) / c.spt;
     c.tj = kGmN;
     const int sms = num_sms > 0 ? num_sms : 148;
     // one CTA per SM: the fewest input splits whose waves are >= 90% full
@@ -547,21 +592,29 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
     c.ichunk = per * c.ic;
     c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
-    c.smem = gemm_smem(L.G);
+    c.smem = gemm_smem(L.G, L.fmt == FMT_DENSE, c.spt);
     return c;
 }
 
-void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
-    void (*k)(FwdArgs);
-    const bool i4 = c.ic == 4;
-    switch (a.L.fmt) {
-        case FMT_I8_R32: k = i4 ? k_layer_gemm<FMT_I8_R32, 4> : k_layer_gemm<FMT_I8_R32, 8>; break;
-        case FMT_I8_WIDE: k = i4 ? k_layer_gemm<FMT_I8_WIDE, 4> : k_layer_gemm<FMT_I8_WIDE, 8>; break;
-        case FMT_F32: k = i4 ? k_layer_gemm<FMT_F32, 4> : k_layer_gemm<FMT_F32, 8>; break;
-        default: k = i4 ? k_layer_gemm<FMT_DENSE, 4> : k_layer_gemm<FMT_DENSE, 8>; break;
+template <int MT>
+void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
+    const bool i4 = ic == 4;
+    switch (fmt) {
+        case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, MT> : k_layer_gemm<FMT_I8_R32, 8, MT>;
+        case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, MT> : k_layer_gemm<FMT_I8_WIDE, 8, MT>;
+        case FMT_F32: return i4 ? k_layer_gemm<FMT_F32, 4, MT> : k_layer_gemm<FMT_F32, 8, MT>;
+        default: return i4 ? k_layer_gemm<FMT_DENSE, 4, MT> : k_layer_gemm<FMT_DENSE, 8, MT>;
     }
+}
+
+void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    void (*k)(FwdArgs) = c.spt == 64 ? gemm_kernel<64>(a.L.fmt, c.ic) : gemm_kernel<128>(a.L.fmt, c.ic);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
-    launch_pdl(k, dim3(c.jt, c.nsplit, c.st), dim3(kGmT), c.smem, pdl, s, a);
+    FwdArgs g = a;
+    // dense slabs by TMA when every slab row is 16-byte aligned
+    g.tma_w = a.L.fmt == FMT_DENSE && (static_cast<long long>(a.L.out) * a.L.G) % 4 == 0 &&
+              (reinterpret_cast<uintptr_t>(a.L.cb32) & 15) == 0;
+    launch_pdl(k, dim3(c.jt, c.nsplit, c.st), dim3(kGmT), c.smem, pdl, s, g);
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {

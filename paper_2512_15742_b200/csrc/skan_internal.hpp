@@ -125,6 +125,7 @@ struct FwdArgs {
     const float* prev_partial;    // [prev_nsplit][B][in]
     int prev_nsplit;
     const double* prev_bias_sum;  // [in]
+    int tma_w;                    // layer GEMM: dense grid slabs arrive by TMA bulk copy
 };
 
 // Batch-1 persistent head kernel (skan_head_b1.cu).

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--heads", type=int, default=4)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--skip-dense", action="store_true")
+    ap.add_argument("--only-dense", action="store_true")
     args = ap.parse_args()
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     s = torch.cuda.Stream()
@@ -46,6 +47,8 @@ def main():
     while time.perf_counter() < t_end:
         flush.zero_()
 
+    if args.only_dense:
+        args.heads = 0
     # cfg1
     cn = synthetic.synthetic_head(dims=(256, 256), k=256, grid=10, int8=True, seed=1)
     m = hq.build_model(cn)
@@ -57,13 +60,17 @@ def main():
 
     # cfg5: H cfg2 heads, one shared batch of 256
     heads = [hq.build_model(synthetic.synthetic_head(seed=2026 + 7 * h)) for h in range(args.heads)]
-    wss = [hq.make_workspace(h, 256) for h in heads]
-    xb = torch.from_numpy(synthetic.synthetic_inputs(256, 2048, seed=5)).cuda()
-    ys = [torch.zeros(256 * 20, dtype=torch.float64, device="cuda") for _ in heads]
-    us = timed(lambda: hq.forward_multi(heads, wss, xb, 256, ys, stream=s.cuda_stream), max(3, args.reps // 4), flush, s)
-    print(f"cfg5 {args.heads} heads x batch 256: {us:10.2f} us  -> {args.heads * 256 / us * 1e6:,.0f} head-samples/s",
-          flush=True)
-    del heads, wss
+    if not heads:
+        heads = None
+    if heads:
+        wss = [hq.make_workspace(h, 256) for h in heads]
+        xb = torch.from_numpy(synthetic.synthetic_inputs(256, 2048, seed=5)).cuda()
+        ys = [torch.zeros(256 * 20, dtype=torch.float64, device="cuda") for _ in heads]
+        us = timed(lambda: hq.forward_multi(heads, wss, xb, 256, ys, stream=s.cuda_stream), max(3, args.reps // 4),
+                   flush, s)
+        print(f"cfg5 {args.heads} heads x batch 256: {us:10.2f} us  -> {args.heads * 256 / us * 1e6:,.0f} "
+              f"head-samples/s", flush=True)
+        del heads, wss
 
     if not args.skip_dense:
         layers = synthetic.dense_runtime_head()
