@@ -271,6 +271,12 @@ int skan_head_b1_grid(const skan_head* head);
 skan_status skan_debug_gemm_tf32(const float* d_a, const float* d_b, float* d_d, int n, int k, int passes,
                                  void* stream);
 
+/* Phase timeline of the tensor-core layer GEMM: while d_stamps is set,
+ * every layer-GEMM launch has CTA (0,0,0) write clock64 stamps into
+ * d_stamps[2][64][8] (role 0: producer thread 0, role 1: the MMA thread;
+ * per chunk < 64, phases as skan_gemm.cu documents).  NULL disables. */
+skan_status skan_debug_gemm_timeline(unsigned long long* d_stamps);
+
 /* ---- single-edge primitive (lutham.cpp:730-755) ----------------------- */
 
 /* Batched pli_lookup over n independent (row, g, b, x) tuples on the GPU:

@@ -102,12 +102,24 @@ int device_format(const skan_layer_header& h) {
     return skan::FMT_F32;
 }
 
+// Dense layers wide enough for the tensor-core layer GEMM also keep their
+// grid pre-tiled in its shared-memory layout (DevLayer::wt): the GEMM then
+// streams each chunk with one TMA bulk copy.  Built on the device at upload.
+bool dense_tiled(const skan_layer_header& h) {
+    return h.k == 0 && h.out_dim >= 128 && h.grid_size >= 2 && h.grid_size <= 16 &&
+           skan::gemm_ic(static_cast<int>(h.grid_size)) * static_cast<int>(h.grid_size) <= 88;
+}
+
 uint64_t device_bytes(const skan_layer_header& h) {
     const uint64_t e = mul_checked(h.in_dim, h.out_dim);
     const int fmt = device_format(h);
     // node positions + their integer keys (fast knot selection), every format
     uint64_t b = 2 * align_up(mul_checked(h.grid_size, 8));
-    if (fmt == skan::FMT_DENSE) return add_checked(b, align_up(mul_checked(mul_checked(e, h.grid_size), 4)));
+    if (fmt == skan::FMT_DENSE) {
+        b = add_checked(b, align_up(mul_checked(mul_checked(e, h.grid_size), 4)));
+        if (dense_tiled(h)) b = add_checked(b, align_up(mul_checked(skan::dense_tile_floats(h.in_dim, h.out_dim, h.grid_size), 4)));
+        return b;
+    }
     const uint64_t kg = mul_checked(h.k, h.grid_size);
     // int8 codebook: rows padded to 16 B (one 128-bit load per row) plus the
     // (c[m], c[m+1]) pair table (one 2-byte gather per edge-sample)
@@ -427,13 +439,25 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
         h->dbytes = total;
         skan::cuda_check(cudaMalloc(&h->dmem, std::max<uint64_t>(total, 256)), "cudaMalloc(head)");
     }
-    std::vector<uint8_t> host(total, 0);
+    // host image of everything but the holes (device-built regions, never touched here)
+    std::unique_ptr<uint8_t[]> host(new uint8_t[std::max<uint64_t>(total, 1)]);
+    std::vector<std::pair<uint64_t, uint64_t>> holes;
     uint64_t cur = 0;
     auto put = [&](const void* src, uint64_t bytes) -> void* {
         if (add_checked(cur, bytes) > total) raise(SKAN_PLAN_ERROR, "resident layout overruns the plan");
         void* dst = static_cast<uint8_t*>(h->dmem) + cur;
-        if (bytes) std::memcpy(host.data() + cur, src, bytes);
-        cur = align_up(add_checked(cur, bytes));
+        if (bytes) std::memcpy(host.get() + cur, src, bytes);
+        const uint64_t next = std::min(align_up(add_checked(cur, bytes)), total);
+        std::memset(host.get() + cur + bytes, 0, next - cur - bytes);
+        cur = next;
+        return dst;
+    };
+    auto reserve = [&](uint64_t bytes) -> void* {
+        if (add_checked(cur, bytes) > total) raise(SKAN_PLAN_ERROR, "resident layout overruns the plan");
+        void* dst = static_cast<uint8_t*>(h->dmem) + cur;
+        const uint64_t next = std::min(align_up(add_checked(cur, bytes)), total);
+        holes.emplace_back(cur, next);
+        cur = next;
         return dst;
     };
     for (size_t l = 0; l < st.size(); ++l) {
@@ -485,6 +509,10 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
         switch (d.fmt) {
             case skan::FMT_DENSE:
                 d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
+                if (dense_tiled(s.h)) {
+                    d.wt = static_cast<const float*>(reserve(skan::dense_tile_floats(d.in, d.out, d.G) * 4));
+                    d.wt_nch = (d.in + skan::gemm_ic(d.G) - 1) / skan::gemm_ic(d.G);
+                }
                 break;
             case skan::FMT_I8_R32:
             case skan::FMT_I8_WIDE: {
@@ -527,12 +555,21 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
         h->dl.push_back(d);
         h->headers.push_back(s.h);
     }
-    if (swap) {
-        skan::cuda_check(cudaMemcpyAsync(h->dmem, host.data(), total, cudaMemcpyHostToDevice, stream), "swap head");
-        skan::cuda_check(cudaStreamSynchronize(stream), "swap head");  // host image is freed on return
-    } else {
-        skan::cuda_check(cudaMemcpy(h->dmem, host.data(), total, cudaMemcpyHostToDevice), "upload head");
+    // copy the image around the holes, then build the device-side regions
+    const cudaStream_t cs = swap ? stream : nullptr;
+    uint64_t from = 0;
+    holes.emplace_back(total, total);
+    for (const auto& hole : holes) {
+        if (hole.first > from)
+            skan::cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(h->dmem) + from, host.get() + from, hole.first - from,
+                                             cudaMemcpyHostToDevice, cs),
+                             swap ? "swap head" : "upload head");
+        from = hole.second;
     }
+    for (const DevLayer& d : h->dl)
+        if (d.wt) skan::build_dense_tiles(d, const_cast<float*>(d.wt), cs);
+    skan::cuda_check(cudaGetLastError(), "dense tiles");
+    skan::cuda_check(cudaStreamSynchronize(cs), swap ? "swap head" : "upload head");  // host image is freed on return
 }
 
 std::vector<Staged> stage_all(const skan_layer_desc* layers, int n) {

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "skan_internal.hpp"
 #include "skan_tc.cuh"
@@ -20,7 +21,7 @@ namespace skan {
 namespace {
 
 __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__ A, const float* __restrict__ B,
-                                                      float* __restrict__ D, int N, int K, int passes, int M) {
+                                                      float* __restrict__ D, int N, int K, int passes, int M, int ts) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint32_t s_tmem;
@@ -46,24 +47,57 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc::fence_proxy_async();
-    if (warp == 0) tc::tmem_alloc<256>(&s_tmem);
+    if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
+    // TS form (M = 128): row r of A_hi / A_lo in TMEM lane r, columns 256 + k / 256 + K + k
+    const uint32_t ta_hi = tmem + 256, ta_lo = tmem + 256 + K;
+    if (ts == 1) {
+        const int r = warp * 32 + lane;
+        for (int c = 0; c < K; c += 8) {
+            float h[8], l[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                h[q] = A[r * K + c + q];
+                l[q] = tc::tf32_lo(h[q]);
+            }
+            tc::tmem_st8(ta_hi + (static_cast<uint32_t>(warp * 32) << 16) + c, h);
+            tc::tmem_st8(ta_lo + (static_cast<uint32_t>(warp * 32) << 16) + c, l);
+        }
+        tc::tmem_wait_st();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
     if (tid == 0) {
         const uint32_t idesc = tc::idesc_tf32(M, N);
         const uint32_t lbo_a = (M / 8) * 128, lbo_b = (N / 8) * 128;
+        if (ts == 2)  // A staged in shared memory, copied into TMEM by the tensor pipe
+            for (int s = 0; s < K / 8; ++s) {
+                const uint32_t oa = s * 2 * lbo_a;
+                tc::cp_128x256b(ta_hi + s * 8, tc::make_desc(tc::smem_addr(a_hi) + oa, lbo_a, 128));
+                tc::cp_128x256b(ta_lo + s * 8, tc::make_desc(tc::smem_addr(a_lo) + oa, lbo_a, 128));
+            }
         for (int s = 0; s < K / 8; ++s) {
             const uint32_t oa = s * 2 * lbo_a, ob = s * 2 * lbo_b;
             const uint64_t ah = tc::make_desc(tc::smem_addr(a_hi) + oa, lbo_a, 128);
             const uint64_t al = tc::make_desc(tc::smem_addr(a_lo) + oa, lbo_a, 128);
             const uint64_t bh = tc::make_desc(tc::smem_addr(b_hi) + ob, lbo_b, 128);
             const uint64_t bl = tc::make_desc(tc::smem_addr(b_lo) + ob, lbo_b, 128);
-            tc::mma_tf32(tmem, ah, bh, idesc, s > 0);
-            if (passes >= 3) {
-                tc::mma_tf32(tmem, ah, bl, idesc, true);
-                tc::mma_tf32(tmem, al, bh, idesc, true);
+            if (ts) {
+                tc::mma_tf32_ts(tmem, ta_hi + s * 8, bh, idesc, s > 0);
+                if (passes >= 3) {
+                    tc::mma_tf32_ts(tmem, ta_hi + s * 8, bl, idesc, true);
+                    tc::mma_tf32_ts(tmem, ta_lo + s * 8, bh, idesc, true);
+                }
+            } else {
+                tc::mma_tf32(tmem, ah, bh, idesc, s > 0);
+                if (passes >= 3) {
+                    tc::mma_tf32(tmem, ah, bl, idesc, true);
+                    tc::mma_tf32(tmem, al, bh, idesc, true);
+                }
             }
         }
         tc::mma_commit(&s_bar);
@@ -88,7 +122,7 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_free<256>(tmem);
+    if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
 }  // namespace
@@ -96,7 +130,11 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
 
 extern "C" skan_status skan_debug_gemm_tf32(const float* dA, const float* dB, float* dD, int N, int K, int passes,
                                             void* stream) {
-    // passes >= 100: M = 64 variant (passes - 100), D receives the raw 128 TMEM lanes
+    // passes >= 300: A from TMEM, copied there from shared memory by
+    // tcgen05.cp; >= 200: A from TMEM written by tcgen05.st (TS form, M =
+    // 128); >= 100: M = 64 variant (passes - 100), D receives the raw 128 TMEM lanes
+    const int ts = passes >= 300 ? 2 : (passes >= 200 ? 1 : 0);
+    passes -= 100 * ts + (ts ? 100 : 0);
     const int M = passes >= 100 ? 64 : 128;
     if (passes >= 100) passes -= 100;
     if (N < 8 || N > 256 || N % 16 || K < 8 || K > 64 || K % 8)
@@ -104,7 +142,7 @@ extern "C" skan_status skan_debug_gemm_tf32(const float* dA, const float* dB, fl
                                SKAN_FAULT_NONE);
     const size_t smem = static_cast<size_t>(2 * 128 * K + 2 * N * K) * 4;
     cudaFuncSetAttribute(skan::k_debug_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    skan::k_debug_gemm<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K, passes, M);
+    skan::k_debug_gemm<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K, passes, M, ts);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return skan::set_error(SKAN_CUDA_ERROR, cudaGetErrorString(e), 0, SKAN_FAULT_NONE);
     return SKAN_OK;
@@ -138,11 +176,10 @@ namespace {
 
 using namespace dev;
 
-constexpr int kGmM = 128;  // samples per tile (MMA M)
-constexpr int kGmN = 128;  // outputs per tile (MMA N, TMEM columns)
-constexpr int kGmP = 512;        // producers: 4 knot groups x 128 output columns (W), 128 samples x 4 inputs (A)
+constexpr int kGmM = 128;        // TMEM lanes = MMA M
+constexpr int kGmN = 128;        // outputs per tile (MMA N, accumulator columns)
+constexpr int kGmP = 512;        // producers: 4 knot groups x 128 output columns (W); 4 x 128 TMEM lanes (A)
 constexpr int kGmT = kGmP + 32;  // + one warp that issues the tensor-core MMAs
-constexpr int kStg = 3;          // DENSE: grid-slab staging slots (TMA bulk copies, 3 chunks ahead)
 
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
     uint32_t done = 0;
@@ -158,13 +195,11 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity)
 // Per-thread staging of one edge (i, j), loaded one chunk ahead: I8 the
 // 16-byte codebook row plus gain and bias already decoded (the record that
 // names the row is loaded one chunk earlier still, so the row load never
-// waits on it); F32 the row index, gain and bias; DENSE the grid values at
-// the thread's knots.
+// waits on it); F32 the row index, gain and bias.
 struct EdgeRaw {
     uint4 row;
     uint32_t k;
     float g, b;
-    float v[4];
 };
 
 // record word of an int8 edge: (row, gain code, bias code); WIDE also the
@@ -180,13 +215,11 @@ __device__ __forceinline__ void rec_load(const DevLayer& L, size_t e, uint32_t& 
     }
 }
 
-// W value of a staged edge at its u-th knot m (fast-path decode); int8
-// codes become floats through the 2^23 + (u ^ 0x80) bit pattern (no I2F).
+// W value of a staged edge at knot m (fast-path decode); int8 codes become
+// floats through the 2^23 + (u ^ 0x80) bit pattern (no I2F).
 template <int FMT>
-__device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int m, int u) {
-    if constexpr (FMT == FMT_DENSE) {
-        return r.v[u];
-    } else if constexpr (FMT == FMT_F32) {
+__device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int m) {
+    if constexpr (FMT == FMT_F32) {
         return fmaf(r.g, __ldg(L.cb32 + static_cast<size_t>(r.k) * L.G + m), r.b);
     } else {
         const uint32_t w = m < 4 ? r.row.x : (m < 8 ? r.row.y : (m < 12 ? r.row.z : r.row.w));
@@ -196,286 +229,401 @@ __device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int
 }
 
 // Chunk K order: k = m * IC + il (knot-major), so the IC inputs of one
-// edge column at one knot are contiguous 4-float groups of the K-major
-// tile: W is written with 16-byte stores.  IC is 4 (G even) or 8 (G odd).
-// Thread t: W for output column t % 128 at knots t/128, t/128 + 4, ...;
-// A for sample t % 128 at input t / 128 (and + 4 when IC = 8).
-template <int FMT, int IC, int MT>  // MT: samples per tile (MMA M = 64 or 128)
+// edge column at one knot are contiguous 4-float groups of the K-major W
+// tile (16-byte stores).  IC is 4 (G even) or 8 (G odd).
+//
+// Operands of one chunk (both from shared memory, canonical K-major):
+//   A (hat weights, 128 rows x KC), written SPARSELY: 2 nonzeros per sample
+//     and input; the thread that owns a (row, input) slot clears its two
+//     entries of the chunk that last used the buffer and writes the new
+//     ones.  STACK (batch <= 64): rows 0-63 = A_hi of samples 0-63, rows
+//     64-127 = their A_lo, so one M = 128 MMA does both; else rows = 128
+//     samples and A_hi, A_lo are two tiles.  Two buffers.
+//   W (KC x NT outputs), hi (raw f32: the tensor core truncates) and lo
+//     planes, `wst` stages.  Compressed layers: decoded by the producers
+//     from the records + codebook; dense layers (NT = 128): the resident
+//     pre-tiled grid (DevLayer::wt, the same byte layout) arrives by TMA
+//     bulk copy into a ring of slots and the producers only derive the lo
+//     plane.
+// MMAs per K = 8 step: STACK 2 (A.W_hi, A.W_lo), else 3 (A_hi.W_hi,
+// A_hi.W_lo, A_lo.W_hi).  (Measured alternatives, tools/mb_mma.cu: A in
+// TMEM runs the MMA ~1.6x faster, but filling TMEM costs more than it
+// saves: tcgen05.cp moves ~40 B/clk, and tcgen05.st needs every hat
+// weight, zeros included, computed in registers.)
+// Debug phase stamps (skan_debug_gemm_timeline): CTA (0,0,0) only, role 0 =
+// producer thread 0 (phases: 0 top, 1 W stage free, 2 W written, 3 A tile
+// free, 4 arrived), role 1 = the MMA thread (0 stage full, 1 descriptors ready,
+// 2 MMAs issued).
+__device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph) {
+    if (a.dbg && c < 64 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) a.dbg[(role * 64 + c) * 8 + ph] = clock64();
+}
+
+template <int FMT, int IC, bool STACK, int NT>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t s_bar[2];   // stage free: committed by the MMA warp
-    __shared__ __align__(8) uint64_t s_full[2];  // stage written: every producer arrives
-    __shared__ __align__(8) uint64_t s_stg[kStg];  // DENSE: grid slab of chunk c landed in staging slot c % kStg
+    __shared__ __align__(8) uint64_t s_wfree[3];  // W stage free: the MMAs of its last chunk completed
+    __shared__ __align__(8) uint64_t s_full[3];   // stage written: every producer arrives
+    __shared__ __align__(8) uint64_t s_afree[2];  // A buffer free: the MMAs of its last chunk completed
+    __shared__ __align__(8) uint64_t s_ring[6];  // DENSE: W tile of chunk c landed in ring slot c % ring
     __shared__ uint32_t s_tmem;
     __shared__ float s_lut[256];
+    constexpr bool kDense = FMT == FMT_DENSE;
+    constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
+    constexpr int S = STACK ? 64 : kGmM;            // samples per tile
+    constexpr int kTPC = kGmP / NT;                 // W: threads per output column
+    constexpr int kEPT = IC / kTPC;                 // W: edges (inputs) per thread and chunk
+    constexpr uint32_t kLboW = (NT / 8) * 128, kLboA = (kGmM / 8) * 128;
+    constexpr int kAU = IC * kGmM / kGmP;           // A slots (row, input) per thread: 1 or 2
+    static_assert(!kDense || NT == kGmN, "dense tiles are 128 outputs wide");
     const DevLayer& L = a.L;
     const int G = L.G, KC = IC * G;
-    const uint32_t tile_a = MT * KC * 4, tile_w = kGmN * KC * 4;
-    const uint32_t stage_bytes = 2 * tile_a + 2 * tile_w;  // [A_hi][A_lo][W_hi][W_lo]
-    constexpr uint32_t kLboA = (MT / 8) * 128, kLboW = (kGmN / 8) * 128;
-    constexpr int kAU = (IC * MT + kGmP - 1) / kGmP;  // A slots per producer (1 or 2)
-    // DENSE: the grid slab of a chunk (IC inputs x 128 columns x G floats) is
-    // bulk-copied into a staging ring behind the two operand stages
-    const bool stg = FMT == FMT_DENSE && a.tma_w;
-    const uint32_t slab = kGmN * static_cast<uint32_t>(G) * 4;  // bytes per input row of the slab
-    unsigned char* s_slab = smem + 2 * stage_bytes;
+    const uint32_t tile_w = NT * KC * 4, tile_a = kGmM * KC * 4;
+    const int ring = kDense ? a.gemm_ring : 1;
+    // smem: two A buffers [A_hi (| A_lo)], then `wst` W stages (compressed:
+    // [W_hi | W_lo]; dense: W_lo), then (dense) the ring slots
+    const int wst = a.gemm_wst;
+    const uint32_t abuf = (STACK ? 1 : 2) * tile_a;
+    unsigned char* s_a = smem;
+    unsigned char* s_w = smem + 2 * abuf;
+    const uint32_t wstage = kDense ? tile_w : 2 * tile_w;
+    unsigned char* s_ringbuf = s_w + wst * wstage;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * MT;
-    const int nS = min(MT, a.B - s0), nJ = min(kGmN, L.out - j0);
+    const int j0 = blockIdx.x * NT, s0 = blockIdx.z * S;
+    const int nS = min(S, a.B - s0), nJ = min(NT, L.out - j0);
     const int r0 = blockIdx.y * a.rows_per_cta, rend = min(L.in, r0 + a.rows_per_cta);
     const int nchunks = rend > r0 ? (rend - r0 + IC - 1) / IC : 0;
     pdl_trigger();
-    if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
+    if constexpr (kI8) {
         if (tid < 256) s_lut[tid] = L.lutf[tid];
     }
-    // the A tiles are sparse (2 of G weights per sample and input): zero both
-    // stages once, then write and clear only the nonzeros
-    for (uint32_t q = tid * 16; q < 2 * stage_bytes; q += kGmT * 16) {
-        const uint32_t st = q / stage_bytes, o = q % stage_bytes;
-        if (o < 2 * tile_a) *reinterpret_cast<uint4*>(smem + st * stage_bytes + o) = make_uint4(0, 0, 0, 0);
-    }
+    // the A tile is sparse: zero it once; each slot owner keeps it clean
+    for (uint32_t q = tid * 16; q < 2 * abuf; q += kGmT * 16)
+        *reinterpret_cast<uint4*>(s_a + q) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar[1])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[0])), "r"(kGmP));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[1])), "r"(kGmP));
-        for (int q = 0; q < kStg; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_stg[q])));
+        for (int q = 0; q < 3; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_wfree[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[q])), "r"(kGmP));
+        }
+        for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_afree[q])));
+        for (int q = 0; q < 6; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_ring[q])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tc::tmem_alloc<kGmN>(&s_tmem);
+    if (warp == 0) tc::tmem_alloc<NT>(&s_tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
-    const uint32_t idesc = tc::idesc_tf32(MT, kGmN);
+    const uint32_t idesc = tc::idesc_tf32(kGmM, NT);
 
-    const int rl = tid & (kGmN - 1), grp = tid >> 7;  // W: output column, knot group 0..3
-    const uint32_t rbase = tc::kmajor_off(rl, 0, kGmN);  // row part of the W offset
-    EdgeRaw er[IC];
-    unsigned evalid = 0;   // edges of the staged chunk inside the layer
-    uint32_t recn[IC], kn[IC];  // I8: records of the chunk after the staged one
+    // W roles: thread (column rl, lane group eg) owns the edges of inputs
+    // il = eg + kTPC * v, v < kEPT, of its column: every edge record and
+    // codebook row is gathered by exactly one thread (consecutive lanes:
+    // the same column's inputs, then the next column)
+    const int rl = tid / kTPC, eg = tid % kTPC;
+    const uint32_t rbase = tc::kmajor_off(rl, 0, NT);
+    // Producer state, double-buffered: while chunk c is written from set
+    // (c & 1), chunk c+1's loads land in the other set (issued at the top of
+    // iteration c, so a whole iteration hides their latency).
+    struct Stage {
+        EdgeRaw er[kDense ? 1 : kEPT];
+        unsigned valid;  // edges of the chunk inside the layer
+        int bm[kAU];     // A slot brackets
+        float bt[kAU];
+        uint32_t aoff[kAU];  // this slot's two nonzero offsets in the A buffer of this parity, or ~0
+    };
+    Stage sa, sb;
+#pragma unroll
+    for (int u = 0; u < kAU; ++u) sa.aoff[u] = sb.aoff[u] = 0xFFFFFFFFu;
+    uint32_t recn[kI8 ? kEPT : 1], kn[kI8 ? kEPT : 1];  // I8: records of the chunk after next
     unsigned nvalid = 0;
-    int bm[kAU];
-    float bt[kAU];
-    uint32_t aoff0[kAU], aoff1[kAU];  // nonzero A offsets written into stage 0 / 1 (cleared on reuse)
+    // A roles: slot u = (row ra = q % 128, input ila = q / 128), q = tid + 512 u
+    const int* bm0[kAU];
+    const float* bt0[kAU];
+    bool aok[kAU];
 #pragma unroll
-    for (int u = 0; u < kAU; ++u) aoff0[u] = aoff1[u] = 0xFFFFFFFFu;
-    constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
+    for (int u = 0; u < kAU; ++u) {
+        const int q = tid + kGmP * u, ra = q % kGmM, ila = q / kGmM;
+        const int smp = STACK ? (ra & 63) : ra;
+        aok[u] = smp < nS;
+        bm0[u] = a.bm_in + static_cast<size_t>(r0 + ila) * a.B + s0 + smp;
+        bt0[u] = a.bt_in + static_cast<size_t>(r0 + ila) * a.B + s0 + smp;
+    }
     const float bs_f = static_cast<float>(L.bs);
-    auto load_recs = [&](int c) {  // I8 records of chunk c
-        const int ib = r0 + c * IC;
-        nvalid = 0;
-#pragma unroll
-        for (int il = 0; il < IC; ++il) {
-            const int i = ib + il;
-            if (rl < nJ && i < rend) {
-                nvalid |= 1u << il;
-                rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, recn[il], kn[il]);
-            }
+    const size_t cbase = static_cast<size_t>(r0 / IC);  // DENSE: first chunk of this split in the tiles
+    auto issue_tile = [&](int c, int slot) {  // DENSE: TMA of chunk c's pre-tiled W into ring slot `slot`
+        if constexpr (kDense) {
+            if (c >= nchunks) return;
+            uint64_t* bar = &s_ring[slot];
+            mbar_expect_tx(bar, tile_w);
+            bulk_g2s(s_ringbuf + slot * tile_w,
+                     L.wt + (static_cast<size_t>(blockIdx.x) * L.wt_nch + cbase + c) * (kGmN * KC), tile_w, bar);
         }
     };
-    auto load_chunk = [&](int c) {  // stage chunk c's edge data and brackets into registers
-        const int ib = r0 + c * IC;
+    auto load_recs = [&](int c) {  // I8 records of chunk c
         if constexpr (kI8) {
-            evalid = nvalid;
+            const int ib = r0 + c * IC;
+            nvalid = 0;
 #pragma unroll
-            for (int il = 0; il < IC; ++il) {
-                if (!(evalid >> il & 1)) continue;
-                const uint32_t r = recn[il];
-                const uint32_t k = FMT == FMT_I8_R32 ? (r & 0xFFFFu) : kn[il];
-                const uint32_t gb = FMT == FMT_I8_R32 ? (r >> 16) : r;  // gain code | bias code << 8
-                er[il].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
-                er[il].g = s_lut[gb & 0xFFu];  // float(gain(code) * codebook scale)
-                er[il].b = static_cast<float>(static_cast<int8_t>((gb >> 8) & 0xFFu)) * bs_f;
-            }
-        } else {
-            evalid = 0;
-#pragma unroll
-            for (int il = 0; il < IC; ++il) {
-                const int i = ib + il;
-                if (!(rl < nJ && i < rend)) continue;
-                evalid |= 1u << il;
-                const size_t e = static_cast<size_t>(i) * L.out + j0 + rl;
-                if constexpr (FMT == FMT_F32) {
-                    er[il].k = L.idx ? __ldg(L.idx + e) : 0u;
-                    er[il].g = __ldg(L.gain + e);
-                    er[il].b = __ldg(L.bias + e);
-                } else if (!stg) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int m = grp + 4 * u;
-                        er[il].v[u] = m < G ? __ldg(L.cb32 + e * static_cast<size_t>(G) + m) : 0.f;
-                    }
+            for (int v = 0; v < kEPT; ++v) {
+                const int i = ib + eg + kTPC * v;
+                if (rl < nJ && i < rend) {
+                    nvalid |= 1u << v;
+                    rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, recn[v], kn[v]);
                 }
             }
         }
+    };
+    // issue chunk c's edge loads (from the records already in registers) and
+    // bracket loads into `st`, and the records of chunk c+1
+    auto load_chunk = [&](Stage& st, int c) {
+        const int ib = r0 + c * IC;
+        if constexpr (kI8) {
+            st.valid = nvalid;
+#pragma unroll
+            for (int v = 0; v < kEPT; ++v) {
+                if (!(st.valid >> v & 1)) continue;
+                const uint32_t r = recn[v];
+                const uint32_t k = FMT == FMT_I8_R32 ? (r & 0xFFFFu) : kn[v];
+                const uint32_t gb = FMT == FMT_I8_R32 ? (r >> 16) : r;  // gain code | bias code << 8
+                st.er[v].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
+                st.er[v].g = s_lut[gb & 0xFFu];  // float(gain(code) * codebook scale)
+                st.er[v].b = static_cast<float>(static_cast<int8_t>((gb >> 8) & 0xFFu)) * bs_f;
+            }
+        } else if constexpr (FMT == FMT_F32) {
+            st.valid = 0;
+#pragma unroll
+            for (int v = 0; v < kEPT; ++v) {
+                const int i = ib + eg + kTPC * v;
+                if (!(rl < nJ && i < rend)) continue;
+                st.valid |= 1u << v;
+                const size_t e = static_cast<size_t>(i) * L.out + j0 + rl;
+                st.er[v].k = L.idx ? __ldg(L.idx + e) : 0u;
+                st.er[v].g = __ldg(L.gain + e);
+                st.er[v].b = __ldg(L.bias + e);
+            }
+        }
+        const size_t step = static_cast<size_t>(c) * IC * a.B;
 #pragma unroll
         for (int u = 0; u < kAU; ++u) {
-            const int q = tid + kGmP * u, ra = q % MT, ila = q / MT, i = ib + ila;
-            bm[u] = -2;
-            bt[u] = 0.f;
-            if (ila < IC && ra < nS && i < rend) {
-                const size_t p = static_cast<size_t>(i) * a.B + s0 + ra;
-                bm[u] = a.bm_in[p];
-                bt[u] = a.bt_in[p];
+            const int ila = (tid + kGmP * u) / kGmM;
+            st.bm[u] = -2;
+            st.bt[u] = 0.f;
+            if (aok[u] && ib + ila < rend) {
+                st.bm[u] = bm0[u][step];
+                st.bt[u] = bt0[u][step];
             }
         }
         if constexpr (kI8) {
             if (c + 1 < nchunks) load_recs(c + 1);
         }
     };
+    int rslot = 0;  // DENSE: ring slot of chunk c (c % ring) and its phase
+    unsigned rphase = 0;
+    int ws = 0;     // W stage of chunk c (c % wst) and the parity of its use count
+    unsigned wph = 0;
+    // producer iteration c: writes chunk c from `cur` (A buffer c & 1) while
+    // chunk c+1 loads into `nxt`
+    auto produce = [&](Stage& cur, Stage& nxt, int c) {
+        const int ab = c & 1;
+        if (tid == 0) gstamp(a, 0, c, 0);
+        if (c + 1 < nchunks && !(a.gemm_skip & 4)) load_chunk(nxt, c + 1);
+        if (c >= wst) {
+            mbar_wait_parity(&s_wfree[ws], wph ^ 1u);
+            if (tid == 0) gstamp(a, 0, c, 1);
+            if constexpr (kDense) {
+                if (tid == 0) {  // chunk c-wst's ring slot is free again
+                    const int s2 = rslot - wst;
+                    issue_tile(c - wst + ring, s2 >= 0 ? s2 : s2 + ring);
+                }
+            }
+        }
+        unsigned char* st = s_w + ws * wstage;
+        if (a.gemm_skip & 1) {
+        } else if constexpr (kDense) {
+            // W_lo = the remainder of the landed tile below its tf32 truncation
+            mbar_wait_parity(&s_ring[rslot], rphase);
+            const float4* src = reinterpret_cast<const float4*>(s_ringbuf + rslot * tile_w);
+            float4* dst = reinterpret_cast<float4*>(st);
+            for (int q = tid; q < static_cast<int>(tile_w / 16); q += kGmP) {
+                const float4 v = src[q];
+                dst[q] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+            }
+        } else {
+            // W: every knot of this thread's edges (hi, lo); k = m * IC + il
+            // sits at byte (k/4) * LBO + rbase + (k%4) * 4 of the K-major tile
+#pragma unroll
+            for (int v = 0; v < kEPT; ++v) {
+                const int il = eg + kTPC * v;
+                const uint32_t ob = rbase + (il >> 2) * kLboW + (il & 3) * 4;
+                const bool ok = cur.valid >> v & 1;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    if (m >= G) break;
+                    const float w = ok ? edge_w<FMT>(L, cur.er[v], m) : 0.f;
+                    const uint32_t o = ob + m * (IC / 4) * kLboW;
+                    *reinterpret_cast<float*>(st + o) = w;
+                    *reinterpret_cast<float*>(st + tile_w + o) = tc::tf32_lo(w);
+                }
+            }
+        }
+        // A: clear this slot's two entries of chunk c-1, write chunk c's
+        if (tid == 0) gstamp(a, 0, c, 2);
+        if (c >= 2) mbar_wait_parity(&s_afree[ab], ((c >> 1) - 1) & 1);
+        if (tid == 0) gstamp(a, 0, c, 3);
+        unsigned char* sab = s_a + ab * abuf;
+#pragma unroll
+        for (int u = 0; u < ((a.gemm_skip & 2) ? 0 : kAU); ++u) {
+            const int q = tid + kGmP * u, ra = q % kGmM, il = q / kGmM;
+            const bool lo_row = STACK && ra >= 64;
+            if (cur.aoff[u] != 0xFFFFFFFFu) {
+                const uint32_t o0 = cur.aoff[u] & 0xFFFFu, o1 = cur.aoff[u] >> 16;
+                *reinterpret_cast<float*>(sab + o0) = 0.f;
+                *reinterpret_cast<float*>(sab + o1) = 0.f;
+                if constexpr (!STACK) {
+                    *reinterpret_cast<float*>(sab + tile_a + o0) = 0.f;
+                    *reinterpret_cast<float*>(sab + tile_a + o1) = 0.f;
+                }
+                cur.aoff[u] = 0xFFFFFFFFu;
+            }
+            if (cur.bm[u] >= 0) {
+                const int k0 = cur.bm[u] * IC + il, k1 = k0 + IC;
+                const uint32_t o0 = tc::kmajor_off(ra, k0, kGmM), o1 = tc::kmajor_off(ra, k1, kGmM);
+                const float w0 = 1.f - cur.bt[u], w1 = cur.bt[u];
+                *reinterpret_cast<float*>(sab + o0) = lo_row ? tc::tf32_lo(w0) : w0;
+                *reinterpret_cast<float*>(sab + o1) = lo_row ? tc::tf32_lo(w1) : w1;
+                if constexpr (!STACK) {
+                    *reinterpret_cast<float*>(sab + tile_a + o0) = tc::tf32_lo(w0);
+                    *reinterpret_cast<float*>(sab + tile_a + o1) = tc::tf32_lo(w1);
+                }
+                cur.aoff[u] = o0 | (o1 << 16);
+            }
+        }
+        tc::fence_proxy_async();  // this thread's smem writes -> the tensor core
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[ws])) : "memory");
+        if (tid == 0) gstamp(a, 0, c, 4);
+        if (++rslot == ring) {
+            rslot = 0;
+            rphase ^= 1u;
+        }
+        if (++ws == wst) {
+            ws = 0;
+            wph ^= 1u;
+        }
+    };
     pdl_wait();  // brackets come from the previous kernel
     __syncthreads();  // s_lut visible
     if (tid < kGmP) {
-        // producers: write stage c as soon as the MMAs of chunk c-2 released it
+        // producers: W of chunk c into stage c % wst once the MMAs of chunk
+        // c - wst released it; A into buffer c & 1 once chunk c-2's did
+        if constexpr (kDense) {
+            if (tid == 0)
+                for (int c = 0; c < ring; ++c) issue_tile(c, c);
+        }
         if (nchunks > 0) {
-            if constexpr (kI8) load_recs(0);
-            load_chunk(0);
+            load_recs(0);
+            load_chunk(sa, 0);
         }
 #pragma unroll 1
-        for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            unsigned char* st = smem + buf * stage_bytes;
-            if (c >= 2) mbar_wait_parity(&s_bar[buf], ((c - 2) >> 1) & 1);
-            const float* slabf = nullptr;
-            if constexpr (FMT == FMT_DENSE) {
-                if (stg) {
-                    mbar_wait_parity(&s_stg[c % kStg], (c / kStg) & 1);
-                    slabf = reinterpret_cast<const float*>(s_slab + (c % kStg) * IC * slab);
-                }
-            }
-            // W: this thread's knots, the IC inputs' values as 16-byte groups
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int m = grp + 4 * u;
-                if (m >= G) break;
-#pragma unroll
-                for (int h = 0; h < IC / 4; ++h) {
-                    float v[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int il = 4 * h + q;
-                        if constexpr (FMT == FMT_DENSE) {
-                            if (stg) {
-                                v[q] = (evalid >> il & 1) ? slabf[(il * kGmN + rl) * G + m] : 0.f;
-                                continue;
-                            }
-                        }
-                        v[q] = (evalid >> il & 1) ? edge_w<FMT>(L, er[il], m, u) : 0.f;
-                    }
-                    const uint32_t o = (m * (IC / 4) + h) * kLboW + rbase;
-                    *reinterpret_cast<float4*>(st + 2 * tile_a + o) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(st + 2 * tile_a + tile_w + o) =
-                        make_float4(tc::tf32_lo(v[0]), tc::tf32_lo(v[1]), tc::tf32_lo(v[2]), tc::tf32_lo(v[3]));
-                }
-            }
-            // A: clear the two weights chunk c-2 left, write this chunk's
-#pragma unroll
-            for (int u = 0; u < kAU; ++u) {
-                const int qa = tid + kGmP * u, ra = qa % MT, il = qa / MT;
-                const uint32_t rbase_a = tc::kmajor_off(ra, 0, MT);
-                uint32_t& ao = buf ? aoff1[u] : aoff0[u];
-                if (ao != 0xFFFFFFFFu) {
-                    const uint32_t o0 = ao & 0xFFFFu, o1 = ao >> 16;
-                    *reinterpret_cast<float*>(st + o0) = 0.f;
-                    *reinterpret_cast<float*>(st + tile_a + o0) = 0.f;
-                    *reinterpret_cast<float*>(st + o1) = 0.f;
-                    *reinterpret_cast<float*>(st + tile_a + o1) = 0.f;
-                    ao = 0xFFFFFFFFu;
-                }
-                if (bm[u] >= 0) {
-                    const int k0 = bm[u] * IC + il, k1 = k0 + IC;
-                    const uint32_t o0 = rbase_a + (k0 >> 2) * kLboA + (k0 & 3) * 4;
-                    const uint32_t o1 = rbase_a + (k1 >> 2) * kLboA + (k1 & 3) * 4;
-                    const float w0 = 1.f - bt[u], w1 = bt[u];
-                    *reinterpret_cast<float*>(st + o0) = w0;
-                    *reinterpret_cast<float*>(st + tile_a + o0) = tc::tf32_lo(w0);
-                    *reinterpret_cast<float*>(st + o1) = w1;
-                    *reinterpret_cast<float*>(st + tile_a + o1) = tc::tf32_lo(w1);
-                    ao = o0 | (o1 << 16);
-                }
-            }
-            if (c + 1 < nchunks) load_chunk(c + 1);  // next chunk's tables fly while this one multiplies
-            tc::fence_proxy_async();                 // this thread's stage writes -> the tensor core
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[buf])) : "memory");
+        for (int c = 0; c < nchunks; c += 2) {
+            produce(sa, sb, c);
+            if (c + 1 < nchunks) produce(sb, sa, c + 1);
         }
     } else {
-        // the MMA warp: one lane issues 3 x (KC/8) tcgen05.mma per chunk, in
-        // order (and, for dense layers, the grid-slab bulk copies kStg chunks ahead)
-        auto issue_slab = [&](int c) {
-            if constexpr (FMT == FMT_DENSE) {
-                if (!stg || c >= nchunks) return;
-                const int ib = r0 + c * IC;
-                const uint32_t bytes = static_cast<uint32_t>(nJ) * G * 4;
-                int nv = 0;
-                for (int il = 0; il < IC; ++il) nv += ib + il < rend;
-                uint64_t* bar = &s_stg[c % kStg];
-                mbar_expect_tx(bar, nv * bytes);
-                unsigned char* dst = s_slab + (c % kStg) * IC * slab;
-                for (int il = 0; il < IC; ++il)
-                    if (ib + il < rend)
-                        bulk_g2s(dst + il * slab, L.cb32 + (static_cast<size_t>(ib + il) * L.out + j0) * G, bytes, bar);
-            }
-        };
-        if (lane == 0)
-            for (int c = 0; c < kStg; ++c) issue_slab(c);
+        // the MMA warp: issues the chunk's tcgen05.mma in order,
+        // warp-uniform (one elected lane issues); descriptors advance by
+        // immediates from per-chunk bases
+        const int nks = KC / 8;
+        const uint64_t da0 = tc::make_desc(tc::smem_addr(s_a), kLboA, 128);
+        constexpr uint64_t kStepA = (2 * kLboA) >> 4, kStepW = (2 * kLboW) >> 4;  // descriptor address units
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            mbar_wait_parity(&s_full[buf], (c >> 1) & 1);
-            if (lane == 0) {
-                issue_slab(c + kStg);  // the producers are done with chunk c's slab
-                tc::fence_after_sync();
-                const uint32_t base = tc::smem_addr(smem + buf * stage_bytes);
-#pragma unroll 1
-                for (int s = 0; s < KC / 8; ++s) {
-                    const uint32_t oa = s * 2 * kLboA, ow = s * 2 * kLboW;
-                    const uint64_t ah = tc::make_desc(base + oa, kLboA, 128);
-                    const uint64_t al = tc::make_desc(base + tile_a + oa, kLboA, 128);
-                    const uint64_t wh = tc::make_desc(base + 2 * tile_a + ow, kLboW, 128);
-                    const uint64_t wl = tc::make_desc(base + 2 * tile_a + tile_w + ow, kLboW, 128);
-                    tc::mma_tf32(tmem, ah, wh, idesc, c > 0 || s > 0);
-                    tc::mma_tf32(tmem, ah, wl, idesc, true);
-                    tc::mma_tf32(tmem, al, wh, idesc, true);
-                }
-                tc::mma_commit(&s_bar[buf]);
+            const int ab = c & 1;
+            mbar_wait_parity(&s_full[ws], wph);
+            if constexpr (kDense) mbar_wait_parity(&s_ring[rslot], rphase);
+            if (lane == 0) gstamp(a, 1, c, 0);
+            tc::fence_after_sync();
+            const uint64_t da = da0 + ab * (abuf >> 4);  // A_hi (STACK: A_hi / A_lo rows); A_lo tile next
+            const uint64_t dwh = tc::make_desc(kDense ? tc::smem_addr(s_ringbuf + rslot * tile_w)
+                                                      : tc::smem_addr(s_w + ws * wstage), kLboW, 128);
+            const uint64_t dwl = kDense ? tc::make_desc(tc::smem_addr(s_w + ws * wstage), kLboW, 128)
+                                        : dwh + (tile_w >> 4);
+            if (lane == 0) gstamp(a, 1, c, 1);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                if (s >= nks) break;
+                tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dwh + s * kStepW, idesc, (c | s) != 0);
+                tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dwl + s * kStepW, idesc, 1u);
+                if constexpr (!STACK)
+                    tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dwh + s * kStepW, idesc, 1u);
             }
-            __syncwarp();
+            tc::mma_commit_warp(&s_afree[ab]);
+            tc::mma_commit_warp(&s_wfree[ws]);
+            if (lane == 0) gstamp(a, 1, c, 2);
+            if (++rslot == ring) {
+                rslot = 0;
+                rphase ^= 1u;
+            }
+            if (++ws == wst) {
+                ws = 0;
+                wph ^= 1u;
+            }
         }
     }
-    if (nchunks > 0) mbar_wait_parity(&s_bar[(nchunks - 1) & 1], ((nchunks - 1) >> 1) & 1);
+    if (nchunks > 0) mbar_wait_parity(&s_wfree[(nchunks - 1) % wst], ((nchunks - 1) / wst) & 1);
     tc::fence_after_sync();
-    // epilogue: producer warp w reads TMEM lanes (w%4)*32.. (its samples), columns (w/4)*32..+32
-    const int q4 = warp & 3, cq = warp >> 2;
+    // epilogue: producer warp w reads TMEM lanes (w%4)*32.. and columns
+    // (w/4)*NT/4..+NT/4.  STACK: lanes 64-127 (A_lo rows) go to their own
+    // partial plane, summed with the A_hi plane by the split reduction.
     if (warp < kGmP / 32) {
-    // M = 128: sample r in TMEM lane r; M = 64: sample r in lane (r/16)*32 + r%16
-    const int row = MT == 128 ? q4 * 32 + lane : (lane < 16 ? q4 * 16 + lane : MT);
-    const size_t plane = static_cast<size_t>(a.B) * L.out;
-    float* dst = a.partial + blockIdx.y * plane + static_cast<size_t>(s0 + min(row, MT - 1)) * L.out + j0;
+        const int q4 = warp & 3, cq = warp >> 2;
+        const int as = STACK ? (q4 & 1) * 32 + lane : q4 * 32 + lane;
+        const size_t plane = static_cast<size_t>(a.B) * L.out;
+        const int pz = STACK ? 2 * blockIdx.y + (q4 >> 1) : blockIdx.y;
+        float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
 #pragma unroll 1
-    for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
-        float v[8];
-        if (nchunks > 0) {
-            tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
-        } else {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = 0.f;
-        }
-        if (row < nS) {
-            if (c8 + 8 <= nJ && (L.out & 3) == 0) {
-                *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
-                *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        for (int c8 = cq * (NT / 4); c8 < (cq + 1) * (NT / 4); c8 += 8) {
+            float v[8];
+            if (nchunks > 0) {
+                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
             } else {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (c8 + u < nJ) dst[c8 + u] = v[u];
+                for (int u = 0; u < 8; ++u) v[u] = 0.f;
+            }
+            if (as < nS) {
+                if (c8 + 8 <= nJ && (L.out & 3) == 0) {
+                    *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (c8 + u < nJ) dst[c8 + u] = v[u];
+                }
             }
         }
-    }
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_free<kGmN>(tmem);
+    if (warp == 0) tc::tmem_free<NT>(tmem);
+}
+
+// Pre-tiled copy of a dense grid for the layer GEMM (built once at upload):
+// tile (jt, ch) = the chunk's KC x 128 W block in exactly the shared-memory
+// byte layout above, zero-padded past `out` and `in`, tiles of one output
+// block consecutive along the inputs (one TMA bulk copy per chunk).
+__global__ void k_dense_tiles(const float* __restrict__ cb32, float* __restrict__ wt, int in, int out, int G,
+                              int IC, int nch, size_t total) {
+    const int KC = IC * G;
+    const size_t per = static_cast<size_t>(kGmN) * KC;
+    for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < total;
+         q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t tile = q / per;
+        const int f = static_cast<int>(q % per);
+        const int jt = static_cast<int>(tile / nch), ch = static_cast<int>(tile % nch);
+        // invert kmajor_off(r, k, 128) / 4 = (k/4)*512 + (r/8)*32 + (r%8)*4 + k%4
+        const int k = (f >> 9) * 4 + (f & 3), r = ((f >> 5) & 15) * 8 + ((f >> 2) & 7);
+        const int m = k / IC, i = ch * IC + k % IC, j = jt * kGmN + r;
+        wt[q] = (i < in && j < out) ? cb32[(static_cast<size_t>(i) * out + j) * G + m] : 0.f;
+    }
 }
 
 __device__ __forceinline__ void reduce_finish(const FwdArgs& a, size_t p, double v, int add_bias) {
@@ -554,25 +702,60 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStre
 // a multiple of 4 (16-byte W groups): 4 for even G, 8 for odd G.
 int gemm_ic(int G) { return G % 2 == 0 ? 4 : 8; }
 
-size_t gemm_smem(int G, bool dense, int mt = kGmM) {
-    const size_t kc = static_cast<size_t>(gemm_ic(G)) * G;
-    return 2 * (2 * static_cast<size_t>(mt) * kc * 4 + 2 * kGmN * kc * 4) + (dense ? kStg * kc * kGmN * 4 : 0);
+// Shared-memory plan of one configuration: two A buffers, `wst` W stages
+// (3 where they fit, so the producers run two chunks ahead of the tensor
+// core), and for dense layers the TMA ring (>= wst + 1 slots, up to 6).
+struct GemmPlan {
+    int wst, ring;
+    size_t smem;
+};
+constexpr size_t kGemmSmemLimit = 220 * 1024;
+
+bool gemm_plan(int G, int fmt, bool stack, int nt, GemmPlan* out) {
+    const int kc = gemm_ic(G) * G;
+    const size_t tile_a = static_cast<size_t>(kGmM) * kc * 4, tile_w = static_cast<size_t>(nt) * kc * 4;
+    const size_t abuf = (stack ? 1 : 2) * tile_a, wstage = (fmt == FMT_DENSE ? 1 : 2) * tile_w;
+    for (int wst = 3; wst >= 2; --wst) {
+        size_t smem = 2 * abuf + wst * wstage;
+        int ring = 0;
+        if (fmt == FMT_DENSE) {
+            if (nt != kGmN || smem >= kGemmSmemLimit) continue;
+            ring = static_cast<int>(std::min<size_t>(6, (kGemmSmemLimit - smem) / tile_w));
+            if (ring < wst + 1) continue;
+            smem += ring * tile_w;
+        }
+        if (smem > kGemmSmemLimit) continue;
+        if (out) *out = GemmPlan{wst, ring, smem};
+        return true;
+    }
+    return false;
 }
 
 bool gemm_supported(const DevLayer& L) {
-    const int ic = gemm_ic(L.G);
-    return ic > 0 && L.G <= 16 && gemm_smem(L.G, L.fmt == FMT_DENSE) <= 222 * 1024 &&
-           (L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32 || L.fmt == FMT_DENSE);
+    if (L.G > 16 || !gemm_plan(L.G, L.fmt, false, kGmN, nullptr) || !gemm_plan(L.G, L.fmt, true, kGmN, nullptr))
+        return false;
+    if (L.fmt == FMT_DENSE) return L.wt != nullptr;
+    return L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32;
 }
 
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     LaunchCfg c{};
     c.kind = 4;
     c.ic = gemm_ic(L.G);
-    c.jt = (L.out + kGmN - 1) / kGmN;
-    c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: the M = 64 MMA when the batch fits it
+    c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: 64 = A_hi / A_lo stacked in the 128 rows
+    const bool stack = c.spt == 64;
+    static const int nt_env = [] {
+        const char* e = std::getenv("SKAN_GEMM_NT");  // experiment override: 256
+        return e ? std::atoi(e) : 0;
+    }();
+    // outputs per tile: 128 (three W stages fit); 256 only as an experiment
+    c.tj = (nt_env == 256 && L.fmt != FMT_DENSE && gemm_plan(L.G, L.fmt, stack, 256, nullptr)) ? 256 : kGmN;
+    GemmPlan gp{};
+    gemm_plan(L.G, L.fmt, stack, c.tj, &gp);
+    c.vj = gp.wst;
+    c.rw = gp.ring;
+    c.jt = (L.out + c.tj - 1) / c.tj;
     c.st = (B + c.spt - 1) / c.spt;
-    c.tj = kGmN;
     const int sms = num_sms > 0 ? num_sms : 148;
     // one CTA per SM: the fewest input splits whose waves are >= 90% full
     const long long base = static_cast<long long>(c.jt) * c.st;
@@ -591,30 +774,50 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     const int chunks = (L.in + c.ic - 1) / c.ic;
     const int per = (chunks + static_cast<int>(ns) - 1) / static_cast<int>(ns);
     c.ichunk = per * c.ic;
-    c.nsplit = (L.in + c.ichunk - 1) / c.ichunk;
-    c.smem = gemm_smem(L.G, L.fmt == FMT_DENSE, c.spt);
+    // partial planes: one per input split, two when A_hi / A_lo are stacked
+    c.nsplit = (L.in + c.ichunk - 1) / c.ichunk * (stack ? 2 : 1);
+    c.smem = gp.smem;
     return c;
 }
 
-template <int MT>
+template <bool STACK, int NT>
 void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
     const bool i4 = ic == 4;
     switch (fmt) {
-        case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, MT> : k_layer_gemm<FMT_I8_R32, 8, MT>;
-        case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, MT> : k_layer_gemm<FMT_I8_WIDE, 8, MT>;
-        case FMT_F32: return i4 ? k_layer_gemm<FMT_F32, 4, MT> : k_layer_gemm<FMT_F32, 8, MT>;
-        default: return i4 ? k_layer_gemm<FMT_DENSE, 4, MT> : k_layer_gemm<FMT_DENSE, 8, MT>;
+        case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, STACK, NT> : k_layer_gemm<FMT_I8_R32, 8, STACK, NT>;
+        case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, STACK, NT> : k_layer_gemm<FMT_I8_WIDE, 8, STACK, NT>;
+        default: return i4 ? k_layer_gemm<FMT_F32, 4, STACK, NT> : k_layer_gemm<FMT_F32, 8, STACK, NT>;
     }
 }
 
-void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
-    void (*k)(FwdArgs) = c.spt == 64 ? gemm_kernel<64>(a.L.fmt, c.ic) : gemm_kernel<128>(a.L.fmt, c.ic);
+template <bool STACK>
+void (*gemm_kernel_dense(int ic))(FwdArgs) {
+    return ic == 4 ? k_layer_gemm<FMT_DENSE, 4, STACK, kGmN> : k_layer_gemm<FMT_DENSE, 8, STACK, kGmN>;
+}
+
+unsigned long long* g_gemm_dbg = nullptr;
+
+void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    FwdArgs a = a0;
+    a.dbg = g_gemm_dbg;
+    a.gemm_wst = c.vj;
+    a.gemm_ring = c.rw;
+    static const int skip_env = [] {
+        const char* e = std::getenv("SKAN_GEMM_SKIP");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.gemm_skip = skip_env;
+    const bool stack = c.spt == 64;
+    void (*k)(FwdArgs);
+    if (a.L.fmt == FMT_DENSE)
+        k = stack ? gemm_kernel_dense<true>(c.ic) : gemm_kernel_dense<false>(c.ic);
+    else if (c.tj == 256)
+        k = stack ? gemm_kernel<true, 256>(a.L.fmt, c.ic) : gemm_kernel<false, 256>(a.L.fmt, c.ic);
+    else
+        k = stack ? gemm_kernel<true, kGmN>(a.L.fmt, c.ic) : gemm_kernel<false, kGmN>(a.L.fmt, c.ic);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
-    FwdArgs g = a;
-    // dense slabs by TMA when every slab row is 16-byte aligned
-    g.tma_w = a.L.fmt == FMT_DENSE && (static_cast<long long>(a.L.out) * a.L.G) % 4 == 0 &&
-              (reinterpret_cast<uintptr_t>(a.L.cb32) & 15) == 0;
-    launch_pdl(k, dim3(c.jt, c.nsplit, c.st), dim3(kGmT), c.smem, pdl, s, g);
+    const int splits = (a.L.in + c.ichunk - 1) / c.ichunk;
+    launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
@@ -626,4 +829,24 @@ void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStrea
     }
 }
 
+// Dense layers keep a GEMM-tiled copy of their grid (DevLayer::wt) next to
+// the natural one: number of floats, and the device-side build.
+uint64_t dense_tile_floats(int in, int out, int G) {
+    const int ic = gemm_ic(G);
+    return static_cast<uint64_t>((out + kGmN - 1) / kGmN) * ((in + ic - 1) / ic) * kGmN * ic * G;
+}
+
+void build_dense_tiles(const DevLayer& L, float* wt, cudaStream_t s) {
+    const int ic = gemm_ic(L.G);
+    const int nch = (L.in + ic - 1) / ic;
+    const uint64_t total = dense_tile_floats(L.in, L.out, L.G);
+    const int blocks = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
+    k_dense_tiles<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L.cb32, wt, L.in, L.out, L.G, ic, nch, total);
+}
+
 }  // namespace skan
+
+extern "C" skan_status skan_debug_gemm_timeline(unsigned long long* d_stamps) {
+    skan::g_gemm_dbg = d_stamps;
+    return SKAN_OK;
+}

@@ -81,6 +81,11 @@ struct DevLayer {
     //   float(gain(code) * cs) ~= exp2(g_base + code * g_step), code 127 -> 0
     // with g_base = log_min + log2(cs) (dequantize_gain_code, quant.cpp:88-91)
     float g_base, g_step;
+    // dense layers: the grid again, pre-tiled in the layer GEMM's shared-memory
+    // layout (one TMA bulk copy per chunk, skan_gemm.cu); wt_nch = chunks per
+    // output block
+    const float* wt;
+    int wt_nch;
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -93,8 +98,8 @@ struct LaunchCfg {
     int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes
                  // (large batch), 2 = pair planes in shared memory (batch 1), 4 = tensor-core
                  // GEMM over the knot basis (large batch, wide layers; skan_gemm.cu)
-    int vj;      // outputs per lane (small kernel)
-    int rw;      // rows per warp (small kernel)
+    int vj;      // outputs per lane (small kernel); GEMM: W stages
+    int rw;      // rows per warp (small kernel); GEMM: dense TMA ring slots
     int ic;      // inputs per staged chunk (large kernel)
     size_t smem; // dynamic shared memory bytes (large kernel)
 };
@@ -125,7 +130,10 @@ struct FwdArgs {
     const float* prev_partial;    // [prev_nsplit][B][in]
     int prev_nsplit;
     const double* prev_bias_sum;  // [in]
-    int tma_w;                    // layer GEMM: dense grid slabs arrive by TMA bulk copy
+    unsigned long long* dbg;      // layer GEMM phase stamps (skan_debug_gemm_timeline), or null
+    int gemm_wst;                 // layer GEMM: W stages in shared memory (2 or 3)
+    int gemm_ring;                // layer GEMM, dense: TMA ring slots
+    int gemm_skip;                // experiment (SKAN_GEMM_SKIP): 1 = producers skip W, 2 = skip A, 3 = both
 };
 
 // Batch-1 persistent head kernel (skan_head_b1.cu).
@@ -190,6 +198,9 @@ void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint3
 constexpr int kGemmMinBatch = 64;  // smallest batch routed to the tensor-core layer GEMM
 bool gemm_supported(const DevLayer& L);
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms);
+int gemm_ic(int G);
+uint64_t dense_tile_floats(int in, int out, int G);
+void build_dense_tiles(const DevLayer& L, float* wt, cudaStream_t s);
 void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);
 
 // Record a thread-local error for skan_last_error and return its status.

@@ -10,8 +10,13 @@ from paper_2512_15742_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("ts", [0, 200, 300], ids=["smem_a", "tmem_a", "tmem_a_cp"])
 @pytest.mark.parametrize("n,k", [(16, 8), (64, 32), (256, 64), (208, 40)])
-def test_tf32x3_gemm_matches_f64(n, k):
+def test_tf32x3_gemm_matches_f64(n, k, ts):
+    """ts = 200: A written to TMEM with tcgen05.st and read by the MMA from
+    there; ts = 300: A staged in shared memory and moved to TMEM by
+    tcgen05.cp (the layer GEMM's form).  The tensor core truncates a TMEM
+    operand to tf32 the same way, so the lo terms still carry the rest."""
     import torch
     rng = np.random.default_rng(n + k)
     a = rng.standard_normal((128, k)).astype(np.float32)
@@ -22,7 +27,7 @@ def test_tf32x3_gemm_matches_f64(n, k):
     out = {}
     for passes in (1, 3):
         dd = torch.zeros((128, n), dtype=torch.float32, device="cuda")
-        _lib.check(_lib.lib().skan_debug_gemm_tf32(da.data_ptr(), db.data_ptr(), dd.data_ptr(), n, k, passes,
+        _lib.check(_lib.lib().skan_debug_gemm_tf32(da.data_ptr(), db.data_ptr(), dd.data_ptr(), n, k, passes + ts,
                                                    torch.cuda.current_stream().cuda_stream))
         torch.cuda.synchronize()
         out[passes] = np.max(np.abs(dd.cpu().numpy() - want) / scale)
