@@ -106,7 +106,7 @@ int device_format(const skan_layer_header& h) {
 // grid pre-tiled in its shared-memory layout (DevLayer::wt): the GEMM then
 // streams each chunk with one TMA bulk copy.  Built on the device at upload.
 bool dense_tiled(const skan_layer_header& h) {
-    return h.k == 0 && h.out_dim >= 128 && h.grid_size >= 2 && h.grid_size <= 16 &&
+    return h.k == 0 && h.out_dim >= 16 && h.grid_size >= 2 && h.grid_size <= 16 &&
            skan::gemm_ic(static_cast<int>(h.grid_size)) * static_cast<int>(h.grid_size) <= 88;
 }
 

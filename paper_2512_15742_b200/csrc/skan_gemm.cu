@@ -228,75 +228,79 @@ __device__ __forceinline__ float edge_w(const DevLayer& L, const EdgeRaw& r, int
     }
 }
 
-// Chunk K order: k = m * IC + il (knot-major), so the IC inputs of one
-// edge column at one knot are contiguous 4-float groups of the K-major W
-// tile (16-byte stores).  IC is 4 (G even) or 8 (G odd).
+// Chunk K order: k = m * IC + il (knot-major).  IC is 4 (G even) or 8
+// (G odd), so a chunk is KC = IC * G columns, a multiple of the MMA K (8).
 //
 // Operands of one chunk (both from shared memory, canonical K-major):
 //   A (hat weights, 128 rows x KC), written SPARSELY: 2 nonzeros per sample
 //     and input; the thread that owns a (row, input) slot clears its two
 //     entries of the chunk that last used the buffer and writes the new
 //     ones.  STACK (batch <= 64): rows 0-63 = A_hi of samples 0-63, rows
-//     64-127 = their A_lo, so one M = 128 MMA does both; else rows = 128
-//     samples and A_hi, A_lo are two tiles.  Two buffers.
-//   W (KC x NT outputs), hi (raw f32: the tensor core truncates) and lo
-//     planes, `wst` stages.  Compressed layers: decoded by the producers
-//     from the records + codebook; dense layers (NT = 128): the resident
-//     pre-tiled grid (DevLayer::wt, the same byte layout) arrives by TMA
-//     bulk copy into a ring of slots and the producers only derive the lo
-//     plane.
-// MMAs per K = 8 step: STACK 2 (A.W_hi, A.W_lo), else 3 (A_hi.W_hi,
-// A_hi.W_lo, A_lo.W_hi).  (Measured alternatives, tools/mb_mma.cu: A in
+//     64-127 = their A_lo; else rows = 128 samples and A_hi, A_lo are two
+//     tiles.  Two buffers.
+//   W (KC x 256 "outputs"): rows 0-127 the 128 outputs' W_hi (raw f32: the
+//     tensor core truncates to tf32), rows 128-255 their W_lo, so ONE
+//     N = 256 MMA multiplies A by both planes (the N = 256 step costs ~0.78
+//     of two N = 128 steps, tools/mb_mma.cu).  `wst` stages.  Compressed
+//     layers: decoded by the producers from the records + codebook; dense
+//     layers: the resident pre-tiled grid (DevLayer::wt, 128-output tiles)
+//     arrives by TMA bulk copy in a ring of slots the producers release as
+//     soon as they copied it into a stage next to its lo plane.
+// MMAs per K = 8 step: STACK 1 (A x [W_hi | W_lo]); else 2 (A_hi x [W_hi |
+// W_lo], A_lo x W_hi into columns 0-127).  The epilogue adds the two
+// 128-column halves of the accumulator (and STACK: the A_lo rows' partial
+// plane is summed by the split reduction).  (Measured alternatives: A in
 // TMEM runs the MMA ~1.6x faster, but filling TMEM costs more than it
 // saves: tcgen05.cp moves ~40 B/clk, and tcgen05.st needs every hat
 // weight, zeros included, computed in registers.)
+
 // Debug phase stamps (skan_debug_gemm_timeline): CTA (0,0,0) only, role 0 =
 // producer thread 0 (phases: 0 top, 1 W stage free, 2 W written, 3 A tile
-// free, 4 arrived), role 1 = the MMA thread (0 stage full, 1 descriptors ready,
-// 2 MMAs issued).
+// free, 4 arrived), role 1 = the MMA thread (0 stage full, 1 descriptors
+// ready, 2 MMAs issued).
 __device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph) {
     if (a.dbg && c < 64 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) a.dbg[(role * 64 + c) * 8 + ph] = clock64();
 }
 
-template <int FMT, int IC, bool STACK, int NT>
+template <int FMT, int IC, bool STACK>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_wfree[3];  // W stage free: the MMAs of its last chunk completed
     __shared__ __align__(8) uint64_t s_full[3];   // stage written: every producer arrives
     __shared__ __align__(8) uint64_t s_afree[2];  // A buffer free: the MMAs of its last chunk completed
-    __shared__ __align__(8) uint64_t s_ring[6];  // DENSE: W tile of chunk c landed in ring slot c % ring
+    __shared__ __align__(8) uint64_t s_ring[6];   // DENSE: W tile of chunk c landed in ring slot c % ring
     __shared__ uint32_t s_tmem;
     __shared__ float s_lut[256];
     constexpr bool kDense = FMT == FMT_DENSE;
     constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
     constexpr int S = STACK ? 64 : kGmM;            // samples per tile
-    constexpr int kTPC = kGmP / NT;                 // W: threads per output column
+    constexpr int kTPC = kGmP / kGmN;               // W: threads per output column (4)
     constexpr int kEPT = IC / kTPC;                 // W: edges (inputs) per thread and chunk
-    constexpr uint32_t kLboW = (NT / 8) * 128, kLboA = (kGmM / 8) * 128;
+    constexpr uint32_t kLboW = (2 * kGmN / 8) * 128, kLboA = (kGmM / 8) * 128;
+    constexpr uint32_t kLoRows = (kGmN / 8) * 128;  // byte offset of the lo rows inside a K group
     constexpr int kAU = IC * kGmM / kGmP;           // A slots (row, input) per thread: 1 or 2
-    static_assert(!kDense || NT == kGmN, "dense tiles are 128 outputs wide");
     const DevLayer& L = a.L;
     const int G = L.G, KC = IC * G;
-    const uint32_t tile_w = NT * KC * 4, tile_a = kGmM * KC * 4;
-    const int ring = kDense ? a.gemm_ring : 1;
-    // smem: two A buffers [A_hi (| A_lo)], then `wst` W stages (compressed:
-    // [W_hi | W_lo]; dense: W_lo), then (dense) the ring slots
+    const uint32_t tile_t = kGmN * KC * 4;          // one 128-output plane (a dense tile)
+    const uint32_t tile_a = kGmM * KC * 4;
     const int wst = a.gemm_wst;
-    const uint32_t abuf = (STACK ? 1 : 2) * tile_a;
+    const int ring = kDense ? a.gemm_ring : 1;
+    // smem: two A buffers [A_hi (| A_lo)], `wst` W stages (2 planes each),
+    // then (dense) the ring slots
+    const uint32_t abuf = (STACK ? 1 : 2) * tile_a, wstage = 2 * tile_t;
     unsigned char* s_a = smem;
     unsigned char* s_w = smem + 2 * abuf;
-    const uint32_t wstage = kDense ? tile_w : 2 * tile_w;
     unsigned char* s_ringbuf = s_w + wst * wstage;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int j0 = blockIdx.x * NT, s0 = blockIdx.z * S;
-    const int nS = min(S, a.B - s0), nJ = min(NT, L.out - j0);
+    const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * S;
+    const int nS = min(S, a.B - s0), nJ = min(kGmN, L.out - j0);
     const int r0 = blockIdx.y * a.rows_per_cta, rend = min(L.in, r0 + a.rows_per_cta);
     const int nchunks = rend > r0 ? (rend - r0 + IC - 1) / IC : 0;
     pdl_trigger();
     if constexpr (kI8) {
         if (tid < 256) s_lut[tid] = L.lutf[tid];
     }
-    // the A tile is sparse: zero it once; each slot owner keeps it clean
+    // the A tiles are sparse: zero them once; each slot owner keeps them clean
     for (uint32_t q = tid * 16; q < 2 * abuf; q += kGmT * 16)
         *reinterpret_cast<uint4*>(s_a + q) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
@@ -308,26 +312,25 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         for (int q = 0; q < 6; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_ring[q])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tc::tmem_alloc<NT>(&s_tmem);
+    if (warp == 0) tc::tmem_alloc<2 * kGmN>(&s_tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
-    const uint32_t idesc = tc::idesc_tf32(kGmM, NT);
 
     // W roles: thread (column rl, lane group eg) owns the edges of inputs
     // il = eg + kTPC * v, v < kEPT, of its column: every edge record and
     // codebook row is gathered by exactly one thread (consecutive lanes:
     // the same column's inputs, then the next column)
     const int rl = tid / kTPC, eg = tid % kTPC;
-    const uint32_t rbase = tc::kmajor_off(rl, 0, NT);
+    const uint32_t rbase = tc::kmajor_off(rl, 0, 2 * kGmN);
     // Producer state, double-buffered: while chunk c is written from set
     // (c & 1), chunk c+1's loads land in the other set (issued at the top of
     // iteration c, so a whole iteration hides their latency).
     struct Stage {
         EdgeRaw er[kDense ? 1 : kEPT];
-        unsigned valid;  // edges of the chunk inside the layer
-        int bm[kAU];     // A slot brackets
+        unsigned valid;      // edges of the chunk inside the layer
+        int bm[kAU];         // A slot brackets
         float bt[kAU];
         uint32_t aoff[kAU];  // this slot's two nonzero offsets in the A buffer of this parity, or ~0
     };
@@ -354,9 +357,9 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         if constexpr (kDense) {
             if (c >= nchunks) return;
             uint64_t* bar = &s_ring[slot];
-            mbar_expect_tx(bar, tile_w);
-            bulk_g2s(s_ringbuf + slot * tile_w,
-                     L.wt + (static_cast<size_t>(blockIdx.x) * L.wt_nch + cbase + c) * (kGmN * KC), tile_w, bar);
+            mbar_expect_tx(bar, tile_t);
+            bulk_g2s(s_ringbuf + slot * tile_t,
+                     L.wt + (static_cast<size_t>(blockIdx.x) * L.wt_nch + cbase + c) * (kGmN * KC), tile_t, bar);
         }
     };
     auto load_recs = [&](int c) {  // I8 records of chunk c
@@ -426,31 +429,36 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     auto produce = [&](Stage& cur, Stage& nxt, int c) {
         const int ab = c & 1;
         if (tid == 0) gstamp(a, 0, c, 0);
-        if (c + 1 < nchunks && !(a.gemm_skip & 4)) load_chunk(nxt, c + 1);
+        if constexpr (kDense) {
+            // ring slot of chunk c-1 was copied out by every producer (they
+            // all arrived for chunk c-1): refill it with chunk c-1+ring
+            if (tid == 0 && c >= 1) {
+                const int pws = ws > 0 ? ws - 1 : wst - 1;
+                mbar_wait_parity(&s_full[pws], ws > 0 ? wph : wph ^ 1u);
+                issue_tile(c - 1 + ring, rslot > 0 ? rslot - 1 : ring - 1);
+            }
+        }
+        if (c + 1 < nchunks) load_chunk(nxt, c + 1);
         if (c >= wst) {
             mbar_wait_parity(&s_wfree[ws], wph ^ 1u);
             if (tid == 0) gstamp(a, 0, c, 1);
-            if constexpr (kDense) {
-                if (tid == 0) {  // chunk c-wst's ring slot is free again
-                    const int s2 = rslot - wst;
-                    issue_tile(c - wst + ring, s2 >= 0 ? s2 : s2 + ring);
-                }
-            }
         }
         unsigned char* st = s_w + ws * wstage;
-        if (a.gemm_skip & 1) {
-        } else if constexpr (kDense) {
-            // W_lo = the remainder of the landed tile below its tf32 truncation
+        if constexpr (kDense) {
+            // the landed 128-output tile (K groups of 2 KB) -> the hi rows of
+            // each 4 KB K group of the stage, its tf32 remainder -> the lo rows
             mbar_wait_parity(&s_ring[rslot], rphase);
-            const float4* src = reinterpret_cast<const float4*>(s_ringbuf + rslot * tile_w);
-            float4* dst = reinterpret_cast<float4*>(st);
-            for (int q = tid; q < static_cast<int>(tile_w / 16); q += kGmP) {
+            const float4* src = reinterpret_cast<const float4*>(s_ringbuf + rslot * tile_t);
+            for (int q = tid; q < static_cast<int>(tile_t / 16); q += kGmP) {
                 const float4 v = src[q];
-                dst[q] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+                const uint32_t o = (q >> 7) * kLboW + (q & 127) * 16;
+                *reinterpret_cast<float4*>(st + o) = v;
+                *reinterpret_cast<float4*>(st + o + kLoRows) =
+                    make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
             }
         } else {
-            // W: every knot of this thread's edges (hi, lo); k = m * IC + il
-            // sits at byte (k/4) * LBO + rbase + (k%4) * 4 of the K-major tile
+            // W: every knot of this thread's edges (hi row rl, lo row 128 + rl);
+            // k = m * IC + il sits at byte (k/4) * LBO + row part + (k%4) * 4
 #pragma unroll
             for (int v = 0; v < kEPT; ++v) {
                 const int il = eg + kTPC * v;
@@ -462,17 +470,17 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                     const float w = ok ? edge_w<FMT>(L, cur.er[v], m) : 0.f;
                     const uint32_t o = ob + m * (IC / 4) * kLboW;
                     *reinterpret_cast<float*>(st + o) = w;
-                    *reinterpret_cast<float*>(st + tile_w + o) = tc::tf32_lo(w);
+                    *reinterpret_cast<float*>(st + o + kLoRows) = tc::tf32_lo(w);
                 }
             }
         }
-        // A: clear this slot's two entries of chunk c-1, write chunk c's
+        // A: clear this slot's two entries of chunk c-2, write chunk c's
         if (tid == 0) gstamp(a, 0, c, 2);
         if (c >= 2) mbar_wait_parity(&s_afree[ab], ((c >> 1) - 1) & 1);
         if (tid == 0) gstamp(a, 0, c, 3);
         unsigned char* sab = s_a + ab * abuf;
 #pragma unroll
-        for (int u = 0; u < ((a.gemm_skip & 2) ? 0 : kAU); ++u) {
+        for (int u = 0; u < kAU; ++u) {
             const int q = tid + kGmP * u, ra = q % kGmM, il = q / kGmM;
             const bool lo_row = STACK && ra >= 64;
             if (cur.aoff[u] != 0xFFFFFFFFu) {
@@ -534,35 +542,28 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         // immediates from per-chunk bases
         const int nks = KC / 8;
         const uint64_t da0 = tc::make_desc(tc::smem_addr(s_a), kLboA, 128);
+        const uint64_t dw0 = tc::make_desc(tc::smem_addr(s_w), kLboW, 128);
         constexpr uint64_t kStepA = (2 * kLboA) >> 4, kStepW = (2 * kLboW) >> 4;  // descriptor address units
+        const uint32_t idesc2 = tc::idesc_tf32(kGmM, 2 * kGmN), idesc1 = tc::idesc_tf32(kGmM, kGmN);
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
             const int ab = c & 1;
             mbar_wait_parity(&s_full[ws], wph);
-            if constexpr (kDense) mbar_wait_parity(&s_ring[rslot], rphase);
             if (lane == 0) gstamp(a, 1, c, 0);
             tc::fence_after_sync();
             const uint64_t da = da0 + ab * (abuf >> 4);  // A_hi (STACK: A_hi / A_lo rows); A_lo tile next
-            const uint64_t dwh = tc::make_desc(kDense ? tc::smem_addr(s_ringbuf + rslot * tile_w)
-                                                      : tc::smem_addr(s_w + ws * wstage), kLboW, 128);
-            const uint64_t dwl = kDense ? tc::make_desc(tc::smem_addr(s_w + ws * wstage), kLboW, 128)
-                                        : dwh + (tile_w >> 4);
+            const uint64_t dw = dw0 + ws * (wstage >> 4);
             if (lane == 0) gstamp(a, 1, c, 1);
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 if (s >= nks) break;
-                tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dwh + s * kStepW, idesc, (c | s) != 0);
-                tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dwl + s * kStepW, idesc, 1u);
+                tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
                 if constexpr (!STACK)
-                    tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dwh + s * kStepW, idesc, 1u);
+                    tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
             }
             tc::mma_commit_warp(&s_afree[ab]);
             tc::mma_commit_warp(&s_wfree[ws]);
             if (lane == 0) gstamp(a, 1, c, 2);
-            if (++rslot == ring) {
-                rslot = 0;
-                rphase ^= 1u;
-            }
             if (++ws == wst) {
                 ws = 0;
                 wph ^= 1u;
@@ -572,8 +573,9 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     if (nchunks > 0) mbar_wait_parity(&s_wfree[(nchunks - 1) % wst], ((nchunks - 1) / wst) & 1);
     tc::fence_after_sync();
     // epilogue: producer warp w reads TMEM lanes (w%4)*32.. and columns
-    // (w/4)*NT/4..+NT/4.  STACK: lanes 64-127 (A_lo rows) go to their own
-    // partial plane, summed with the A_hi plane by the split reduction.
+    // (w/4)*32..+32 of both halves (W_hi and W_lo products) and adds them.
+    // STACK: lanes 64-127 (A_lo rows) go to their own partial plane, summed
+    // with the A_hi plane by the split reduction.
     if (warp < kGmP / 32) {
         const int q4 = warp & 3, cq = warp >> 2;
         const int as = STACK ? (q4 & 1) * 32 + lane : q4 * 32 + lane;
@@ -581,10 +583,13 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         const int pz = STACK ? 2 * blockIdx.y + (q4 >> 1) : blockIdx.y;
         float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
 #pragma unroll 1
-        for (int c8 = cq * (NT / 4); c8 < (cq + 1) * (NT / 4); c8 += 8) {
-            float v[8];
+        for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+            float v[8], w[8];
             if (nchunks > 0) {
                 tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] += w[u];
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) v[u] = 0.f;
@@ -603,7 +608,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_free<NT>(tmem);
+    if (warp == 0) tc::tmem_free<2 * kGmN>(tmem);
 }
 
 // Pre-tiled copy of a dense grid for the layer GEMM (built once at upload):
@@ -711,18 +716,18 @@ struct GemmPlan {
 };
 constexpr size_t kGemmSmemLimit = 220 * 1024;
 
-bool gemm_plan(int G, int fmt, bool stack, int nt, GemmPlan* out) {
+bool gemm_plan(int G, int fmt, bool stack, GemmPlan* out) {
     const int kc = gemm_ic(G) * G;
-    const size_t tile_a = static_cast<size_t>(kGmM) * kc * 4, tile_w = static_cast<size_t>(nt) * kc * 4;
-    const size_t abuf = (stack ? 1 : 2) * tile_a, wstage = (fmt == FMT_DENSE ? 1 : 2) * tile_w;
+    const size_t tile_a = static_cast<size_t>(kGmM) * kc * 4, tile_t = static_cast<size_t>(kGmN) * kc * 4;
+    const size_t abuf = (stack ? 1 : 2) * tile_a, wstage = 2 * tile_t;
     for (int wst = 3; wst >= 2; --wst) {
         size_t smem = 2 * abuf + wst * wstage;
         int ring = 0;
         if (fmt == FMT_DENSE) {
-            if (nt != kGmN || smem >= kGemmSmemLimit) continue;
-            ring = static_cast<int>(std::min<size_t>(6, (kGemmSmemLimit - smem) / tile_w));
-            if (ring < wst + 1) continue;
-            smem += ring * tile_w;
+            if (smem >= kGemmSmemLimit) continue;
+            ring = static_cast<int>(std::min<size_t>(6, (kGemmSmemLimit - smem) / tile_t));
+            if (ring < 3) continue;
+            smem += ring * tile_t;
         }
         if (smem > kGemmSmemLimit) continue;
         if (out) *out = GemmPlan{wst, ring, smem};
@@ -732,7 +737,7 @@ bool gemm_plan(int G, int fmt, bool stack, int nt, GemmPlan* out) {
 }
 
 bool gemm_supported(const DevLayer& L) {
-    if (L.G > 16 || !gemm_plan(L.G, L.fmt, false, kGmN, nullptr) || !gemm_plan(L.G, L.fmt, true, kGmN, nullptr))
+    if (L.G > 16 || !gemm_plan(L.G, L.fmt, false, nullptr) || !gemm_plan(L.G, L.fmt, true, nullptr))
         return false;
     if (L.fmt == FMT_DENSE) return L.wt != nullptr;
     return L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32;
@@ -744,14 +749,9 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     c.ic = gemm_ic(L.G);
     c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: 64 = A_hi / A_lo stacked in the 128 rows
     const bool stack = c.spt == 64;
-    static const int nt_env = [] {
-        const char* e = std::getenv("SKAN_GEMM_NT");  // experiment override: 256
-        return e ? std::atoi(e) : 0;
-    }();
-    // outputs per tile: 128 (three W stages fit); 256 only as an experiment
-    c.tj = (nt_env == 256 && L.fmt != FMT_DENSE && gemm_plan(L.G, L.fmt, stack, 256, nullptr)) ? 256 : kGmN;
+    c.tj = kGmN;
     GemmPlan gp{};
-    gemm_plan(L.G, L.fmt, stack, c.tj, &gp);
+    gemm_plan(L.G, L.fmt, stack, &gp);
     c.vj = gp.wst;
     c.rw = gp.ring;
     c.jt = (L.out + c.tj - 1) / c.tj;
@@ -759,7 +759,7 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     const int sms = num_sms > 0 ? num_sms : 148;
     // one CTA per SM: the fewest input splits whose waves are >= 90% full
     const long long base = static_cast<long long>(c.jt) * c.st;
-    const long long maxns = std::max<long long>(1, std::min<long long>(64, (L.in + c.ic - 1) / c.ic));
+    const long long maxns = std::max<long long>(1, std::min<long long>(148, (L.in + c.ic - 1) / c.ic));
     long long ns = 1;
     double best = 0.0;
     for (long long k = 1; k <= maxns; ++k) {
@@ -780,19 +780,15 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     return c;
 }
 
-template <bool STACK, int NT>
+template <bool STACK>
 void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
     const bool i4 = ic == 4;
     switch (fmt) {
-        case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, STACK, NT> : k_layer_gemm<FMT_I8_R32, 8, STACK, NT>;
-        case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, STACK, NT> : k_layer_gemm<FMT_I8_WIDE, 8, STACK, NT>;
-        default: return i4 ? k_layer_gemm<FMT_F32, 4, STACK, NT> : k_layer_gemm<FMT_F32, 8, STACK, NT>;
+        case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, STACK> : k_layer_gemm<FMT_I8_R32, 8, STACK>;
+        case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, STACK> : k_layer_gemm<FMT_I8_WIDE, 8, STACK>;
+        case FMT_F32: return i4 ? k_layer_gemm<FMT_F32, 4, STACK> : k_layer_gemm<FMT_F32, 8, STACK>;
+        default: return i4 ? k_layer_gemm<FMT_DENSE, 4, STACK> : k_layer_gemm<FMT_DENSE, 8, STACK>;
     }
-}
-
-template <bool STACK>
-void (*gemm_kernel_dense(int ic))(FwdArgs) {
-    return ic == 4 ? k_layer_gemm<FMT_DENSE, 4, STACK, kGmN> : k_layer_gemm<FMT_DENSE, 8, STACK, kGmN>;
 }
 
 unsigned long long* g_gemm_dbg = nullptr;
@@ -808,13 +804,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     }();
     a.gemm_skip = skip_env;
     const bool stack = c.spt == 64;
-    void (*k)(FwdArgs);
-    if (a.L.fmt == FMT_DENSE)
-        k = stack ? gemm_kernel_dense<true>(c.ic) : gemm_kernel_dense<false>(c.ic);
-    else if (c.tj == 256)
-        k = stack ? gemm_kernel<true, 256>(a.L.fmt, c.ic) : gemm_kernel<false, 256>(a.L.fmt, c.ic);
-    else
-        k = stack ? gemm_kernel<true, kGmN>(a.L.fmt, c.ic) : gemm_kernel<false, kGmN>(a.L.fmt, c.ic);
+    void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic) : gemm_kernel<false>(a.L.fmt, c.ic);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
     const int splits = (a.L.in + c.ichunk - 1) / c.ichunk;
     launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
