@@ -277,6 +277,13 @@ skan_status skan_debug_gemm_tf32(const float* d_a, const float* d_b, float* d_d,
  * per chunk < 64, phases as skan_gemm.cu documents).  NULL disables. */
 skan_status skan_debug_gemm_timeline(unsigned long long* d_stamps);
 
+/* Smallest batch the fast path routes to the tensor-core layer GEMM
+ * (default 3; <= 0 restores it).  Returns the previous value.  A test and
+ * tuning knob: the CUDA-core kernels serve the batches below it.  Set it
+ * before creating workspaces (their scratch is sized for the launch plans
+ * in force then); not thread-safe against concurrent forwards. */
+int skan_debug_set_gemm_min_batch(int batch);
+
 /* ---- single-edge primitive (lutham.cpp:730-755) ----------------------- */
 
 /* Batched pli_lookup over n independent (row, g, b, x) tuples on the GPU:

@@ -792,6 +792,7 @@ void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
 }
 
 unsigned long long* g_gemm_dbg = nullptr;
+int g_gemm_min_batch = kGemmMinBatch;
 
 void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
     FwdArgs a = a0;
@@ -839,4 +840,10 @@ void build_dense_tiles(const DevLayer& L, float* wt, cudaStream_t s) {
 extern "C" skan_status skan_debug_gemm_timeline(unsigned long long* d_stamps) {
     skan::g_gemm_dbg = d_stamps;
     return SKAN_OK;
+}
+
+extern "C" int skan_debug_set_gemm_min_batch(int batch) {
+    const int prev = skan::g_gemm_min_batch;
+    skan::g_gemm_min_batch = batch > 0 ? batch : skan::kGemmMinBatch;
+    return prev;
 }

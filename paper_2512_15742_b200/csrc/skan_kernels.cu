@@ -1074,7 +1074,7 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         c.ichunk = L.in;
         return c;
     }
-    if (B >= kGemmMinBatch && L.out >= 16 && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
+    if (B >= g_gemm_min_batch && L.out >= 16 && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {
         // samples in lanes: tile 128 samples x (32 or 64) outputs x split of the rows

@@ -427,6 +427,31 @@ def test_fast_mode_tensor_core_gemm_formats(torch_cuda, batch):
         assert np.array_equal(_bits(got), _bits(again)), name  # fixed-order split reduction
 
 
+@pytest.mark.parametrize("batch", [3, 16, 64, 200])
+@pytest.mark.parametrize("engine", ["cuda_cores", "tensor_cores"])
+def test_fast_mode_both_engines_agree_with_oracle(torch_cuda, batch, engine):
+    """The fast path has two engines for batches >= 3: the tensor-core layer
+    GEMM (default) and the CUDA-core kernels (k_fwd_small / k_fwd_large,
+    forced here by raising the GEMM threshold).  Both meet the tolerance on
+    a two-layer int8 head and a dense head."""
+    from paper_2512_15742_b200 import _lib
+    rng = np.random.default_rng(500 + batch)
+    cases = [
+        [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(
+            synthetic.synthetic_head(dims=(160, 136, 20), k=1024, grid=10, int8=True, seed=9))],
+        oracle.ref_random([40, 144, 18], 10, 0.4, 6, 0, False).tables(),
+    ]
+    prev = _lib.lib().skan_debug_set_gemm_min_batch(1 << 20 if engine == "cuda_cores" else 0)
+    try:
+        for tables in cases:
+            x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+            want, _ = oracle.port_forward(tables, x, batch)
+            got, _ = _gpu_forward(_upload(tables), x, batch, "fast", max_batch=256)
+            assert_close(got, want, l1_scale(tables, x, batch))
+    finally:
+        _lib.lib().skan_debug_set_gemm_min_batch(prev)
+
+
 def test_hot_swap_refills_a_resident_head(torch_cuda):
     """skan_head_swap: a head (batch-1 persistent path and the multi-kernel
     path) refilled in place serves the new tables bitwise in exact mode and
