@@ -29,3 +29,14 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_he
     -o "$OUT/prof_head_b1" python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
     > "$OUT/ncu_full.log" 2>&1
 echo "ncu full exit $?" >> "$OUT/status.txt"
+
+# tensor-core layer GEMM: ncu captures (cfg2 layer 0 at batch 256, cfg4
+# dense layer 0 at batch 64), phase timelines, latency by batch, configs
+bash tools/run_prof_gemm.sh "$TAG" 256 > /dev/null 2>&1
+echo "ncu gemm exit $?" >> "$OUT/status.txt"
+timeout 120 python tools/gemm_timeline.py --batch 256 --chunks 24 > "$OUT/gemm_timeline_b256.txt" 2>&1
+timeout 120 python tools/gemm_timeline.py --batch 64 --dense --chunks 24 > "$OUT/gemm_timeline_dense.txt" 2>&1
+timeout 300 python tools/diag_latency.py --batches 1,2,3,4,8,16,32,64,128,256 > "$OUT/latency_by_batch.txt" 2>&1
+timeout 300 python tools/diag_configs.py > "$OUT/configs.txt" 2>&1
+[ -x tools/bin/mb_mma ] && timeout 60 ./tools/bin/mb_mma > "$OUT/mb_mma.txt" 2>&1
+echo "done" >> "$OUT/status.txt"
