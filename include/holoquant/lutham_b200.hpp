@@ -369,4 +369,22 @@ inline void compressed_forward_async(const DeviceHead& head, const double* d_inp
 
 inline void check_workspace(DeviceWorkspace& ws) { b200_detail::check(skan_workspace_check(ws.get())); }
 
+// assign_indices (gsb.cpp:275-286) on the GPU: same signature and
+// ShapeError as the reference, bit-identical indices (skan_assign_indices).
+inline std::vector<std::uint32_t> assign_indices_device(std::span<const ShapeRecord> shapes,
+                                                        const Codebook& codebook) {
+    const int dim = codebook.grid_size;
+    std::vector<double> flat;
+    flat.reserve(shapes.size() * static_cast<std::size_t>(dim > 0 ? dim : 0));
+    for (const ShapeRecord& r : shapes) {
+        if (static_cast<int>(r.shape.size()) != dim) throw ShapeError("shape/codebook grid size mismatch");
+        flat.insert(flat.end(), r.shape.begin(), r.shape.end());
+    }
+    std::vector<std::uint32_t> idx(shapes.size());
+    if (shapes.empty()) return idx;
+    b200_detail::check(skan_assign_indices(flat.data(), shapes.size(), dim, codebook.entries.data(), codebook.k,
+                                           idx.data(), SKAN_PTR_HOST, nullptr));
+    return idx;
+}
+
 }  // namespace holoquant

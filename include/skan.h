@@ -295,6 +295,18 @@ skan_status skan_pli_lookup(const double* d_codebook, int k, int grid_size, cons
                             double domain_lo, double domain_hi, int n, double* d_y,
                             void* stream);
 
+/* ---- GSB-VQ nearest-row assignment (gsb.cpp:275-286) ------------------ */
+
+/* indices[i] = the codebook row (of k, each `dim` doubles, row-major) at the
+ * least squared distance from shapes[i] (n x dim, row-major), ties to the
+ * lowest row: holoquant::assign_indices with nearest_row (gsb.cpp:62-73)
+ * and dist2 (23-30), bit-identical (f64, dim order, no contraction).
+ * dim in [1, 64]; k == 0 gives row 0 everywhere (as nearest_row does).
+ * ptr_flags: SKAN_PTR_HOST (synchronous, copies inside) or SKAN_PTR_DEVICE
+ * (device pointers, asynchronous on stream). */
+skan_status skan_assign_indices(const double* shapes, uint64_t n, int dim, const double* codebook, int k,
+                                uint32_t* indices, unsigned ptr_flags, void* stream);
+
 /* ---- knot selection (kan.cpp:28-58) ------------------------------------ */
 
 /* Bracket n inputs on the GPU: index[n], t[n], clamped[n] (device

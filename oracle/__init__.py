@@ -95,6 +95,8 @@ def _load_port():
         L.oracle_pack_indices.argtypes = [_p, C.c_size_t, C.c_int, _p, C.c_size_t]
         L.oracle_unpack_indices.restype = C.c_int
         L.oracle_unpack_indices.argtypes = [_p, C.c_size_t, C.c_uint64, C.c_int, _p]
+        L.oracle_assign_indices.restype = None
+        L.oracle_assign_indices.argtypes = [_p, C.c_uint64, C.c_int, _p, C.c_int, _p]
         L.oracle_compressed_forward.restype = C.c_int
         L.oracle_compressed_forward.argtypes = [C.POINTER(OracleLayer), C.c_int, _p, C.c_int, _p, _p,
                                                 C.POINTER(C.c_uint64)]
@@ -140,6 +142,9 @@ def _load_ref():
             "hqref_model_deserialize": (C.c_int, [_p, C.c_size_t, C.POINTER(_p)]),
             "hqref_model_serialize": (C.c_longlong, [_p, _p, C.c_size_t]),
             "hqref_model_free": (None, [_p]),
+            "hqref_assign_indices": (C.c_int, [_p, C.c_uint64, C.c_int, _p, C.c_int, _p]),
+            "hqref_kmeans_codebook": (C.c_int, [_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_uint64, _p,
+                                                C.POINTER(C.c_int)]),
             "hqref_model_nlayers": (C.c_int, [_p]),
             "hqref_model_layer": (C.c_int, [_p, C.c_int, C.POINTER(OracleLayer)]),
             "hqref_forward": (C.c_int, [_p, _p, C.c_int, _p, C.c_int, C.POINTER(C.c_uint64)]),
@@ -400,6 +405,36 @@ def _locate_many(fn, lo, hi, G, xs):
 def port_locate_many(lo, hi, G, xs):
     """oracle_locate_many: (index, t, clamped, n_nonfinite)."""
     return _locate_many(port().oracle_locate_many, lo, hi, G, xs)
+
+
+def port_assign_indices(shapes: np.ndarray, entries: np.ndarray) -> np.ndarray:
+    """oracle_assign_indices (gsb.cpp:275-286 restated): nearest codebook row
+    per shape, f64 squared distance in dim order, ties to the lowest row."""
+    s = np.ascontiguousarray(shapes, dtype=np.float64)
+    e = np.ascontiguousarray(entries, dtype=np.float64)
+    out = np.zeros(s.shape[0], np.uint32)
+    port().oracle_assign_indices(s.ctypes.data, s.shape[0], s.shape[1], e.ctypes.data, e.shape[0], out.ctypes.data)
+    return out
+
+
+def ref_assign_indices(shapes: np.ndarray, entries: np.ndarray) -> np.ndarray:
+    """holoquant::assign_indices (the reference, compiled) on row-major arrays."""
+    s = np.ascontiguousarray(shapes, dtype=np.float64)
+    e = np.ascontiguousarray(entries, dtype=np.float64)
+    out = np.zeros(s.shape[0], np.uint32)
+    _ref_check(ref().hqref_assign_indices(s.ctypes.data, s.shape[0], s.shape[1], e.ctypes.data, e.shape[0],
+                                          out.ctypes.data))
+    return out
+
+
+def ref_kmeans_codebook(shapes: np.ndarray, k: int, seed: int, max_iters: int = 50) -> np.ndarray:
+    """holoquant::kmeans_codebook entries (k x dim) for test codebooks."""
+    s = np.ascontiguousarray(shapes, dtype=np.float64)
+    e = np.zeros((k, s.shape[1]), np.float64)
+    it = C.c_int(0)
+    _ref_check(ref().hqref_kmeans_codebook(s.ctypes.data, s.shape[0], s.shape[1], k, max_iters, seed, e.ctypes.data,
+                                           C.byref(it)))
+    return e
 
 
 def ref_locate_many(lo, hi, G, xs):

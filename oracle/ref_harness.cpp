@@ -397,4 +397,34 @@ int hqref_projected_storage(std::uint64_t edges, std::uint64_t k, std::uint64_t 
     });
 }
 
+// assign_indices gsb.cpp:275 (shapes n x dim, codebook k x dim, row-major)
+int hqref_assign_indices(const double* shapes, std::uint64_t n, int dim, const double* entries, int k,
+                         std::uint32_t* out) {
+    return guarded([&] {
+        std::vector<ShapeRecord> recs(n);
+        for (std::uint64_t i = 0; i < n; ++i) recs[i].shape.assign(shapes + i * dim, shapes + (i + 1) * dim);
+        Codebook cb;
+        cb.k = k;
+        cb.grid_size = dim;
+        cb.entries.assign(entries, entries + static_cast<std::size_t>(k) * dim);
+        const std::vector<std::uint32_t> idx = assign_indices(recs, cb);
+        std::memcpy(out, idx.data(), idx.size() * sizeof(std::uint32_t));
+    });
+}
+
+// kmeans_codebook gsb.cpp:236 (entries out: k x dim); returns iterations via *iters
+int hqref_kmeans_codebook(const double* shapes, std::uint64_t n, int dim, int k, int max_iters,
+                          std::uint64_t seed, double* entries, int* iters) {
+    return guarded([&] {
+        std::vector<ShapeRecord> recs(n);
+        for (std::uint64_t i = 0; i < n; ++i) recs[i].shape.assign(shapes + i * dim, shapes + (i + 1) * dim);
+        KMeansConfig cfg;
+        cfg.max_iters = max_iters;
+        cfg.seed = seed;
+        const Codebook cb = kmeans_codebook(recs, k, cfg);
+        std::memcpy(entries, cb.entries.data(), cb.entries.size() * sizeof(double));
+        if (iters) *iters = cb.training_meta.iterations;
+    });
+}
+
 }  // extern "C"

@@ -314,3 +314,26 @@ int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double
     free(tids);
     return rc;
 }
+
+/* gsb.cpp:23-30 (dist2), 62-73 (nearest_row), 275-286 (assign_indices). */
+void oracle_assign_indices(const double* shapes, uint64_t n, int dim, const double* entries, int k,
+                           uint32_t* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const double* a = shapes + i * (uint64_t)dim;
+        int best = 0;
+        double best_d = INFINITY;
+        for (int r = 0; r < k; ++r) {
+            const double* b = entries + (uint64_t)r * (uint64_t)dim;
+            double s = 0.0;
+            for (int c = 0; c < dim; ++c) {
+                const double d = a[c] - b[c];
+                s += d * d;
+            }
+            if (s < best_d) {
+                best_d = s;
+                best = r;
+            }
+        }
+        out[i] = (uint32_t)best;
+    }
+}

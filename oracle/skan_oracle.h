@@ -83,6 +83,13 @@ int oracle_compressed_forward(const oracle_layer* layers, int n, const double* i
 int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double* inputs,
                                  int batch, double* outputs, int threads, uint64_t* interp_ops);
 
+/* assign_indices, gsb.cpp:275-286 with nearest_row 62-73 and dist2 23-30:
+ * per shape (n x dim row-major) the codebook row (k x dim) of least
+ * squared distance, accumulated in dim order as s += (a-b)*(a-b) (no
+ * contraction); strict <, so ties keep the lowest row. */
+void oracle_assign_indices(const double* shapes, uint64_t n, int dim, const double* entries, int k,
+                           uint32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

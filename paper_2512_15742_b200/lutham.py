@@ -527,6 +527,33 @@ def pli_lookup(codebook, rows, g, b, x, domain_lo: float, domain_hi: float, grid
     return y
 
 
+def assign_indices(shapes, codebook: Codebook) -> np.ndarray:
+    """assign_indices (gsb.cpp:275-286) on the GPU: the nearest codebook row
+    per shape, ties to the lowest row, bit-identical to the reference.
+
+    shapes: a sequence of objects with a ``shape`` vector (ShapeRecord-like)
+    or an (n, grid_size) float64 array.  Raises ShapeError("shape/codebook
+    grid size mismatch") like the reference."""
+    if isinstance(shapes, np.ndarray):
+        arr = np.ascontiguousarray(shapes, dtype=np.float64)
+        if arr.ndim != 2 or (arr.shape[0] and arr.shape[1] != codebook.grid_size):
+            raise ShapeError("shape/codebook grid size mismatch")
+    else:
+        rows = [np.asarray(getattr(r, "shape", r), dtype=np.float64) for r in shapes]
+        for r in rows:
+            if r.size != codebook.grid_size:
+                raise ShapeError("shape/codebook grid size mismatch")
+        arr = np.ascontiguousarray(np.stack(rows) if rows else np.zeros((0, codebook.grid_size)))
+    n = arr.shape[0]
+    out = np.zeros(n, np.uint32)
+    if n == 0:
+        return out
+    ent = np.ascontiguousarray(codebook.entries, dtype=np.float64)
+    _lib.check(_lib.lib().skan_assign_indices(arr.ctypes.data, n, int(codebook.grid_size), ent.ctypes.data,
+                                              int(codebook.k), out.ctypes.data, 0, None))
+    return out
+
+
 def unpack_indices(d_bytes, count: int, bits: int):
     """GPU unpack_indices (lutham.cpp:114-137) of a uint8 CUDA tensor."""
     import torch

@@ -8,6 +8,7 @@
 //   test_lutham_b200 cpu   cases that need no GPU (planner, file faults)
 //   test_lutham_b200 gpu   device cases (forward parity, errors, interp_ops)
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -290,6 +291,28 @@ TEST_GPU("swap_device_model: a resident head refilled in place forwards like the
     compressed_forward(dev, x, 4, y, ws, DeviceMode::Exact);
     CHECK(bitwise_equal(y, ref_forward(build_model(b), x, 4)));
     CHECK_THROWS_AS(swap_device_model(dev, head({64, 40, 5}, 10, 256, true, 33)), ContractError);
+}
+
+TEST_GPU("assign_indices_device == holoquant::assign_indices (test_gsb.cpp:104-132), ties to the lowest row") {
+    std::mt19937_64 rng(6);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    std::vector<ShapeRecord> pts(300);
+    for (auto& p : pts) {
+        p.shape.resize(6);
+        for (double& x : p.shape) x = u(rng);
+    }
+    KMeansConfig cfg;
+    cfg.seed = 2;
+    Codebook cb = kmeans_codebook(pts, 12, cfg);
+    CHECK(assign_indices_device(pts, cb) == assign_indices(pts, cb));
+    // duplicated rows: every tie resolves to the first copy
+    cb.entries.insert(cb.entries.end(), cb.entries.begin(), cb.entries.end());
+    cb.k *= 2;
+    const std::vector<std::uint32_t> got = assign_indices_device(pts, cb);
+    CHECK(got == assign_indices(pts, cb));
+    CHECK(*std::max_element(got.begin(), got.end()) < 12u);
+    pts[7].shape.pop_back();
+    CHECK_THROWS_AS(assign_indices_device(pts, cb), ShapeError);
 }
 
 TEST_GPU("cfg2 head {2048,1408,20} K=65536 int8: batch 1 fast within tolerance, exact bitwise") {
