@@ -265,8 +265,8 @@ __device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph
 template <int FMT, int IC, bool STACK>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t s_wfree[3];  // W stage free: the MMAs of its last chunk completed
-    __shared__ __align__(8) uint64_t s_full[3];   // stage written: every producer arrives
+    __shared__ __align__(8) uint64_t s_wfree[4];  // W stage free: the MMAs of its last chunk completed
+    __shared__ __align__(8) uint64_t s_full[4];   // stage written: every producer arrives
     __shared__ __align__(8) uint64_t s_afree[2];  // A buffer free: the MMAs of its last chunk completed
     __shared__ __align__(8) uint64_t s_ring[6];   // DENSE: W tile of chunk c landed in ring slot c % ring
     __shared__ uint32_t s_tmem;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     for (uint32_t q = tid * 16; q < 2 * abuf; q += kGmT * 16)
         *reinterpret_cast<uint4*>(s_a + q) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 4; ++q) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_wfree[q])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&s_full[q])), "r"(kGmP));
         }
@@ -339,13 +339,14 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     for (int u = 0; u < kAU; ++u) sa.aoff[u] = sb.aoff[u] = 0xFFFFFFFFu;
     uint32_t recn[kI8 ? kEPT : 1], kn[kI8 ? kEPT : 1];  // I8: records of the chunk after next
     unsigned nvalid = 0;
-    // A roles: slot u = (row ra = q % 128, input ila = q / 128), q = tid + 512 u
+    // A roles: slot u = (row ra = q / IC, input ila = q % IC), q = tid + 512 u: a warp's
+    // 32 stores then land in 32 distinct banks (8 rows x 4 inputs, IC = 4)
     const int* bm0[kAU];
     const float* bt0[kAU];
     bool aok[kAU];
 #pragma unroll
     for (int u = 0; u < kAU; ++u) {
-        const int q = tid + kGmP * u, ra = q % kGmM, ila = q / kGmM;
+        const int q = tid + kGmP * u, ra = q / IC, ila = q % IC;
         const int smp = STACK ? (ra & 63) : ra;
         aok[u] = smp < nS;
         bm0[u] = a.bm_in + static_cast<size_t>(r0 + ila) * a.B + s0 + smp;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         const size_t step = static_cast<size_t>(c) * IC * a.B;
 #pragma unroll
         for (int u = 0; u < kAU; ++u) {
-            const int ila = (tid + kGmP * u) / kGmM;
+            const int ila = (tid + kGmP * u) % IC;
             st.bm[u] = -2;
             st.bt[u] = 0.f;
             if (aok[u] && ib + ila < rend) {
@@ -481,7 +482,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         unsigned char* sab = s_a + ab * abuf;
 #pragma unroll
         for (int u = 0; u < kAU; ++u) {
-            const int q = tid + kGmP * u, ra = q % kGmM, il = q / kGmM;
+            const int q = tid + kGmP * u, ra = q / IC, il = q % IC;
             const bool lo_row = STACK && ra >= 64;
             if (cur.aoff[u] != 0xFFFFFFFFu) {
                 const uint32_t o0 = cur.aoff[u] & 0xFFFFu, o1 = cur.aoff[u] >> 16;
@@ -557,9 +558,20 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 if (s >= nks) break;
+                if (a.gemm_skip & 16) {  // experiment: three N = 128 MMAs
+                    tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc1, (c | s) != 0);
+                    tc::mma_tf32_ss_warp(tmem + kGmN, da + s * kStepA, dw + ((kLoRows >> 4) + s * kStepW), idesc1, (c | s) != 0);
+                    if constexpr (!STACK)
+                        tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
+                } else if (a.gemm_skip & 32) {  // experiment: two N = 256 MMAs
+                    tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
+                    if constexpr (!STACK)
+                        tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc2, 1u);
+                } else {
                 tc::mma_tf32_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
                 if constexpr (!STACK)
                     tc::mma_tf32_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
+                }
             }
             tc::mma_commit_warp(&s_afree[ab]);
             tc::mma_commit_warp(&s_wfree[ws]);
@@ -720,7 +732,13 @@ bool gemm_plan(int G, int fmt, bool stack, GemmPlan* out) {
     const int kc = gemm_ic(G) * G;
     const size_t tile_a = static_cast<size_t>(kGmM) * kc * 4, tile_t = static_cast<size_t>(kGmN) * kc * 4;
     const size_t abuf = (stack ? 1 : 2) * tile_a, wstage = 2 * tile_t;
-    for (int wst = 3; wst >= 2; --wst) {
+    static const int wst_env = [] {
+        const char* e = std::getenv("SKAN_GEMM_WST");  // experiment: most W stages to try
+        return e ? std::atoi(e) : 0;
+    }();
+    // two W stages by default: measured faster than three (the smaller
+    // carve-out leaves the L1 ~90 KB instead of ~30 KB for the gathers)
+    for (int wst = wst_env >= 2 && wst_env <= 4 ? wst_env : 2; wst >= 2; --wst) {
         size_t smem = 2 * abuf + wst * wstage;
         int ring = 0;
         if (fmt == FMT_DENSE) {
@@ -807,6 +825,11 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     const bool stack = c.spt == 64;
     void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic) : gemm_kernel<false>(a.L.fmt, c.ic);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+    static const int carve_env = [] {
+        const char* e = std::getenv("SKAN_GEMM_CARVEOUT");  // experiment: shared-memory carve-out percent
+        return e ? std::atoi(e) : -1;
+    }();
+    if (carve_env >= 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve_env);
     const int splits = (a.L.in + c.ichunk - 1) / c.ichunk;
     launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
     // bias: folded into W for compressed layers; dense layers have none

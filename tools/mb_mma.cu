@@ -48,7 +48,7 @@ __device__ __forceinline__ uint4 lds_v(const void* p) {
 }
 
 __global__ void __launch_bounds__(kT, 1) k_mma(int M, int N, int kind, int reps, int noise, int swz, long long* out,
-                                                int commit_every) {
+                                                int commit_every, int data_kind) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ __align__(8) uint64_t bar2[2];
@@ -60,7 +60,16 @@ __global__ void __launch_bounds__(kT, 1) k_mma(int M, int N, int kind, int reps,
     unsigned char* A = smem;
     unsigned char* B = smem + M * 256;
     unsigned char* scratch = B + N * 256;  // noise region (64 KB)
-    for (int q = tid * 16; q < (M + N) * 256; q += kT * 16) *reinterpret_cast<uint4*>(smem + q) = make_uint4(0, 0, 0, 0);
+    for (int q = tid * 16; q < (M + N) * 256; q += kT * 16) {
+        // non-zero operands (pseudo-random f32 in [-1, 1]): the tensor pipe's rate with real data
+        uint32_t h = (q * 2654435761u) ^ 0x9E3779B9u;
+        float f[4];
+        for (int u = 0; u < 4; ++u) {
+            h = h * 1664525u + 1013904223u;
+            f[u] = data_kind ? (static_cast<float>(h >> 8) * (2.0f / 16777216.0f) - 1.0f) : 0.f;
+        }
+        *reinterpret_cast<float4*>(smem + q) = make_float4(f[0], f[1], f[2], f[3]);
+    }
     if (tid == 0) {
         s_stop = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar)));
@@ -99,16 +108,9 @@ __global__ void __launch_bounds__(kT, 1) k_mma(int M, int N, int kind, int reps,
                 for (int s = 0; s < 8; ++s) da[s] = tmem + 256 + 8 * s;
             const long long t0 = clock64();
 #pragma unroll 1
-            int cnt = 0;
             for (int r = 0; r < reps; r += 8) {
 #pragma unroll
-                for (int s = 0; s < 8; ++s) {
-                    mma_any(tmem, da[s], db[s], idesc, kind);
-                    if (commit_every && ++cnt == commit_every) {
-                        cnt = 0;
-                        tc::mma_commit(&bar2[(r >> 3) & 1]);
-                    }
-                }
+                for (int s = 0; s < 8; ++s) mma_any(tmem, da[s], db[s], idesc, kind);
             }
             tc::mma_commit(&bar);
             uint32_t done = 0;
@@ -160,22 +162,23 @@ int main() {
     cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     struct S { int M, N, kind; } shapes[] = {{64, 128, 0}, {128, 128, 0}, {64, 256, 0}, {128, 256, 0}, {128, 128, 1}, {128, 256, 1}, {128, 128, 2}, {128, 256, 2}, {64, 256, 2}, {128, 128, 3}, {128, 128, 4}};
     const int reps = 4096;
-    for (int ce : {0, 15, 5})
+    for (int dk : {0, 1})
+    for (int ce : {0})
     for (int swz : {0})
     for (auto sh : shapes) {
         if (sh.kind == 1 || sh.M == 64) continue;
         for (int noise = 0; noise < 1; noise += 3) {
             long long h[2] = {0, 0};
             cudaMemset(d, 0, 64);
-            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce);
-            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce);
+            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce, dk);
+            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce, dk);
             cudaError_t e = cudaDeviceSynchronize();
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
             const double cpm = static_cast<double>(h[0]) / reps;
             const int kk = sh.kind == 1 ? 16 : 8;
             const double flop_clk = 2.0 * sh.M * sh.N * kk / cpm;
-            printf("commit/%2d swz%3d %s M=%3d N=%3d noise=%d: %6.1f clk/mma  %7.0f flop/clk/SM  operand B/clk %5.1f  noise ops/thread %lld %s\n",
-                   ce, swz, sh.kind == 1 ? "bf16" : (sh.kind == 2 ? "tf32-TS" : (sh.kind == 3 ? "cp+TS" : (sh.kind == 4 ? "cp-only" : "tf32"))), sh.M, sh.N, noise, cpm, flop_clk, (sh.M + sh.N) * 32.0 / cpm, h[1],
+            printf("data%d commit/%2d swz%3d %s M=%3d N=%3d noise=%d: %6.1f clk/mma  %7.0f flop/clk/SM  operand B/clk %5.1f  noise ops/thread %lld %s\n",
+                   dk, ce, swz, sh.kind == 1 ? "bf16" : (sh.kind == 2 ? "tf32-TS" : (sh.kind == 3 ? "cp+TS" : (sh.kind == 4 ? "cp-only" : "tf32"))), sh.M, sh.N, noise, cpm, flop_clk, (sh.M + sh.N) * 32.0 / cpm, h[1],
                    e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     }
