@@ -1,7 +1,9 @@
-// tcgen05.mma issue throughput (cycles per instruction, one CTA per SM on
-// all SMs) for the shapes the layer GEMM can use, alone and while 512
-// threads stream 16-byte shared-memory stores/loads next to it (the
-// producers' operand writes compete with the tensor core's operand reads).
+// tcgen05.mma throughput (cycles per instruction, one CTA per SM on all
+// SMs, descriptors precomputed, 8 MMAs unrolled per loop trip) for the
+// shapes the layer GEMM can use: A and B from shared memory (SS), A from
+// TMEM (TS), tcgen05.cp of the A block into TMEM (+ TS MMA); zero or
+// random operands; alone and while 512 threads stream shared-memory
+// loads/stores next to it (noise=3: the producers' traffic pattern).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2512_15742_b200/csrc tools/mb_mma.cu -o tools/bin/mb_mma
 #include <cuda_runtime.h>
 
@@ -48,10 +50,9 @@ __device__ __forceinline__ uint4 lds_v(const void* p) {
 }
 
 __global__ void __launch_bounds__(kT, 1) k_mma(int M, int N, int kind, int reps, int noise, int swz, long long* out,
-                                                int commit_every, int data_kind) {
+                                                int data_kind) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
-    __shared__ __align__(8) uint64_t bar2[2];
     __shared__ uint32_t s_tmem;
     __shared__ volatile int s_stop;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -73,8 +74,6 @@ __global__ void __launch_bounds__(kT, 1) k_mma(int M, int N, int kind, int reps,
     if (tid == 0) {
         s_stop = 0;
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar2[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar2[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
@@ -163,22 +162,20 @@ int main() {
     struct S { int M, N, kind; } shapes[] = {{64, 128, 0}, {128, 128, 0}, {64, 256, 0}, {128, 256, 0}, {128, 128, 1}, {128, 256, 1}, {128, 128, 2}, {128, 256, 2}, {64, 256, 2}, {128, 128, 3}, {128, 128, 4}};
     const int reps = 4096;
     for (int dk : {0, 1})
-    for (int ce : {0})
     for (int swz : {0})
     for (auto sh : shapes) {
-        if (sh.kind == 1 || sh.M == 64) continue;
-        for (int noise = 0; noise < 1; noise += 3) {
+        for (int noise = 0; noise < 4; noise += 3) {
             long long h[2] = {0, 0};
             cudaMemset(d, 0, 64);
-            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce, dk);
-            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, ce, dk);
+            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, dk);
+            k_mma<<<148, kT, smem>>>(sh.M, sh.N, sh.kind, reps, noise, swz, d, dk);
             cudaError_t e = cudaDeviceSynchronize();
             cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
             const double cpm = static_cast<double>(h[0]) / reps;
             const int kk = sh.kind == 1 ? 16 : 8;
             const double flop_clk = 2.0 * sh.M * sh.N * kk / cpm;
-            printf("data%d commit/%2d swz%3d %s M=%3d N=%3d noise=%d: %6.1f clk/mma  %7.0f flop/clk/SM  operand B/clk %5.1f  noise ops/thread %lld %s\n",
-                   dk, ce, swz, sh.kind == 1 ? "bf16" : (sh.kind == 2 ? "tf32-TS" : (sh.kind == 3 ? "cp+TS" : (sh.kind == 4 ? "cp-only" : "tf32"))), sh.M, sh.N, noise, cpm, flop_clk, (sh.M + sh.N) * 32.0 / cpm, h[1],
+            printf("data%d swz%3d %s M=%3d N=%3d noise=%d: %6.1f clk/mma  %7.0f flop/clk/SM  operand B/clk %5.1f  noise ops/thread %lld %s\n",
+                   dk, swz, sh.kind == 1 ? "bf16" : (sh.kind == 2 ? "tf32-TS" : (sh.kind == 3 ? "cp+TS" : (sh.kind == 4 ? "cp-only" : "tf32"))), sh.M, sh.N, noise, cpm, flop_clk, (sh.M + sh.N) * 32.0 / cpm, h[1],
                    e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     }
