@@ -20,6 +20,7 @@ UNMODIFIED holoquant sources compiled into oracle/_ref) on the host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -293,6 +294,46 @@ def main():
     ms256 = sync_max(statistics.mean(t256))
     edges = model.edge_count()
 
+    # dominant kernel of the bs256 step: layer 0's tensor-core GEMM, timed
+    # alone (skan_profile_gemm: the k_layer_gemm launch only) with CUDA events
+    # on its stream, L2 flushed before each launch like the step
+    gemm_roof = None
+    nb = hi - lo
+    if rank == 0 and nb >= 3:
+        issued = C.c_double(0.0)
+        try:
+            with torch.cuda.stream(stream):
+                _lib.check(L.skan_forward_async(model.handle, ws.handle, d_x256.data_ptr(), nb, d_y256.data_ptr(),
+                                                mode, s_ptr))
+                gt = []
+                for r in range(13):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    _lib.check(L.skan_profile_gemm(model.handle, ws.handle, 0, nb, s_ptr, C.byref(issued)))
+                    e1.record(stream)
+                    if r >= 3:
+                        gt.append((e0, e1))
+                stream.synchronize()
+            g_us = statistics.mean(x.elapsed_time(y) * 1e3 for x, y in gt)
+            alg = 2.0 * nb * DIMS[0] * G * DIMS[1]  # Y[B x out] = A[B x in*G] . W[in*G x out]
+            tf32_peak = pk.get("bf16_tflops", 2250.0) / 2.0
+            gprof = os.path.join(ROOT, "profiles", "r1", "ncu_layer_gemm_bs256.json")
+            try:
+                gtraffic = json.load(open(gprof)).get("dram_bytes_per_launch")
+            except Exception:
+                gtraffic = None
+            gemm_roof = {"bound": "tensor", "achieved": alg / g_us / 1e6, "peak": tf32_peak, "unit": "TFLOP/s",
+                         "frac": alg / g_us / 1e6 / tf32_peak, "traffic": gtraffic,
+                         "kernel": "k_layer_gemm (layer 0, 2048->1408, batch %d)" % nb, "kernel_us": g_us,
+                         "algorithmic_flops": alg, "issued_tflops": issued.value / g_us / 1e6,
+                         "issued_flops": issued.value,
+                         "note": "algorithmic = the hat-basis contraction 2*B*(in*G)*out; issued = the split-precision "
+                                 "tf32 MMAs (A_hi x [W_hi|W_lo] + A_lo x W_hi, ~3x); peak = MEASURED_PEAKS bf16_tflops "
+                                 "/ 2 (kind::tf32 issues half the K of kind::f16 per instruction, tools/mb_mma.cu)"}
+        except Exception as e:  # noqa: BLE001 - a side measurement must not sink the bench line
+            gemm_roof = {"unavailable": str(e)}
+
     # ---- the other BASELINE.json configs on this GPU (side measurements) ---
     def event_us(fn, reps):
         """median CUDA-event time (us) of fn on `stream`, L2 flushed before each call"""
@@ -404,7 +445,8 @@ def main():
                       "global_batch": 256, "per_gpu_batch": hi - lo, "scaling": "strong",
                       "edge_evals_per_s": 256 * edges / (ms256 * 1e-3),
                       "effective_gbs": 256 * bytes1 / (ms256 * 1e-3) / 1e9,
-                      "effective_note": "256 x bytes(1) / time (the paper's framing): shows on-chip reuse, not DRAM traffic"},
+                      "effective_note": "256 x bytes(1) / time (the paper's framing): shows on-chip reuse, not DRAM traffic",
+                      "roofline": gemm_roof},
             "e2e": {"value": e2e_value, "unit": "samples/s",
                     "h2d_bytes_per_step": int(xh.nbytes), "d2h_bytes_per_step": int(yh.nbytes),
                     "ms_per_step": e2e_s * 1e3, "path": "skan_forward(SKAN_PTR_HOST) from pinned host memory"},

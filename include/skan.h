@@ -257,6 +257,14 @@ int skan_workspace_last_launches(const skan_workspace* ws);
 skan_status skan_profile_gather(const skan_head* head, skan_workspace* ws, int layer, int batch,
                                 int mode, void* stream);
 
+/* Profiling hook: enqueue ONLY layer `layer`'s tensor-core GEMM kernel
+ * (k_layer_gemm, no split reduction) for `batch` samples on `stream`,
+ * reading the brackets the previous fast forward of the same batch on ws
+ * left behind; ContractError if the layer does not use the GEMM at this
+ * batch.  *issued_flops (optional) = the MMA work one launch issues. */
+skan_status skan_profile_gemm(const skan_head* head, skan_workspace* ws, int layer, int batch, void* stream,
+                              double* issued_flops);
+
 /* Profiling hook: batch-1 forwards on ws record, per CTA of the persistent
  * head kernel, %globaltimer stamps (ns) at 16 fixed phase slots into the
  * device buffer d_stamps[grid][16] (NULL disables). */

@@ -1064,6 +1064,32 @@ skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int laye
     });
 }
 
+skan_status skan_profile_gemm(const skan_head* h, skan_workspace* ws, int layer, int batch, void* stream,
+                              double* issued_flops) {
+    return guarded([&] {
+        check_forward_args(h, ws, batch);
+        if (layer < 0 || layer >= static_cast<int>(h->dl.size())) raise(SKAN_SHAPE_ERROR, "layer index out of range");
+        if (batch < 1 || batch > ws->max_batch) raise(SKAN_CONTRACT_ERROR, "batch outside the workspace capacity");
+        if (!ws->last_x) raise(SKAN_CONTRACT_ERROR, "run a forward on this workspace first");
+        const std::vector<skan::LaunchCfg> cfg = plan_head(h, batch);
+        if (cfg[layer].kind != 4) raise(SKAN_CONTRACT_ERROR, "layer does not run on the tensor-core GEMM at this batch");
+        DeviceGuard g(h->device);
+        auto& d = ws->d;
+        const size_t plane = static_cast<size_t>(ws->max_batch) * h->max_width;
+        skan::FwdArgs a{};
+        a.L = h->dl[layer];
+        a.B = batch;
+        a.rows_per_cta = cfg[layer].ichunk;
+        a.bm_in = d.bm + (layer & 1) * plane;
+        a.bt_in = d.btf + (layer & 1) * plane;
+        a.partial = d.partial + (layer & 1) * ws->partial_floats;
+        a.err = d.err;
+        skan::launch_layer_gemm(a, cfg[layer], false, static_cast<cudaStream_t>(stream), /*with_reduce=*/false);
+        skan::cuda_check(cudaGetLastError(), "profile launch");
+        if (issued_flops) *issued_flops = skan::gemm_issued_flops(h->dl[layer], cfg[layer], batch);
+    });
+}
+
 skan_status skan_debug_b1_timeline(skan_workspace* ws, unsigned long long* d_stamps) {
     return guarded([&] {
         if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");

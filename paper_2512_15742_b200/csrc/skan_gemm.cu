@@ -809,10 +809,18 @@ void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
     }
 }
 
+double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B) {
+    // per CTA and K = 8 step: one M=128 x N=256 MMA, plus (not stacked) one N=128
+    const double ksteps = static_cast<double>((L.in + c.ic - 1) / c.ic) * c.ic * L.G / 8.0;
+    const double per_step = 2.0 * kGmM * 8 * (2 * kGmN + (c.spt == 64 ? 0 : kGmN));
+    (void)B;
+    return ksteps * per_step * c.jt * c.st;
+}
+
 unsigned long long* g_gemm_dbg = nullptr;
 int g_gemm_min_batch = kGemmMinBatch;
 
-void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce) {
     FwdArgs a = a0;
     a.dbg = g_gemm_dbg;
     a.gemm_wst = c.vj;
@@ -832,6 +840,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     if (carve_env >= 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve_env);
     const int splits = (a.L.in + c.ichunk - 1) / c.ichunk;
     launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
+    if (!with_reduce) return;
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {

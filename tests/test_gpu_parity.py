@@ -452,6 +452,27 @@ def test_fast_mode_both_engines_agree_with_oracle(torch_cuda, batch, engine):
         _lib.lib().skan_debug_set_gemm_min_batch(prev)
 
 
+def test_profile_gemm_hook(torch_cuda):
+    """skan_profile_gemm launches one layer's GEMM alone after a forward and
+    reports the MMA work it issues; layers off the GEMM are a ContractError."""
+    import ctypes as C
+    from paper_2512_15742_b200 import _lib
+    torch = torch_cuda
+    model = hq.build_model(synthetic.synthetic_head(dims=(256, 160, 20), k=512, grid=10, int8=True, seed=8))
+    ws = hq.make_workspace(model, 64)
+    x = torch.from_numpy(synthetic.synthetic_inputs(64, 256, seed=1)).cuda()
+    y = torch.zeros(64 * 20, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    hq.forward_async(model, x, 64, y, ws, stream=s)
+    fl = C.c_double(0)
+    _lib.check(_lib.lib().skan_profile_gemm(model.handle, ws.handle, 0, 64, s, C.byref(fl)))
+    torch.cuda.synchronize()
+    # stacked (batch <= 64): one M=128 x N=256 x K=8 MMA per K step, two 128-output tiles
+    assert fl.value == 2.0 * 128 * 8 * 256 * (256 * 10 / 8) * 2
+    hq.forward_async(model, x, 1, y, ws, stream=s)
+    assert _lib.lib().skan_profile_gemm(model.handle, ws.handle, 0, 1, s, None) == 3  # SKAN_CONTRACT_ERROR
+
+
 def test_hot_swap_refills_a_resident_head(torch_cuda):
     """skan_head_swap: a head (batch-1 persistent path and the multi-kernel
     path) refilled in place serves the new tables bitwise in exact mode and
