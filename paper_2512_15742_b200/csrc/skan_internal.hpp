@@ -133,7 +133,7 @@ struct FwdArgs {
     unsigned long long* dbg;      // layer GEMM phase stamps (skan_debug_gemm_timeline), or null
     int gemm_wst;                 // layer GEMM: W stages in shared memory (2 or 3)
     int gemm_ring;                // layer GEMM, dense: TMA ring slots
-    int gemm_skip;                // experiment (SKAN_GEMM_SKIP): 1 = producers skip W, 2 = skip A, 3 = both
+    int gemm_skip;                // experiment (SKAN_GEMM_SKIP): 16 = three N=128 MMAs per K step, 32 = two N=256
 };
 
 // Batch-1 persistent head kernel (skan_head_b1.cu).
