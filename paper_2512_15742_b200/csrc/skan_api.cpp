@@ -750,23 +750,26 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
         }
     } else {
         ws->last_x = x;
-        if (B == 1 && h->b1_ok && ws->b1_part) {
-            // the whole head in one persistent cooperative kernel
-            skan::HeadB1Args a = h->b1_plan;
-            a.x = x;
-            a.y = y;
-            const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
-            a.part[0] = ws->b1_part;
-            a.part[1] = ws->b1_part + n;
-            a.x_tma = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (h->in_dim % 2 == 0);
-            a.done = ws->b1_done;
-            a.epoch = ws->b1_epoch;
-            ws->b1_epoch += static_cast<unsigned>(h->b1_grid);  // every CTA arrives once
-            a.err = d.err;
-            a.timeline = ws->b1_timeline;
-            skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s);
+        if (B <= skan::kB1MaxBatch && h->b1_ok && ws->b1_part) {
+            // the whole head in one persistent cooperative kernel per sample
+            // (B = 2: two back-to-back launches beat the multi-kernel path)
+            for (int b = 0; b < B; ++b) {
+                skan::HeadB1Args a = h->b1_plan;
+                a.x = x + static_cast<size_t>(b) * h->in_dim;
+                a.y = y + static_cast<size_t>(b) * h->out_dim;
+                const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
+                a.part[0] = ws->b1_part;
+                a.part[1] = ws->b1_part + n;
+                a.x_tma = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (h->in_dim % 2 == 0);
+                a.done = ws->b1_done;
+                a.epoch = ws->b1_epoch;
+                ws->b1_epoch += static_cast<unsigned>(h->b1_grid);  // every CTA arrives once
+                a.err = d.err;
+                a.timeline = ws->b1_timeline;
+                skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s);
+            }
             skan::cuda_check(cudaGetLastError(), "kernel launch");
-            return 1;
+            return B;
         }
         const std::vector<skan::LaunchCfg> cfg = plan_head(h, B);
         bool chained = false;

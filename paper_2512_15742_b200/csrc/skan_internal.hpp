@@ -195,7 +195,8 @@ void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint3
 
 // Tensor-core layer GEMM (skan_gemm.cu), kind 4 of LaunchCfg: two launches
 // (the GEMM over input splits, then the fixed-order split reduction).
-constexpr int kGemmMinBatch = 3;  // smallest batch routed to the tensor-core layer GEMM (default)
+constexpr int kB1MaxBatch = 3;     // batches served by per-sample persistent batch-1 launches
+constexpr int kGemmMinBatch = 3;  // smallest batch routed to the tensor-core layer GEMM (default; heads the batch-1 kernel takes use it from 4)
 extern int g_gemm_min_batch;      // current threshold (skan_debug_set_gemm_min_batch)
 bool gemm_supported(const DevLayer& L);
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms);

@@ -160,11 +160,13 @@ def test_fast_mode_headline_head(torch_cuda):
     cn = synthetic.synthetic_head()
     tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
     model = hq.build_model(cn)
-    for batch in (1, 4):
+    for batch in (1, 2, 3, 4):  # 1-3: per-sample persistent launches; 4: tensor-core GEMM
         x = synthetic.synthetic_inputs(batch, 2048, seed=30 + batch)
         want, _ = oracle.port_forward(tables, x, batch)
-        got, _ = _gpu_forward(model, x, batch, "fast")
+        got, ws = _gpu_forward(model, x, batch, "fast")
         assert_close(got, want, l1_scale(tables, x, batch))
+        if batch <= 3:
+            assert ws.last_launches() == batch
 
 
 def test_fast_mode_headline_head_batch256(torch_cuda):
