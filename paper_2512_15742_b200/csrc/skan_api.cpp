@@ -229,6 +229,8 @@ struct skan_workspace {
     double* yout = nullptr;  // staging for host outputs
     uint64_t partial_floats = 0;
     int* h_err = nullptr;    // pinned
+    int* zc_err_h = nullptr; // pinned + mapped error flag of the zero-copy host path (host view)
+    int* zc_err_d = nullptr; //   ... and its device alias
     cudaStream_t last_stream = nullptr;
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
@@ -729,7 +731,7 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const std::vector<
 //          each layer's last CTAs write the next layer's brackets)
 //   exact: locate -> gather_exact -> locate -> gather_exact ...
 int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B, double* y,
-                  bool exact, cudaStream_t s) {
+                  bool exact, cudaStream_t s, int* err_flag = nullptr) {
     const int nl = static_cast<int>(h->dl.size());
     auto& d = ws->d;
     int launches = 0;
@@ -764,7 +766,7 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
                 a.done = ws->b1_done;
                 a.epoch = ws->b1_epoch;
                 ws->b1_epoch += static_cast<unsigned>(h->b1_grid);  // every CTA arrives once
-                a.err = d.err;
+                a.err = err_flag ? err_flag : d.err;
                 a.timeline = ws->b1_timeline;
                 skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s);
             }
@@ -972,6 +974,10 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
         skan::cuda_check(cudaMallocHost(&ws->h_err, sizeof(int)), "cudaMallocHost");
         *ws->h_err = 0;
+        skan::cuda_check(cudaHostAlloc(&ws->zc_err_h, sizeof(int), cudaHostAllocMapped), "cudaHostAlloc");
+        *ws->zc_err_h = 0;
+        skan::cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->zc_err_d), ws->zc_err_h, 0),
+                         "cudaHostGetDevicePointer");
         skan::cuda_check(cudaMemset(ws->d.err, 0, sizeof(int)), "cudaMemset");
         *out = ws.release();
     });
@@ -983,6 +989,7 @@ skan_status skan_workspace_destroy(skan_workspace* ws) {
         DeviceGuard g(ws->device);
         for (void* p : ws->allocs) cudaFree(p);
         if (ws->h_err) cudaFreeHost(ws->h_err);
+        if (ws->zc_err_h) cudaFreeHost(ws->zc_err_h);
         delete ws;
     });
 }
@@ -991,6 +998,19 @@ uint64_t skan_workspace_interp_ops(const skan_workspace* ws) { return ws ? ws->i
 int skan_workspace_max_batch(const skan_workspace* ws) { return ws ? ws->max_batch : 0; }
 int skan_workspace_width(const skan_workspace* ws) { return ws ? ws->width : 0; }
 int skan_workspace_last_launches(const skan_workspace* ws) { return ws ? ws->last_launches : 0; }
+
+// Device alias of a page-locked, mapped host buffer (cudaHostAlloc /
+// cudaMallocHost / cudaHostRegister'd memory, e.g. torch pin_memory), or
+// null for pageable memory.
+const double* mapped_alias(const double* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free error of an unknown pointer
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+    return static_cast<const double*>(at.devicePointer);
+}
 
 skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* inputs,
                          uint64_t n_inputs, int batch, double* outputs, uint64_t n_outputs,
@@ -1011,6 +1031,25 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
         ws->last_stream = s;
         ws->last_launches = 0;
         if (batch == 0) return;
+        // Low-overhead host path: small fast-mode batches the persistent
+        // kernel serves, with a page-locked output buffer: x goes over in one
+        // H2D copy (every CTA reads all of it, so it must sit in HBM/L2), the
+        // kernel writes y straight into host memory and reports a non-finite
+        // input in a mapped host flag: copy + launch + sync instead of
+        // memset + copy + launch + two D2H copies + sync.
+        if (host && !exact && batch <= skan::kB1MaxBatch && batch <= ws->max_batch && h->b1_ok && ws->b1_part) {
+            double* dy = const_cast<double*>(mapped_alias(outputs));
+            if (dy) {
+                *ws->zc_err_h = 0;
+                skan::cuda_check(cudaMemcpyAsync(ws->xin, inputs, static_cast<size_t>(batch) * in * 8,
+                                                 cudaMemcpyHostToDevice, s), "H2D inputs");
+                ws->last_launches = enqueue_chunk(h, ws, ws->xin, batch, dy, false, s, ws->zc_err_d);
+                ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;
+                skan::cuda_check(cudaStreamSynchronize(s), "forward");
+                if (*static_cast<volatile int*>(ws->zc_err_h)) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+                return;
+            }
+        }
         skan::cuda_check(cudaMemsetAsync(ws->d.err, 0, sizeof(int), s), "reset error flag");
         for (int b0 = 0; b0 < batch; b0 += ws->max_batch) {
             const int B = std::min(ws->max_batch, batch - b0);

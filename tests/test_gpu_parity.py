@@ -475,6 +475,46 @@ def test_profile_gemm_hook(torch_cuda):
     assert _lib.lib().skan_profile_gemm(model.handle, ws.handle, 0, 1, s, None) == 3  # SKAN_CONTRACT_ERROR
 
 
+def test_zero_copy_host_forward(torch_cuda):
+    """Small fast-mode batches with a page-locked output buffer take the
+    low-overhead host path (one H2D copy, the persistent kernel writes y to
+    host memory, mapped error flag): bitwise equal to the device-pointer
+    forward; a non-finite input still raises ValueError; pageable buffers
+    keep the copy path."""
+    import ctypes as C
+    from paper_2512_15742_b200 import _lib
+    torch = torch_cuda
+    cn = synthetic.synthetic_head()
+    model = hq.build_model(cn)
+    ws = hq.make_workspace(model, 8)
+    L = _lib.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for batch in (1, 2, 3):
+        x = synthetic.synthetic_inputs(batch, 2048, seed=90 + batch)
+        xp = torch.from_numpy(x).pin_memory()
+        yp = torch.zeros(batch * 20, dtype=torch.float64).pin_memory()
+        _lib.check(L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), batch, yp.data_ptr(),
+                                  yp.numel(), hq.MODE_FAST, _lib.SKAN_PTR_HOST, s))
+        assert ws.last_launches() == batch
+        dx = torch.from_numpy(x).cuda()
+        dy = torch.zeros(batch * 20, dtype=torch.float64, device="cuda")
+        hq.forward_async(model, dx, batch, dy, ws, stream=s)
+        ws.check()
+        assert np.array_equal(_bits(yp.numpy()), _bits(dy.cpu().numpy()))
+        yn = np.zeros(batch * 20)  # pageable: copy path, same result
+        hq.compressed_forward(model, x, batch, yn, ws, mode="fast")
+        assert np.array_equal(_bits(yn), _bits(yp.numpy()))
+    xp[5] = float("nan")
+    rc = L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 3, yp.data_ptr(), yp.numel(),
+                        hq.MODE_FAST, _lib.SKAN_PTR_HOST, s)
+    assert rc == 2  # SKAN_VALUE_ERROR
+    x = synthetic.synthetic_inputs(1, 2048, seed=5)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.zeros(20, dtype=torch.float64).pin_memory()
+    _lib.check(L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 1, yp.data_ptr(), yp.numel(),
+                              hq.MODE_FAST, _lib.SKAN_PTR_HOST, s))  # the flag was reset
+
+
 def test_hot_swap_refills_a_resident_head(torch_cuda):
     """skan_head_swap: a head (batch-1 persistent path and the multi-kernel
     path) refilled in place serves the new tables bitwise in exact mode and
