@@ -128,11 +128,13 @@ uint64_t device_bytes(const skan_layer_header& h) {
     if (fmt == skan::FMT_I8_R32) {
         b = add_checked(b, align_up(mul_checked(e, 4)));        // records
         b = add_checked(b, align_up(cb8));
+        b = add_checked(b, align_up(cb8));                      // biased copy (tensor-core GEMM)
         b = add_checked(b, align_up(pairs));
     } else if (fmt == skan::FMT_I8_WIDE) {
         b = add_checked(b, align_up(mul_checked(e, 4)));        // u32 index
         b = add_checked(b, align_up(mul_checked(e, 2)));        // gain|bias codes
         b = add_checked(b, align_up(cb8));
+        b = add_checked(b, align_up(cb8));                      // biased copy (tensor-core GEMM)
         b = add_checked(b, align_up(pairs));
     } else {
         if (h.k > 1) b = add_checked(b, align_up(mul_checked(e, 4)));  // u32 index
@@ -537,6 +539,11 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
                 }
                 d.rs = static_cast<int>(rs);
                 d.cb8 = static_cast<const int8_t*>(put(padded.data(), padded.size()));
+                // the same rows with every code biased to u = c ^ 0x80: the GEMM
+                // builds 2^23 + u with one byte permute (no XOR per element)
+                std::vector<uint8_t> biased(padded.size());
+                for (size_t q = 0; q < padded.size(); ++q) biased[q] = static_cast<uint8_t>(padded[q]) ^ 0x80u;
+                d.cb8u = static_cast<const uint8_t*>(put(biased.data(), biased.size()));
                 d.pair8 = static_cast<const uint16_t*>(put(pairs.data(), pairs.size() * 2));
                 break;
             }

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                 const uint32_t r = recn[v];
                 const uint32_t k = FMT == FMT_I8_R32 ? (r & 0xFFFFu) : kn[v];
                 const uint32_t gb = FMT == FMT_I8_R32 ? (r >> 16) : r;  // gain code | bias code << 8
-                st.er[v].row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(k) * L.rs));
+                st.er[v].row = __ldg(reinterpret_cast<const uint4*>(L.cb8u + static_cast<size_t>(k) * L.rs));
                 st.er[v].g = s_lut[gb & 0xFFu];  // float(gain(code) * codebook scale)
                 st.er[v].b = static_cast<float>(static_cast<int8_t>((gb >> 8) & 0xFFu)) * bs_f;
             }
@@ -465,13 +465,43 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                 const int il = eg + kTPC * v;
                 const uint32_t ob = rbase + (il >> 2) * kLboW + (il & 3) * 4;
                 const bool ok = cur.valid >> v & 1;
+                if constexpr (kI8) {
+                    // two knots per step in packed f32x2: 2^23 + u from one byte
+                    // permute of the biased row (u = c ^ 0x80), minus 2^23 + 128
+                    // = c exactly, then g * c + b and the tf32 remainder
+                    const float g = ok ? cur.er[v].g : 0.f, bb = ok ? cur.er[v].b : 0.f;
+                    const float2 g2 = make_float2(g, g), b2 = make_float2(bb, bb);
+                    const float2 off = make_float2(-8388736.0f, -8388736.0f);
+                    const uint32_t rw[4] = {cur.er[v].row.x, cur.er[v].row.y, cur.er[v].row.z, cur.er[v].row.w};
 #pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    if (m >= G) break;
-                    const float w = ok ? edge_w<FMT>(L, cur.er[v], m) : 0.f;
-                    const uint32_t o = ob + m * (IC / 4) * kLboW;
-                    *reinterpret_cast<float*>(st + o) = w;
-                    *reinterpret_cast<float*>(st + o + kLoRows) = tc::tf32_lo(w);
+                    for (int m = 0; m < 16; m += 2) {
+                        if (m >= G) break;
+                        const uint32_t sel0 = static_cast<uint32_t>(m & 3) | 0x7540u;
+                        const uint32_t sel1 = static_cast<uint32_t>((m + 1) & 3) | 0x7540u;
+                        float2 cf = make_float2(__uint_as_float(__byte_perm(rw[m >> 2], 0x4B000000u, sel0)),
+                                                __uint_as_float(__byte_perm(rw[(m + 1) >> 2], 0x4B000000u, sel1)));
+                        cf = __fadd2_rn(cf, off);
+                        const float2 w = __ffma2_rn(g2, cf, b2);
+                        const float2 wt = make_float2(__uint_as_float(__float_as_uint(w.x) & 0xFFFFE000u),
+                                                      __uint_as_float(__float_as_uint(w.y) & 0xFFFFE000u));
+                        const float2 lo = __fadd2_rn(w, make_float2(-wt.x, -wt.y));
+                        const uint32_t o0 = ob + m * (IC / 4) * kLboW, o1 = o0 + (IC / 4) * kLboW;
+                        *reinterpret_cast<float*>(st + o0) = w.x;
+                        *reinterpret_cast<float*>(st + o0 + kLoRows) = lo.x;
+                        if (m + 1 < G) {
+                            *reinterpret_cast<float*>(st + o1) = w.y;
+                            *reinterpret_cast<float*>(st + o1 + kLoRows) = lo.y;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) {
+                        if (m >= G) break;
+                        const float w = ok ? edge_w<FMT>(L, cur.er[v], m) : 0.f;
+                        const uint32_t o = ob + m * (IC / 4) * kLboW;
+                        *reinterpret_cast<float*>(st + o) = w;
+                        *reinterpret_cast<float*>(st + o + kLoRows) = tc::tf32_lo(w);
+                    }
                 }
             }
         }

@@ -61,6 +61,7 @@ struct DevLayer {
     const float* gain;       // FMT_F32
     const float* bias;       // FMT_F32
     const int8_t* cb8;       // int8 codebook
+    const uint8_t* cb8u;     // the same rows, codes biased to c ^ 0x80 (layer GEMM decode)
     const float* cb32;       // f32 codebook, or dense grid
     const float* lutf;       // [128] float(gain(code) * cs) — fast int8 path
     const double* lutd;      // [128] gain(code) as dequantize_gain_code returns it
