@@ -69,11 +69,12 @@ def test_headline_head_plan():
     p = hq.plan_memory(hs)
     assert p.payload_total == 12_957_696
     # device-resident form per layer: 4 B records, the int8 codebook padded to
-    # 16 B rows, the (c[m], c[m+1]) pair table, gain LUTs and bias sums
-    # (DESIGN.md "HBM layout"); everything 256 B aligned
+    # 16 B rows (twice: as stored and with the codes biased by 0x80 for the
+    # tensor-core GEMM), the (c[m], c[m+1]) pair table, gain LUTs and bias
+    # sums; everything 256 B aligned
     def al(v):
         return (v + 255) // 256 * 256
-    want = sum(2 * al(10 * 8) + al(4 * e) + al(65536 * 16) + al(65536 * 9 * 2) + al(1024) + al(2048) + al(8 * o)
+    want = sum(2 * al(10 * 8) + al(4 * e) + 2 * al(65536 * 16) + al(65536 * 9 * 2) + al(1024) + al(2048) + al(8 * o)
                for e, o in ((2048 * 1408, 1408), (1408 * 20, 20)))  # node positions + keys first
     assert p.device_total == want
     assert p.device_total < 126e6  # fits the B200 L2
