@@ -454,6 +454,33 @@ def test_fast_mode_both_engines_agree_with_oracle(torch_cuda, batch, engine):
         _lib.lib().skan_debug_set_gemm_min_batch(prev)
 
 
+@pytest.mark.parametrize("batch", [2, 3, 5, 63, 65, 129])
+def test_fast_and_exact_across_batch_routes(torch_cuda, batch):
+    """Batch sizes on both sides of every routing threshold (persistent
+    kernel <= 3, GEMM >= 3, stacked tiles <= 64, split-M tiles > 128) for an
+    odd-G int8 head, a K > 65536 wide-index head and a dense G=13 head:
+    fast within tolerance, exact bitwise (tools/parity_sweep.py runs more)."""
+    rng = np.random.default_rng(900 + batch)
+    cases = [
+        [oracle.Tables.from_runtime(r) for r in synthetic.runtime_layers(
+            synthetic.synthetic_head(dims=(129, 200, 17), k=300, grid=7, int8=True, seed=12))],
+        [oracle.Tables.from_runtime(r) for r in synthetic.runtime_layers(
+            synthetic.synthetic_head(dims=(65, 140, 9), k=70000, grid=16, int8=True, seed=13))],
+        oracle.ref_random([20, 129, 16], 13, 0.4, 8, 0, False).tables(),
+    ]
+    for tables in cases:
+        model = _upload(tables)
+        ws = hq.make_workspace(model, 256)
+        x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+        want, _ = oracle.port_forward(tables, x, batch)
+        got = np.zeros(batch * tables[-1].out_dim)
+        hq.compressed_forward(model, x, batch, got, ws, mode="fast")
+        assert_close(got, want, l1_scale(tables, x, batch))
+        ex = np.zeros_like(got)
+        hq.compressed_forward(model, x, batch, ex, ws, mode="exact")
+        assert np.array_equal(_bits(ex), _bits(want))
+
+
 def test_profile_gemm_hook(torch_cuda):
     """skan_profile_gemm launches one layer's GEMM alone after a forward and
     reports the MMA work it issues; layers off the GEMM are a ContractError."""
