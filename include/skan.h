@@ -241,7 +241,11 @@ skan_status skan_workspace_check(skan_workspace* ws);
 
 /* Multi-head forward: H heads with the same input width share one feature
  * batch (cfg5).  outputs[h] receives batch*output_dim(h) doubles.  All heads
- * and workspaces must live on the same device; device pointers only. */
+ * and workspaces must live on the same device; device pointers only.  The
+ * heads run concurrently on up to four library-owned side streams that
+ * fork from and join back into `stream` (stream-ordered: the outputs are
+ * ready when work enqueued on `stream` after this call runs); a deferred
+ * non-finite input is reported by skan_workspace_check(wss[h]). */
 skan_status skan_forward_multi(const skan_head* const* heads, skan_workspace* const* wss,
                                int n_heads, const double* d_inputs, int batch,
                                double* const* d_outputs, int mode, void* stream);

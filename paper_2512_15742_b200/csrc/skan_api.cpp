@@ -13,7 +13,9 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1160,6 +1162,35 @@ skan_status skan_workspace_check(skan_workspace* ws) {
     });
 }
 
+// Side streams for multi-head forwards (per device, created once): heads on
+// one feature batch run concurrently, filling each other's wave tails and
+// the small trailing kernels, then join the caller's stream.
+struct SidePool {
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;  // [0] fork, [1 + q] join of stream q
+    std::mutex use;                   // one multi-head enqueue at a time per device
+};
+SidePool& side_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, SidePool> pools;
+    std::lock_guard<std::mutex> lock(mu);
+    SidePool& p = pools[device];
+    if (p.streams.empty()) {
+        constexpr int kSide = 4;
+        for (int q = 0; q < kSide; ++q) {
+            cudaStream_t st;
+            skan::cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+            p.streams.push_back(st);
+        }
+        for (int q = 0; q <= kSide; ++q) {
+            cudaEvent_t ev;
+            skan::cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+            p.events.push_back(ev);
+        }
+    }
+    return p;
+}
+
 skan_status skan_forward_multi(const skan_head* const* heads, skan_workspace* const* wss, int n,
                                const double* x, int batch, double* const* ys, int mode, void* stream) {
     return guarded([&] {
@@ -1171,9 +1202,29 @@ skan_status skan_forward_multi(const skan_head* const* heads, skan_workspace* co
             if (heads[q]->device != heads[0]->device)
                 raise(SKAN_CONTRACT_ERROR, "heads must live on one device");
         }
+        if (n <= 1) {
+            for (int q = 0; q < n; ++q) {
+                const skan_status st = skan_forward_async(heads[q], wss[q], x, batch, ys[q], mode, stream);
+                if (st != SKAN_OK) raise(st, g_err.msg);
+            }
+            return;
+        }
+        DeviceGuard g(heads[0]->device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        SidePool& pool = side_pool(heads[0]->device);
+        std::lock_guard<std::mutex> lock(pool.use);
+        const int P = static_cast<int>(pool.streams.size());
+        const int used = std::min(n, P);
+        skan::cuda_check(cudaEventRecord(pool.events[0], s), "fork");
+        for (int q = 0; q < used; ++q) skan::cuda_check(cudaStreamWaitEvent(pool.streams[q], pool.events[0], 0), "fork");
         for (int q = 0; q < n; ++q) {
-            const skan_status st = skan_forward_async(heads[q], wss[q], x, batch, ys[q], mode, stream);
+            const skan_status st =
+                skan_forward_async(heads[q], wss[q], x, batch, ys[q], mode, pool.streams[q % P]);
             if (st != SKAN_OK) raise(st, g_err.msg);
+        }
+        for (int q = 0; q < used; ++q) {
+            skan::cuda_check(cudaEventRecord(pool.events[1 + q], pool.streams[q]), "join");
+            skan::cuda_check(cudaStreamWaitEvent(s, pool.events[1 + q], 0), "join");
         }
     });
 }
