@@ -15,7 +15,7 @@
 
 using namespace skan;
 
-__global__ void __launch_bounds__(128, 1) k_chunks(int chunks, int variant, long long* out) {
+__global__ void __launch_bounds__(544, 1) k_chunks(int chunks, int variant, long long* out, const uint4* gbuf) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ uint32_t s_tmem;
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(128, 1) k_chunks(int chunks, int variant, long
     const uint32_t tile_a = 128 * KC * 4, tile_w = 256 * KC * 4;  // 20 KB, 40 KB
     unsigned char* A = smem;                   // 2 buffers x (A_hi | A_lo) = 80 KB
     unsigned char* W = smem + 4 * tile_a;      // 2 stages = 80 KB
-    for (int q = threadIdx.x * 16; q < 4 * tile_a + 2 * tile_w; q += 128 * 16) {
+    for (int q = threadIdx.x * 16; q < 4 * tile_a + 2 * tile_w; q += 544 * 16) {
         uint32_t h = q * 2654435761u;
         *reinterpret_cast<float4*>(smem + q) = make_float4(__uint_as_float((h & 0x3FFFFFFF) | 0x3F000000), 0.5f, -0.25f, 1.f);
     }
@@ -32,12 +32,36 @@ __global__ void __launch_bounds__(128, 1) k_chunks(int chunks, int variant, long
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar[1])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __shared__ volatile int s_stop;
+    if (threadIdx.x == 0) s_stop = 0;
     if (threadIdx.x < 32) tc::tmem_alloc<256>(&s_tmem);
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
+    if (threadIdx.x >= 32) {
+        // producer-like traffic next to the MMAs: noise bit 64 = scattered
+        // 4-byte shared stores, bit 128 = 16-byte random global gathers
+        const int noise = variant & (64 | 128 | 256);
+        unsigned char* scratch = smem + 4 * tile_a + 2 * tile_w;  // 16 KB past the operands
+        uint32_t h = threadIdx.x * 2654435761u + blockIdx.x;
+        uint4 acc = make_uint4(0, 0, 0, 0);
+        while (noise && !s_stop) {
+#pragma unroll 4
+            for (int u = 0; u < 8; ++u) {
+                h = h * 1664525u + 1013904223u;
+                if (noise & 64)
+                    *reinterpret_cast<float*>(scratch + ((threadIdx.x * 16 + u * 4) & 0x3FFC)) = __uint_as_float(h);
+                if (noise & 128) {
+                    const uint4 v = __ldg(gbuf + (h >> 16));  // 65536 x 16 B = 1 MB
+                    acc.x ^= v.x;
+                }
+                if ((variant & 256) && u == 7) tc::fence_proxy_async();  // the producers' per-chunk proxy fence
+            }
+        }
+        if (acc.x == 0x12345678u) out[7] = acc.y;
+    }
     if (threadIdx.x < 32) {
         const uint32_t lboA = 16 * 128, lboW = 32 * 128;
         const uint64_t da0 = tc::make_desc(tc::smem_addr(A), lboA, 128);
@@ -88,6 +112,7 @@ __global__ void __launch_bounds__(128, 1) k_chunks(int chunks, int variant, long
                 : "memory");
         const long long t1 = clock64();
         if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = t1 - t0;
+        if (threadIdx.x == 0) s_stop = 1;
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -97,19 +122,25 @@ __global__ void __launch_bounds__(128, 1) k_chunks(int chunks, int variant, long
 int main() {
     long long* d;
     cudaMalloc(&d, 64);
-    const int smem = 4 * 128 * 40 * 4 + 2 * 256 * 40 * 4;
+    const int smem = 4 * 128 * 40 * 4 + 2 * 256 * 40 * 4 + 16384;
+    uint4* gbuf;
+    cudaMalloc(&gbuf, 1 << 20);
+    cudaMemset(gbuf, 1, 1 << 20);
     cudaFuncSetAttribute(k_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int chunks = 400;
     const char* names[] = {"N256+N128 (kernel)", "2 x N256", "3 x N128"};
-    for (int nc = 0; nc < 3; ++nc)
+    const int flag_list[] = {0, 16, 32, 64, 128, 192, 256 | 64, 256 | 192};
+    const char* flag_names[] = {"commit/chunk", "no commits  ", "round trip  ", "+smem stores", "+gathers    ", "+both       ",
+                                "+stores+fence", "+all+fence  "};
+    for (int nc = 0; nc < 8; ++nc)
         for (int v = 0; v < 3; ++v) {
             long long h = 0;
-            const int flags = nc == 1 ? 16 : (nc == 2 ? 32 : 0);
-            k_chunks<<<148, 128, smem>>>(chunks, v | flags, d);
-            k_chunks<<<148, 128, smem>>>(chunks, v | flags, d);
+            const int flags = flag_list[nc];
+            k_chunks<<<148, 544, smem>>>(chunks, v | flags, d, gbuf);
+            k_chunks<<<148, 544, smem>>>(chunks, v | flags, d, gbuf);
             cudaError_t e = cudaDeviceSynchronize();
             cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-            printf("%-20s %s: %7.1f clk/chunk  %s\n", names[v], nc == 1 ? "no commits  " : (nc == 2 ? "round trip  " : "commit/chunk"),
+            printf("%-20s %s: %7.1f clk/chunk  %s\n", names[v], flag_names[nc],
                    static_cast<double>(h) / chunks, e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     return 0;
