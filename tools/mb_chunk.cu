@@ -4,8 +4,11 @@
 //   variant 0: per step one M128 N256 (A_hi x [W_hi|W_lo]) + one M128 N128 (A_lo x W_hi)
 //   variant 1: per step two M128 N256
 //   variant 2: per step three M128 N128
-// with a tcgen05.commit per chunk (variant bit 4: no commits).  Prints
-// cycles per chunk.
+// with a tcgen05.commit per chunk; modes: no commits, commit/wait round
+// trip, 512 threads of scattered shared stores / random 16 B global gathers
+// / proxy fences next to the MMAs, and the kernel's two-stage
+// full/free mbarrier handshake with 512 producer threads doing no work.
+// Prints cycles per chunk.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2512_15742_b200/csrc tools/mb_chunk.cu -o tools/bin/mb_chunk
 #include <cuda_runtime.h>
 
@@ -18,6 +21,7 @@ using namespace skan;
 __global__ void __launch_bounds__(544, 1) k_chunks(int chunks, int variant, long long* out, const uint4* gbuf) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t fullb[2];
     __shared__ uint32_t s_tmem;
     const int KC = 40;
     const uint32_t tile_a = 128 * KC * 4, tile_w = 256 * KC * 4;  // 20 KB, 40 KB
@@ -30,6 +34,8 @@ __global__ void __launch_bounds__(544, 1) k_chunks(int chunks, int variant, long
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&bar[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&fullb[0])), "r"(512));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_addr(&fullb[1])), "r"(512));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __shared__ volatile int s_stop;
@@ -40,7 +46,23 @@ __global__ void __launch_bounds__(544, 1) k_chunks(int chunks, int variant, long
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = s_tmem;
-    if (threadIdx.x >= 32) {
+    auto waitp = [](uint64_t* b, unsigned par) {
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(ok)
+                : "r"(tc::smem_addr(b)), "r"(par)
+                : "memory");
+    };
+    if ((variant & 512) && threadIdx.x >= 32) {
+        // the kernel's handshake with no work: wait for chunk c-2's MMAs, fence, arrive
+        for (int c = 0; c < chunks; ++c) {
+            if (c >= 2) waitp(&bar[c & 1], ((c - 2) >> 1) & 1);
+            tc::fence_proxy_async();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&fullb[c & 1])) : "memory");
+        }
+    } else if (threadIdx.x >= 32) {
         // producer-like traffic next to the MMAs: noise bit 64 = scattered
         // 4-byte shared stores, bit 128 = 16-byte random global gathers
         const int noise = variant & (64 | 128 | 256);
@@ -71,6 +93,10 @@ __global__ void __launch_bounds__(544, 1) k_chunks(int chunks, int variant, long
         const int v = variant & 3;
         const long long t0 = clock64();
         for (int c = 0; c < chunks; ++c) {
+            if (variant & 512) {
+                waitp(&fullb[c & 1], (c >> 1) & 1);
+                tc::fence_after_sync();
+            }
             const uint64_t da = da0 + (c & 1) * ((2 * tile_a) >> 4), dw = dw0 + (c & 1) * (tile_w >> 4);
 #pragma unroll
             for (int s = 0; s < 5; ++s) {
@@ -129,10 +155,10 @@ int main() {
     cudaFuncSetAttribute(k_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int chunks = 400;
     const char* names[] = {"N256+N128 (kernel)", "2 x N256", "3 x N128"};
-    const int flag_list[] = {0, 16, 32, 64, 128, 192, 256 | 64, 256 | 192};
+    const int flag_list[] = {0, 16, 32, 64, 128, 192, 256 | 64, 256 | 192, 512};
     const char* flag_names[] = {"commit/chunk", "no commits  ", "round trip  ", "+smem stores", "+gathers    ", "+both       ",
-                                "+stores+fence", "+all+fence  "};
-    for (int nc = 0; nc < 8; ++nc)
+                                "+stores+fence", "+all+fence  ", "2-stage handshake"};
+    for (int nc = 0; nc < 9; ++nc)
         for (int v = 0; v < 3; ++v) {
             long long h = 0;
             const int flags = flag_list[nc];
