@@ -103,6 +103,8 @@ def _load_port():
         L.oracle_compressed_forward_mt.restype = C.c_int
         L.oracle_compressed_forward_mt.argtypes = [C.POINTER(OracleLayer), C.c_int, _p, C.c_int, _p, C.c_int,
                                                    C.POINTER(C.c_uint64)]
+        L.oracle_forward_l1_mt.restype = C.c_int
+        L.oracle_forward_l1_mt.argtypes = [C.POINTER(OracleLayer), C.c_int, _p, C.c_int, _p, _p, C.c_int]
         _port = L
     return _port
 
@@ -262,6 +264,22 @@ def port_forward(tables: Sequence[Tables], inputs: np.ndarray, batch: int, threa
     if rc:
         raise RefError(rc, "oracle forward failed")
     return out, ops.value
+
+
+def port_forward_l1(tables: Sequence[Tables], inputs: np.ndarray, batch: int, threads: int = 1):
+    """The port's forward plus the fast mode's per-output tolerance scale
+    max(|y|, sum_i |term_ij|) of the last layer (tests/helpers.py): returns
+    (outputs, scale).  Outputs are bitwise those of port_forward."""
+    L = port()
+    arr = _c_layers(tables)
+    x = np.ascontiguousarray(inputs, dtype=np.float64)
+    out = np.zeros(batch * tables[-1].out_dim, dtype=np.float64)
+    scale = np.zeros_like(out)
+    rc = L.oracle_forward_l1_mt(arr, len(tables), x.ctypes.data, batch, out.ctypes.data, scale.ctypes.data,
+                                max(1, threads))
+    if rc:
+        raise RefError(rc, "oracle forward failed")
+    return out, scale
 
 
 class RefModel:

@@ -195,9 +195,13 @@ static uint32_t edge_index(const oracle_layer* l, uint64_t e) {
 }
 
 /* lutham.cpp:770-815 */
-int oracle_forward_layer(const oracle_layer* l, const double* x, double* y, uint64_t* ops) {
+/* forward_layer with an optional per-output L1 accumulator: l1[j] += |term_ij|
+ * (test tolerance scale only; y is computed exactly as without it). */
+static int forward_layer_l1(const oracle_layer* l, const double* x, double* y, uint64_t* ops, double* l1) {
     const int in = (int)l->in_dim, out = (int)l->out_dim, G = (int)l->grid_size;
     for (int j = 0; j < out; ++j) y[j] = 0.0;
+    if (l1)
+        for (int j = 0; j < out; ++j) l1[j] = 0.0;
     for (int i = 0; i < in; ++i) {
         int idx, cl;
         double t;
@@ -206,8 +210,11 @@ int oracle_forward_layer(const oracle_layer* l, const double* x, double* y, uint
         const uint64_t e0 = (uint64_t)i * (uint64_t)out;
         if (l->k == 0) { /* dense branch 778-791 */
             const float* base = l->table_f32 + e0 * (uint64_t)G + (uint64_t)idx;
-            for (int j = 0; j < out; ++j, base += G)
-                y[j] += (double)base[0] * w0 + (double)base[1] * t;
+            for (int j = 0; j < out; ++j, base += G) {
+                const double term = (double)base[0] * w0 + (double)base[1] * t;
+                y[j] += term;
+                if (l1) l1[j] += fabs(term);
+            }
         } else { /* compressed branch 793-814 */
             for (int j = 0; j < out; ++j) {
                 const uint64_t e = e0 + (uint64_t)j;
@@ -225,12 +232,19 @@ int oracle_forward_layer(const oracle_layer* l, const double* x, double* y, uint
                     c0 = (double)l->table_f32[row];
                     c1 = (double)l->table_f32[row + 1];
                 }
-                y[j] += (g * c0 + b) * w0 + (g * c1 + b) * t;
+                const double term = (g * c0 + b) * w0 + (g * c1 + b) * t;
+                y[j] += term;
+                if (l1) l1[j] += fabs(term);
             }
         }
         *ops += (uint64_t)out;
     }
     return ORACLE_OK;
+}
+
+/* lutham.cpp:770-815 */
+int oracle_forward_layer(const oracle_layer* l, const double* x, double* y, uint64_t* ops) {
+    return forward_layer_l1(l, x, y, ops, NULL);
 }
 
 static int max_width(const oracle_layer* layers, int n) {
@@ -242,9 +256,11 @@ static int max_width(const oracle_layer* layers, int n) {
     return (int)w;
 }
 
-/* lutham.cpp:819-850 */
-int oracle_compressed_forward(const oracle_layer* layers, int n, const double* inputs, int batch,
-                              double* outputs, double* scratch, uint64_t* interp_ops) {
+/* lutham.cpp:819-850.  scale (optional): per output max(|y|, sum_i |term_ij|)
+ * of the last layer (the fast mode's L1 tolerance scale, tests only);
+ * scratch then holds 3*max_width doubles. */
+static int forward_impl(const oracle_layer* layers, int n, const double* inputs, int batch,
+                        double* outputs, double* scratch, uint64_t* interp_ops, double* scale) {
     if (n <= 0) return ORACLE_SHAPE;
     if (batch < 0) return ORACLE_SHAPE;
     const int width = max_width(layers, n);
@@ -253,18 +269,26 @@ int oracle_compressed_forward(const oracle_layer* layers, int n, const double* i
     for (int s = 0; s < batch; ++s) {
         double* cur = scratch;
         double* nxt = scratch + width;
+        double* l1 = scale ? scratch + 2 * (size_t)width : NULL;
         memcpy(cur, inputs + (size_t)s * in, in * sizeof(double));
         for (int l = 0; l < n; ++l) {
-            int rc = oracle_forward_layer(&layers[l], cur, nxt, &ops);
+            int rc = forward_layer_l1(&layers[l], cur, nxt, &ops, l == n - 1 ? l1 : NULL);
             if (rc) return rc;
             double* tmp = cur;
             cur = nxt;
             nxt = tmp;
         }
         memcpy(outputs + (size_t)s * out, cur, out * sizeof(double));
+        if (scale)
+            for (size_t j = 0; j < out; ++j) scale[(size_t)s * out + j] = fabs(cur[j]) > l1[j] ? fabs(cur[j]) : l1[j];
     }
     if (interp_ops) *interp_ops += ops;
     return ORACLE_OK;
+}
+
+int oracle_compressed_forward(const oracle_layer* layers, int n, const double* inputs, int batch,
+                              double* outputs, double* scratch, uint64_t* interp_ops) {
+    return forward_impl(layers, n, inputs, batch, outputs, scratch, interp_ops, NULL);
 }
 
 typedef struct {
@@ -272,24 +296,25 @@ typedef struct {
     int n, s0, s1, rc;
     const double* inputs;
     double* outputs;
+    double* scale;
     uint64_t ops;
 } mt_job;
 
 static void* mt_run(void* p) {
     mt_job* j = (mt_job*)p;
     const int width = max_width(j->layers, j->n);
-    double* scratch = (double*)malloc(sizeof(double) * 2 * (size_t)(width > 0 ? width : 1));
+    double* scratch = (double*)malloc(sizeof(double) * 3 * (size_t)(width > 0 ? width : 1));
     const size_t in = j->layers[0].in_dim, out = j->layers[j->n - 1].out_dim;
     j->ops = 0;
-    j->rc = oracle_compressed_forward(j->layers, j->n, j->inputs + (size_t)j->s0 * in,
-                                      j->s1 - j->s0, j->outputs + (size_t)j->s0 * out, scratch,
-                                      &j->ops);
+    j->rc = forward_impl(j->layers, j->n, j->inputs + (size_t)j->s0 * in, j->s1 - j->s0,
+                         j->outputs + (size_t)j->s0 * out, scratch, &j->ops,
+                         j->scale ? j->scale + (size_t)j->s0 * out : NULL);
     free(scratch);
     return NULL;
 }
 
-int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double* inputs,
-                                 int batch, double* outputs, int threads, uint64_t* interp_ops) {
+static int forward_mt(const oracle_layer* layers, int n, const double* inputs, int batch,
+                      double* outputs, int threads, uint64_t* interp_ops, double* scale) {
     if (n <= 0 || batch < 0) return ORACLE_SHAPE;
     if (threads < 1) threads = 1;
     if (threads > batch) threads = batch > 0 ? batch : 1;
@@ -302,6 +327,7 @@ int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double
         jobs[t].s1 = (int)((long long)batch * (t + 1) / threads);
         jobs[t].inputs = inputs;
         jobs[t].outputs = outputs;
+        jobs[t].scale = scale;
         pthread_create(&tids[t], NULL, mt_run, &jobs[t]);
     }
     int rc = ORACLE_OK;
@@ -313,6 +339,16 @@ int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double
     free(jobs);
     free(tids);
     return rc;
+}
+
+int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double* inputs,
+                                 int batch, double* outputs, int threads, uint64_t* interp_ops) {
+    return forward_mt(layers, n, inputs, batch, outputs, threads, interp_ops, NULL);
+}
+
+int oracle_forward_l1_mt(const oracle_layer* layers, int n, const double* inputs, int batch,
+                         double* outputs, double* scale, int threads) {
+    return forward_mt(layers, n, inputs, batch, outputs, threads, NULL, scale);
 }
 
 /* gsb.cpp:23-30 (dist2), 62-73 (nearest_row), 275-286 (assign_indices). */

@@ -83,6 +83,12 @@ int oracle_compressed_forward(const oracle_layer* layers, int n, const double* i
 int oracle_compressed_forward_mt(const oracle_layer* layers, int n, const double* inputs,
                                  int batch, double* outputs, int threads, uint64_t* interp_ops);
 
+/* The forward above plus, per output of the last layer, the fast mode's
+ * tolerance scale max(|y|, sum_i |term_ij|) with term_ij the reference's
+ * per-edge interpolation (lutham.cpp:791/810).  Tests only. */
+int oracle_forward_l1_mt(const oracle_layer* layers, int n, const double* inputs, int batch,
+                         double* outputs, double* scale, int threads);
+
 /* assign_indices, gsb.cpp:275-286 with nearest_row 62-73 and dist2 23-30:
  * per shape (n x dim row-major) the codebook row (k x dim) of least
  * squared distance, accumulated in dim order as s += (a-b)*(a-b) (no

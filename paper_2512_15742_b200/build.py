@@ -22,6 +22,13 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=of
          "-I" + os.path.join(ROOT, "include")]
 
 
+OBJDIR = os.path.join(HERE, "build_obj")
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJDIR, os.path.basename(src) + ".o")
+
+
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
         return False
@@ -30,12 +37,30 @@ def up_to_date() -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Each translation unit compiles to its own object in parallel (only
+    stale ones are rebuilt), then one nvcc link produces libskan.so."""
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", OUT + ".tmp", *SOURCES]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJDIR, exist_ok=True)
+    newest_hdr = max(os.path.getmtime(p) for p in HEADERS + [__file__])
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = _obj(src)
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(src)
+                and os.path.getmtime(obj) >= newest_hdr):
+            return
+        cmd = [NVCC, *ARCH, *compile_flags, "-c", "-o", obj + ".tmp", src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(obj + ".tmp", obj)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(compile_one, SOURCES))
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *[_obj(s) for s in SOURCES]]
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT

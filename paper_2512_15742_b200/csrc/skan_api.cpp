@@ -16,6 +16,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <shared_mutex>
 #include <string>
 #include <vector>
 
@@ -220,6 +221,10 @@ struct skan_head {
     int b1_grid = 0;
     size_t b1_smem = 0;
     skan::HeadB1Args b1_plan{};  // layers + shared-memory plan; per-call pointers filled at launch
+    // Forwards hold it shared while they read the layer views and enqueue
+    // (host-buffer calls: until they return); skan_head_swap holds it
+    // exclusively, so a swap never races a forward's reads of dl/b1_plan.
+    mutable std::shared_mutex swap_mu;
 };
 
 struct skan_workspace {
@@ -242,6 +247,11 @@ struct skan_workspace {
     unsigned* b1_done = nullptr;     // its monotonic last-layer arrival counter
     unsigned b1_epoch = 0;           // value of *b1_done when the next launch starts
     unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
+    // Fast-path launch plans for every batch 1..max_batch, [B-1][layer],
+    // built at creation (forward allocates nothing); rebuilt in place if the
+    // GEMM routing threshold changes (skan_debug_set_gemm_min_batch).
+    std::vector<skan::LaunchCfg> plans;
+    int plans_gemm_min = -1;
     std::vector<void*> allocs;
 };
 
@@ -657,23 +667,31 @@ skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
 // Fast-path kernel choice for every layer at batch B.  A layer may use the
 // pair-plane kernel only if it has a successor and its predecessor did not
 // (the successor reduces its partials while locating).
-std::vector<skan::LaunchCfg> plan_head(const skan_head* h, int B) {
+void plan_head_into(const skan_head* h, int B, skan::LaunchCfg* cfg) {
     const int nl = static_cast<int>(h->dl.size());
-    std::vector<skan::LaunchCfg> cfg(nl);
     for (int l = 0; l < nl; ++l) {
         const bool allow = l + 1 < nl && !(l > 0 && cfg[l - 1].kind == 2);
         cfg[l] = skan::choose_cfg(h->dl[l], B, false, h->num_sms, allow);
     }
+}
+
+std::vector<skan::LaunchCfg> plan_head(const skan_head* h, int B) {
+    std::vector<skan::LaunchCfg> cfg(h->dl.size());
+    plan_head_into(h, B, cfg.data());
     return cfg;
 }
 
 // Largest split-partial buffer (floats) and per-layer counter count any
 // batch up to max_batch needs on the fast path.
-void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, uint64_t* counters) {
+void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, uint64_t* counters,
+                   std::vector<skan::LaunchCfg>* plans) {
     uint64_t best = 0, cnt = 1;
+    const size_t nl = h->dl.size();
+    plans->assign(static_cast<size_t>(max_batch) * nl, skan::LaunchCfg{});
     for (int b = 1; b <= max_batch; ++b) {
-        const std::vector<skan::LaunchCfg> cfg = plan_head(h, b);
-        for (size_t l = 0; l < cfg.size(); ++l) {
+        skan::LaunchCfg* cfg = plans->data() + static_cast<size_t>(b - 1) * nl;
+        plan_head_into(h, b, cfg);
+        for (size_t l = 0; l < nl; ++l) {
             const skan::LaunchCfg& c = cfg[l];
             best = std::max<uint64_t>(best, static_cast<uint64_t>(c.nsplit) * b * h->dl[l].out);
             cnt = std::max<uint64_t>(cnt, static_cast<uint64_t>(c.jt) * c.st);
@@ -683,12 +701,23 @@ void scratch_needs(const skan_head* h, int max_batch, uint64_t* partial_floats, 
     *counters = cnt;
 }
 
+// The workspace's plan of batch B: no allocation, the table is sized at
+// workspace creation for every batch up to max_batch.
+const skan::LaunchCfg* ws_plan(const skan_head* h, skan_workspace* ws, int B) {
+    const size_t nl = h->dl.size();
+    if (ws->plans_gemm_min != skan::g_gemm_min_batch) {
+        for (int b = 1; b <= ws->max_batch; ++b) plan_head_into(h, b, ws->plans.data() + (b - 1) * nl);
+        ws->plans_gemm_min = skan::g_gemm_min_batch;
+    }
+    return ws->plans.data() + static_cast<size_t>(B - 1) * nl;
+}
+
 // One fused fast-path layer launch (plus the standalone locate in front of
 // layer 0 when that kernel does not locate inline).  Layer l reads brackets
 // bm[l&1] and its finisher writes layer l+1's into bm[(l+1)&1]; split
 // partials ping-pong between two buffers so a layer can reduce its
 // predecessor's partials while writing its own.
-int launch_layer_fast(const skan_head* h, skan_workspace* ws, const std::vector<skan::LaunchCfg>& cfg, int l,
+int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::LaunchCfg* cfg, int l,
                       const double* x, int B, double* out, bool chained, cudaStream_t s) {
     auto& d = ws->d;
     const int nl = static_cast<int>(h->dl.size());
@@ -774,15 +803,16 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
                 a.x_tma = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (h->in_dim % 2 == 0);
                 a.done = ws->b1_done;
                 a.epoch = ws->b1_epoch;
-                ws->b1_epoch += static_cast<unsigned>(h->b1_grid);  // every CTA arrives once
                 a.err = err_flag ? err_flag : d.err;
                 a.timeline = ws->b1_timeline;
-                skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s);
+                skan::cuda_check(skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s), "kernel launch");
+                // every CTA arrives once; advanced only for a launch that was accepted
+                ws->b1_epoch += static_cast<unsigned>(h->b1_grid);
             }
             skan::cuda_check(cudaGetLastError(), "kernel launch");
             return B;
         }
-        const std::vector<skan::LaunchCfg> cfg = plan_head(h, B);
+        const skan::LaunchCfg* cfg = ws_plan(h, ws, B);
         bool chained = false;
         for (int l = 0; l < nl; ++l) {
             launches += launch_layer_fast(h, ws, cfg, l, x, B, l + 1 < nl ? d.act[l & 1] : y, chained, s);
@@ -800,11 +830,31 @@ void check_head_batch(const skan_head* h, int batch) {
     if (batch < 0) raise(SKAN_SHAPE_ERROR, "batch must be nonnegative");
 }
 
+// A workspace's buffers are sized for the head it was made for (staging,
+// split partials, arrival counters, the batch-1 partials).  Another head may
+// use it only if every layer has the same shape, grid, codebook size and
+// format, which fixes all of those sizes (e.g. the same-architecture heads
+// of a multi-head server).  The reference checks only the width
+// (lutham.cpp:833); a wider check is needed here because the device scratch
+// is planned per head.
+bool same_layout(const skan_head* a, const skan_head* b) {
+    if (a == b) return true;
+    if (!a || !b) return false;
+    if (a->dl.size() != b->dl.size() || a->b1_ok != b->b1_ok || a->b1_grid != b->b1_grid) return false;
+    for (size_t l = 0; l < a->dl.size(); ++l) {
+        const DevLayer &x = a->dl[l], &y = b->dl[l];
+        if (x.in != y.in || x.out != y.out || x.G != y.G || x.K != y.K || x.fmt != y.fmt) return false;
+    }
+    return true;
+}
+
 void check_workspace_for(const skan_head* h, const skan_workspace* ws) {
     if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
     if (ws->width < h->max_width)
         raise(SKAN_CONTRACT_ERROR, "workspace is smaller than the model's widest layer");
     if (ws->device != h->device) raise(SKAN_CONTRACT_ERROR, "workspace lives on another device");
+    if (!same_layout(h, ws->head))
+        raise(SKAN_CONTRACT_ERROR, "workspace was made for a head with a different layer layout");
 }
 
 void check_forward_args(const skan_head* h, const skan_workspace* ws, int batch) {
@@ -877,6 +927,10 @@ skan_status skan_head_swap(skan_head* h, const skan_layer_desc* layers, int n, v
         std::vector<skan_layer_plan> lp(n);
         const skan_memory_plan tot = plan(hs.data(), n, lp.data());
         DeviceGuard g(h->device);
+        // No forward reads the host views while we hold the lock; forwards
+        // already enqueued on any stream finish before the tables change.
+        std::unique_lock<std::shared_mutex> lock(h->swap_mu);
+        skan::cuda_check(cudaDeviceSynchronize(), "drain in-flight forwards before a swap");
         h->lplan = lp;
         h->totals = tot;
         upload(h, st, /*swap=*/true, static_cast<cudaStream_t>(stream));
@@ -966,7 +1020,8 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         ws->d.btf = static_cast<float*>(alloc(2 * act * 4));
         ws->d.btd = static_cast<double*>(alloc(act * 8));
         uint64_t ncnt = 0;
-        scratch_needs(h, max_batch, &ws->partial_floats, &ncnt);
+        scratch_needs(h, max_batch, &ws->partial_floats, &ncnt, &ws->plans);
+        ws->plans_gemm_min = skan::g_gemm_min_batch;
         ws->d.partial = static_cast<float*>(alloc(2 * ws->partial_floats * 4));  // ping-pong
         ws->d.counter_stride = ncnt;
         const size_t cbytes = ncnt * h->dl.size() * sizeof(unsigned);
@@ -1037,6 +1092,7 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
         const bool host = (ptr_flags & SKAN_PTR_DEVICE) == 0;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         DeviceGuard g(h->device);
+        std::shared_lock<std::shared_mutex> lock(h->swap_mu);
         ws->last_stream = s;
         ws->last_launches = 0;
         if (batch == 0) return;
@@ -1053,9 +1109,9 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
                 skan::cuda_check(cudaMemcpyAsync(ws->xin, inputs, static_cast<size_t>(batch) * in * 8,
                                                  cudaMemcpyHostToDevice, s), "H2D inputs");
                 ws->last_launches = enqueue_chunk(h, ws, ws->xin, batch, dy, false, s, ws->zc_err_d);
-                ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;
                 skan::cuda_check(cudaStreamSynchronize(s), "forward");
                 if (*static_cast<volatile int*>(ws->zc_err_h)) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+                ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;  // after success, as lutham.cpp:849
                 return;
             }
         }
@@ -1074,13 +1130,16 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
                 ws->last_launches += enqueue_chunk(h, ws, x, B, y, exact, s);
             }
         }
-        ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;
         skan::cuda_check(cudaMemcpyAsync(ws->h_err, ws->d.err, sizeof(int), cudaMemcpyDeviceToHost, s),
                          "error flag");
         if (host) {
             skan::cuda_check(cudaStreamSynchronize(s), "forward");
             if (*ws->h_err) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
         }
+        // host buffers: counted after the call succeeded (lutham.cpp:849);
+        // device buffers: at enqueue (a non-finite input surfaces later, in
+        // skan_workspace_check)
+        ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;
     });
 }
 
@@ -1109,7 +1168,7 @@ skan_status skan_profile_gather(const skan_head* h, skan_workspace* ws, int laye
             if (!ws->last_x) raise(SKAN_CONTRACT_ERROR, "run a forward on this workspace first");
             if (layer > 0 && plan_head(h, batch)[layer - 1].kind == 2)
                 raise(SKAN_CONTRACT_ERROR, "layer consumes pair-plane partials; profile it with its predecessor");
-            launch_layer_fast(h, ws, plan_head(h, batch), layer, ws->last_x, batch, ws->d.act[layer & 1], false, s);
+            launch_layer_fast(h, ws, plan_head(h, batch).data(), layer, ws->last_x, batch, ws->d.act[layer & 1], false, s);
         }
         skan::cuda_check(cudaGetLastError(), "profile launch");
     });
@@ -1122,7 +1181,7 @@ skan_status skan_profile_gemm(const skan_head* h, skan_workspace* ws, int layer,
         if (layer < 0 || layer >= static_cast<int>(h->dl.size())) raise(SKAN_SHAPE_ERROR, "layer index out of range");
         if (batch < 1 || batch > ws->max_batch) raise(SKAN_CONTRACT_ERROR, "batch outside the workspace capacity");
         if (!ws->last_x) raise(SKAN_CONTRACT_ERROR, "run a forward on this workspace first");
-        const std::vector<skan::LaunchCfg> cfg = plan_head(h, batch);
+        const skan::LaunchCfg* cfg = ws_plan(h, ws, batch);
         if (cfg[layer].kind != 4) raise(SKAN_CONTRACT_ERROR, "layer does not run on the tensor-core GEMM at this batch");
         DeviceGuard g(h->device);
         auto& d = ws->d;

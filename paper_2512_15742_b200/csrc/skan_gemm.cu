@@ -862,7 +862,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     a.gemm_skip = skip_env;
     const bool stack = c.spt == 64;
     void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic) : gemm_kernel<false>(a.L.fmt, c.ic);
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+    ensure_smem(k, c.smem);
     static const int carve_env = [] {
         const char* e = std::getenv("SKAN_GEMM_CARVEOUT");  // experiment: shared-memory carve-out percent
         return e ? std::atoi(e) : -1;

@@ -642,7 +642,7 @@ int head_b1_max_grid(size_t smem, int num_sms) {
     return per_sm >= 1 ? num_sms : 0;
 }
 
-void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s) {
+cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kT);
@@ -653,7 +653,7 @@ void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s) 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_head_b1, h);
+    return cudaLaunchKernelEx(&cfg, k_head_b1, h);
 }
 
 }  // namespace skan

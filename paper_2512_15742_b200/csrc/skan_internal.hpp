@@ -33,6 +33,35 @@ inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) raise(SKAN_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size) and thread: a fixed per-thread table, so the per-call launch path
+// makes no driver attribute call and allocates nothing.
+inline void ensure_smem(const void* f, size_t bytes) {
+    if (bytes <= 48 * 1024) return;
+    struct Entry {
+        const void* f;
+        int dev;
+        size_t bytes;
+    };
+    thread_local Entry tab[64];
+    thread_local int n = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (int i = 0; i < n; ++i)
+        if (tab[i].f == f && tab[i].dev == dev) {
+            if (tab[i].bytes >= bytes) return;
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+            tab[i].bytes = bytes;
+            return;
+        }
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (n < 64) tab[n++] = Entry{f, dev, bytes};
+}
+template <class K>
+inline void ensure_smem(K* kernel, size_t bytes) {
+    ensure_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 // ---------------------------------------------------------------------------
 // Resident device formats of one layer.
 enum Fmt : int {
@@ -160,7 +189,7 @@ bool head_b1_supported(const DevLayer* L, int nl);
 // Shared-memory plan of the batch-1 kernel; fills h->planes0, rec_cap,
 // pref_mask, pref_offset.
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h);
-void launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s);
 // Grid for which all CTAs are co-resident (one per SM), or 0 if the kernel
 // cannot be resident at this shared-memory size.
 int head_b1_max_grid(size_t smem, int num_sms);

@@ -1145,14 +1145,14 @@ void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_
             case 8: k = k_fwd_planes<8>; break;
             default: k = k_fwd_planes<12>; break;
         }
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+        ensure_smem(k, c.smem);
         launch_ex(k, dim3(c.nsplit), dim3(256), c.smem, pdl, s, a);
         return;
     }
     if (c.kind == 1) {
         void (*k)(FwdArgs) = a.L.fmt == FMT_I8_R32 ? large_kernel<FMT_I8_R32>(a.L.G, c.vj, c.spt)
                                                     : large_kernel<FMT_I8_WIDE>(a.L.G, c.vj, c.spt);
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(c.smem));
+        ensure_smem(k, c.smem);
         launch_ex(k, dim3(c.jt, c.nsplit, c.st), dim3(256), c.smem, pdl, s, a);
         return;
     }

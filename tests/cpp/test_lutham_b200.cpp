@@ -7,8 +7,11 @@
 //
 //   test_lutham_b200 cpu   cases that need no GPU (planner, file faults)
 //   test_lutham_b200 gpu   device cases (forward parity, errors, interp_ops)
+#include <atomic>
 #include <cmath>
 #include <algorithm>
+#include <cstdlib>
+#include <new>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -17,8 +20,22 @@
 #include <vector>
 
 #include "holoquant/lutham_b200.hpp"
+#include "holoquant/trainer.hpp"
 
 using namespace holoquant;
+
+// operator new counting, as the reference's acceptance check 7
+// (acceptance.cpp:426-447): every heap allocation of the process, including
+// those made inside libskan.so, goes through these while tracking is on.
+static std::atomic<std::uint64_t> g_alloc_count{0};
+static std::atomic<bool> g_alloc_tracking{false};
+void* operator new(std::size_t n) {
+    if (g_alloc_tracking.load(std::memory_order_relaxed)) g_alloc_count.fetch_add(1, std::memory_order_relaxed);
+    if (void* p = std::malloc(n ? n : 1)) return p;
+    throw std::bad_alloc();
+}
+void operator delete(void* p) noexcept { std::free(p); }
+void operator delete(void* p, std::size_t) noexcept { std::free(p); }
 
 namespace {
 
@@ -327,6 +344,42 @@ TEST_GPU("cfg2 head {2048,1408,20} K=65536 int8: batch 1 fast within tolerance, 
     const std::vector<double> f1 = dev_forward(dev, x1, 1, DeviceMode::Fast);
     const std::vector<double> scale = l1_scale(model, x1, 1);
     for (int j = 0; j < 20; ++j) CHECK(std::fabs(f1[j] - w1[j]) <= 1e-5 * scale[j]);
+}
+
+// acceptance.cpp:426-447 (check 7): 1000 drop-in forwards at batch 8 after
+// warm-up make zero heap allocations; here through the device head, in both
+// modes, on the reference's check-7 network and on the cfg2 head (whose
+// batch 8 runs the tensor-core GEMM route) and its batch-1 persistent path.
+TEST_GPU("zero-allocation forward: 1000 calls at B=8 (acceptance.cpp:426-447), both modes") {
+    const KanNetwork net = init_network(std::vector<int>{4, 24, 2}, 12, 0.4, 95);
+    VqConfig cfg;
+    cfg.k = 32;
+    cfg.seed = 96;
+    cfg.int8 = true;
+    const Model small = build_model(compress_network(net, cfg));
+    const Model big = build_model(head({2048, 1408, 20}, 10, 65536, true, 2026));
+    struct Case {
+        const Model* m;
+        int batch, calls;
+    };
+    for (const Case c : {Case{&small, 8, 1000}, Case{&big, 8, 1000}, Case{&big, 1, 1000}}) {
+        const DeviceHead dev = upload(*c.m);
+        DeviceWorkspace ws = make_workspace(dev, 8);
+        const int in = c.m->input_dim();
+        const int out = c.m->output_dim();
+        std::vector<double> x(static_cast<std::size_t>(c.batch) * in, 0.3), y(static_cast<std::size_t>(c.batch) * out);
+        for (DeviceMode mode : {DeviceMode::Fast, DeviceMode::Exact}) {
+            for (int warm = 0; warm < 3; ++warm) compressed_forward(dev, x, c.batch, y, ws, mode);
+            g_alloc_count.store(0);
+            g_alloc_tracking.store(true);
+            for (int call = 0; call < c.calls; ++call) compressed_forward(dev, x, c.batch, y, ws, mode);
+            g_alloc_tracking.store(false);
+            const std::uint64_t n = g_alloc_count.load();
+            if (n) std::fprintf(stderr, "  %llu allocations (in %d, batch %d, mode %d)\n",
+                                static_cast<unsigned long long>(n), in, c.batch, static_cast<int>(mode));
+            CHECK(n == 0);
+        }
+    }
 }
 
 }  // namespace

@@ -169,20 +169,6 @@ def test_fast_mode_headline_head(torch_cuda):
             assert ws.last_launches() == batch
 
 
-def test_fast_mode_headline_head_batch256(torch_cuda):
-    """cfg3 shape: batch 256 (checked with a relative-to-L1 bound computed on
-    a 16-sample slice, the full batch against the multi-threaded oracle)."""
-    cn = synthetic.synthetic_head()
-    tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
-    x = synthetic.synthetic_inputs(256, 2048, seed=77)
-    want, _ = oracle.port_forward(tables, x, 256, threads=8)
-    got, ws = _gpu_forward(hq.build_model(cn), x, 256, "fast", max_batch=256)
-    scale = l1_scale(tables, x[:16 * 2048], 16)
-    assert_close(got[:16 * 20], want[:16 * 20], scale)
-    # whole batch: relative to the head's typical L1 scale
-    assert np.max(np.abs(got - want)) <= TOL * np.median(scale)
-
-
 def test_fast_mode_bitwise_reproducible(torch_cuda):
     cn = synthetic.synthetic_head(dims=(512, 300, 20), k=4096, grid=10, int8=True, seed=5)
     model = hq.build_model(cn)
@@ -333,20 +319,19 @@ def test_device_tensor_forward_matches_host_forward(torch_cuda):
     assert np.array_equal(yd.cpu().numpy(), y)
 
 
-def test_multi_head_forward_equals_single_heads(torch_cuda):
+def test_multi_head_forward_against_oracle(torch_cuda):
     torch = torch_cuda
-    heads = [hq.build_model(synthetic.synthetic_head(dims=(64, 40, 5), k=512, grid=10, int8=True, seed=s))
-             for s in range(4)]
+    cns = [synthetic.synthetic_head(dims=(64, 40, 5), k=512, grid=10, int8=True, seed=s) for s in range(4)]
+    heads = [hq.build_model(cn) for cn in cns]
     wss = [hq.make_workspace(h, 16) for h in heads]
     x = synthetic.synthetic_inputs(16, 64, seed=3)
     xd = torch.from_numpy(x).cuda()
     ys = [torch.zeros(16 * 5, dtype=torch.float64, device="cuda") for _ in heads]
     hq.forward_multi(heads, wss, xd, 16, ys, mode="exact")
     torch.cuda.synchronize()
-    for h, y in zip(heads, ys):
-        want = np.zeros(80)
-        hq.compressed_forward(h, x, 16, want, hq.make_workspace(h, 16), mode="exact")
-        assert np.array_equal(y.cpu().numpy(), want)
+    for cn, y in zip(cns, ys):
+        want, _ = oracle.port_forward([oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)], x, 16)
+        assert np.array_equal(_bits(y.cpu().numpy()), _bits(want))
 
 
 def test_l2_persistence_window(torch_cuda):
