@@ -237,9 +237,15 @@ struct skan_workspace {
     double* xin = nullptr;   // staging for host inputs
     double* yout = nullptr;  // staging for host outputs
     uint64_t partial_floats = 0;
-    int* h_err = nullptr;    // pinned
-    int* zc_err_h = nullptr; // pinned + mapped error flag of the zero-copy host path (host view)
-    int* zc_err_d = nullptr; //   ... and its device alias
+    // Non-finite-input flag (ValueError, kan.cpp:29): page-locked host memory
+    // mapped into the device, written by a kernel only when it meets a
+    // non-finite input.  Sticky: a synchronizing call (host-buffer forward,
+    // skan_workspace_check) reads it after its stream sync, clears it and
+    // raises.  No per-call memset or device->host copy of a device flag: on
+    // the batch-1 path those two copy-engine operations cost more than the
+    // kernel itself.
+    int* zc_err_h = nullptr; // host view
+    int* zc_err_d = nullptr; // device alias (DevScratch::err)
     cudaStream_t last_stream = nullptr;
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
@@ -797,7 +803,7 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
                 skan::HeadB1Args a = h->b1_plan;
                 a.x = x + static_cast<size_t>(b) * h->in_dim;
                 a.y = y + static_cast<size_t>(b) * h->out_dim;
-                const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
+                const size_t n = h->b1_plan.part_floats;
                 a.part[0] = ws->b1_part;
                 a.part[1] = ws->b1_part + n;
                 a.x_tma = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (h->in_dim % 2 == 0);
@@ -1027,22 +1033,19 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         const size_t cbytes = ncnt * h->dl.size() * sizeof(unsigned);
         ws->d.counters = static_cast<unsigned*>(alloc(cbytes));
         skan::cuda_check(cudaMemset(ws->d.counters, 0, std::max<size_t>(cbytes, 256)), "cudaMemset");
-        ws->d.err = static_cast<int*>(alloc(sizeof(int)));
         if (h->b1_ok) {
-            const size_t n = static_cast<size_t>(h->b1_grid) * h->max_width;
+            const size_t n = h->b1_plan.part_floats;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
             ws->b1_done = static_cast<unsigned*>(alloc(sizeof(unsigned)));
             skan::cuda_check(cudaMemset(ws->b1_done, 0, sizeof(unsigned)), "cudaMemset");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
-        skan::cuda_check(cudaMallocHost(&ws->h_err, sizeof(int)), "cudaMallocHost");
-        *ws->h_err = 0;
         skan::cuda_check(cudaHostAlloc(&ws->zc_err_h, sizeof(int), cudaHostAllocMapped), "cudaHostAlloc");
         *ws->zc_err_h = 0;
         skan::cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->zc_err_d), ws->zc_err_h, 0),
                          "cudaHostGetDevicePointer");
-        skan::cuda_check(cudaMemset(ws->d.err, 0, sizeof(int)), "cudaMemset");
+        ws->d.err = ws->zc_err_d;
         *out = ws.release();
     });
 }
@@ -1052,7 +1055,6 @@ skan_status skan_workspace_destroy(skan_workspace* ws) {
         if (!ws) return;
         DeviceGuard g(ws->device);
         for (void* p : ws->allocs) cudaFree(p);
-        if (ws->h_err) cudaFreeHost(ws->h_err);
         if (ws->zc_err_h) cudaFreeHost(ws->zc_err_h);
         delete ws;
     });
@@ -1062,6 +1064,16 @@ uint64_t skan_workspace_interp_ops(const skan_workspace* ws) { return ws ? ws->i
 int skan_workspace_max_batch(const skan_workspace* ws) { return ws ? ws->max_batch : 0; }
 int skan_workspace_width(const skan_workspace* ws) { return ws ? ws->width : 0; }
 int skan_workspace_last_launches(const skan_workspace* ws) { return ws ? ws->last_launches : 0; }
+
+// After a stream sync: a non-finite input met by any forward on this
+// workspace since the last check raises ValueError (and clears the flag).
+void raise_if_flagged(skan_workspace* ws) {
+    volatile int* f = ws->zc_err_h;
+    if (*f) {
+        *f = 0;
+        raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+    }
+}
 
 // Device alias of a page-locked, mapped host buffer (cudaHostAlloc /
 // cudaMallocHost / cudaHostRegister'd memory, e.g. torch pin_memory), or
@@ -1105,17 +1117,15 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
         if (host && !exact && batch <= skan::kB1MaxBatch && batch <= ws->max_batch && h->b1_ok && ws->b1_part) {
             double* dy = const_cast<double*>(mapped_alias(outputs));
             if (dy) {
-                *ws->zc_err_h = 0;
                 skan::cuda_check(cudaMemcpyAsync(ws->xin, inputs, static_cast<size_t>(batch) * in * 8,
                                                  cudaMemcpyHostToDevice, s), "H2D inputs");
-                ws->last_launches = enqueue_chunk(h, ws, ws->xin, batch, dy, false, s, ws->zc_err_d);
+                ws->last_launches = enqueue_chunk(h, ws, ws->xin, batch, dy, false, s);
                 skan::cuda_check(cudaStreamSynchronize(s), "forward");
-                if (*static_cast<volatile int*>(ws->zc_err_h)) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+                raise_if_flagged(ws);
                 ws->interp_ops += static_cast<uint64_t>(batch) * h->edges;  // after success, as lutham.cpp:849
                 return;
             }
         }
-        skan::cuda_check(cudaMemsetAsync(ws->d.err, 0, sizeof(int), s), "reset error flag");
         for (int b0 = 0; b0 < batch; b0 += ws->max_batch) {
             const int B = std::min(ws->max_batch, batch - b0);
             const double* x = inputs + static_cast<size_t>(b0) * in;
@@ -1130,11 +1140,9 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
                 ws->last_launches += enqueue_chunk(h, ws, x, B, y, exact, s);
             }
         }
-        skan::cuda_check(cudaMemcpyAsync(ws->h_err, ws->d.err, sizeof(int), cudaMemcpyDeviceToHost, s),
-                         "error flag");
         if (host) {
             skan::cuda_check(cudaStreamSynchronize(s), "forward");
-            if (*ws->h_err) raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
+            raise_if_flagged(ws);
         }
         // host buffers: counted after the call succeeded (lutham.cpp:849);
         // device buffers: at enqueue (a non-finite input surfaces later, in
@@ -1214,10 +1222,7 @@ skan_status skan_workspace_check(skan_workspace* ws) {
         if (!ws) raise(SKAN_CONTRACT_ERROR, "workspace is null");
         DeviceGuard g(ws->device);
         skan::cuda_check(cudaStreamSynchronize(ws->last_stream), "forward");
-        if (*ws->h_err) {
-            *ws->h_err = 0;
-            raise(SKAN_VALUE_ERROR, "spline evaluated at non-finite x");
-        }
+        raise_if_flagged(ws);
     });
 }
 

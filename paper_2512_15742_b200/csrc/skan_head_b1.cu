@@ -26,7 +26,9 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "skan_device.cuh"
 #include "skan_internal.hpp"
@@ -49,6 +51,7 @@ __device__ __forceinline__ void stamp(const HeadB1Args& h, int phase) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         h.timeline[blockIdx.x * 16 + phase] = t;
+        h.timeline[(gridDim.x + blockIdx.x) * 16 + phase] = clock64();
     }
 }
 
@@ -564,6 +567,353 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(const __grid_constant__ HeadB
     stamp_clock(h, 15);
 }
 
+// ===========================================================================
+// v2: the two-layer head [wide int8 layer] -> [narrow last layer] (the
+// detection-head shape), same algorithm and summation orders as v1 but a
+// shorter critical path, shaped by measured costs (tools/mb_handoff.cu,
+// profiles/r2/): a warp's scattered 4-byte loads of other CTAs' partials cost
+// ~2.7k cycles where one coalesced 16-byte load per thread of a contiguous
+// block costs ~0.7k, so every cross-CTA hand-off is laid out contiguously
+// for its consumer.
+//   * x goes straight into registers with coalesced 16-byte loads: thread
+//     (w, l) owns inputs 256w + 64q + 2l + e (q < 4, e < 2);
+//   * per-warp bracket counts (REDUX); every warp derives the bucket
+//     allocation and its offset into the CTA's bucket from them, and ranks
+//     its rows with ballots: one block barrier between "x arrived" and
+//     "records requested", each thread bulk-copies the records of the rows
+//     it found;
+//   * layer 1's records (bulk copy at kernel start) and its edges' codebook
+//     rows (one 16-byte row per edge, all knots) are in shared memory before
+//     layer 0 ends: after the grid barrier layer 1 makes one dependent load;
+//   * layer 0's partials are written consumer-blocked, part0[d][c][0..nr1):
+//     consumer d reads one contiguous P x nr1 block;
+//   * the last layer's partials part1[c][0..out) are contiguous for the last
+//     arriving CTA, which reduces them.
+constexpr int kPer2 = 8;  // layer-0 inputs per thread: in0 <= kT * kPer2
+
+__device__ __forceinline__ float t_of(const DevLayer& L, double x, double nlo, double nhi) {
+    if (!(x > L.lo)) return 0.f;
+    if (!(x < L.hi) || x >= nhi) return 1.f;
+    return fminf(fmaxf(__double2float_rn(__dsub_rn(x, nlo)) * L.inv_dx_f, 0.f), 1.f);
+}
+
+__global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ HeadB1Args hp) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const HeadB1Args& h = hp;
+    __shared__ __align__(8) uint64_t s_bar[2];  // [0] plane + layer-0 records, [1] layer-1 records
+    __shared__ int s_wcnt[kW][32];              // per-warp bracket counts
+    __shared__ int s_rows[kMaxRows];
+    __shared__ float s_trow[kMaxRows];
+    __shared__ double s_bias1[kW];              // layer 0's bias sums of my layer-1 rows
+    __shared__ double s_bfin[32];               // layer 1's bias sums
+    __shared__ int s_last;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int P = gridDim.x, c = blockIdx.x;
+    const DevLayer& L = h.L[0];
+    const DevLayer& L1 = h.L[1];
+    // x first: four coalesced loads per thread
+    double xr[kPer2];
+    {
+        const int base = 256 * warp + 2 * lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = base + 64 * q;
+            if (h.x_tma && i + 1 < L.in) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(h.x + i));
+                xr[2 * q] = v.x;
+                xr[2 * q + 1] = v.y;
+            } else {
+                xr[2 * q] = i < L.in ? h.x[i] : 0.0;
+                xr[2 * q + 1] = i + 1 < L.in ? h.x[i + 1] : 0.0;
+            }
+        }
+    }
+    stamp(hp, 0);
+    if (hp.exit_at == 100) return;
+    unsigned char* s_pref = smem + h.pref_offset;
+    int r10, r11;
+    rows_of(L1, c, P, r10, r11);
+    const int nr = r11 - r10;
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * L1.out * 4u;
+        mbar_expect_tx(&s_bar[1], bytes);
+        bulk_g2s(s_pref, L1.rec + static_cast<size_t>(r10) * L1.out, bytes, &s_bar[1]);
+    } else if (warp == 1 && lane < 4) {
+        // the whole head streams HBM -> L2 from the first microsecond, sliced over the CTAs
+        if (lane == 0) prefetch_l2_slice(L.rec, static_cast<size_t>(L.in) * L.out * 4, c, P);
+        else if (lane == 1) prefetch_l2_slice(L.pair8, static_cast<size_t>(L.K) * (L.G - 1) * 2, c, P);
+        else if (lane == 2) prefetch_l2_slice(L1.rec, static_cast<size_t>(L1.in) * L1.out * 4, c, P);
+        else prefetch_l2_slice(L1.cb8, static_cast<size_t>(L1.K) * L1.rs, c, P);
+    }
+    const double b1_reg = tid < nr ? L.bias_sum[r10 + tid] : 0.0;
+    const double bf_reg = tid < L1.out ? L1.bias_sum[tid] : 0.0;
+    stamp(h, 1);
+    if (h.exit_at == 1) return;
+    // brackets: fp32 estimate, exact double comparisons where undecided
+    const int GP = L.G - 1;
+    int mb[kPer2];
+    unsigned hard = 0;
+#pragma unroll
+    for (int q = 0; q < kPer2; ++q) {
+        const int i = 256 * warp + 64 * (q >> 1) + 2 * lane + (q & 1);
+        mb[q] = 0xFF;
+        if (i < L.in && !bracket_f32(L, xr[q], mb[q])) hard |= 1u << q;
+    }
+#pragma unroll 1
+    for (; hard; hard &= hard - 1) {
+        const int q = __ffs(hard) - 1;
+        double x = 0.0;
+        int est = 0;
+#pragma unroll
+        for (int u = 0; u < kPer2; ++u)
+            if (u == q) {
+                x = xr[u];
+                est = mb[u];
+            }
+        int mm;
+        if (!finite_bits(x) || !(L.qf_eps >= 0.f)) {
+            float tt;
+            fast_locate(L, x, h.err, mm, tt);
+        } else {
+            mm = bracket_exact(h.node0, L, x, est);
+        }
+#pragma unroll
+        for (int u = 0; u < kPer2; ++u)
+            if (u == q) mb[u] = mm;
+    }
+    const uint32_t w0 = static_cast<uint32_t>(mb[0]) | mb[1] << 8 | mb[2] << 16 | static_cast<uint32_t>(mb[3]) << 24;
+    const uint32_t w1 = static_cast<uint32_t>(mb[4]) | mb[5] << 8 | mb[6] << 16 | static_cast<uint32_t>(mb[7]) << 24;
+#pragma unroll 1
+    for (int b = 0; b < GP; ++b) {  // per-warp counts (integer: order-free)
+        const uint32_t pat = static_cast<uint32_t>(b) * 0x01010101u;
+        const int n = __popc(__vcmpeq4(w0, pat) & 0x01010101u) + __popc(__vcmpeq4(w1, pat) & 0x01010101u);
+        const int tot = __reduce_add_sync(0xFFFFFFFFu, n);
+        if (lane == 0) s_wcnt[warp][b] = tot;
+    }
+    stamp(h, 2);
+    if (h.exit_at == 2) return;
+    __syncthreads();
+    // every warp: bucket totals (lane b), the allocation of CTAs to buckets
+    // (1 + floor((P - nonempty) * n_b / in) each, v1's rule), this CTA's
+    // bucket and row range, and the bucket's count in earlier warps
+    int nb = 0, before = 0;
+    if (lane < GP) {
+#pragma unroll 4
+        for (int w = 0; w < kW; ++w) {
+            const int v = s_wcnt[w][lane];
+            nb += v;
+            before += w < warp ? v : 0;
+        }
+    }
+    const int nonempty = __popc(__ballot_sync(0xFFFFFFFFu, nb > 0));
+    const int alloc = nb > 0 ? 1 + idiv_small((P - nonempty) * nb, L.in) : 0;
+    int incl = alloc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const bool mine = c >= incl - alloc && c < incl;
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, mine);
+    const int bucket = bal ? __ffs(bal) - 1 : GP;  // GP: spare CTA, no rows
+    int lo = 0, hi = 0;
+    if (mine) {
+        const int q = c - (incl - alloc);
+        lo = idiv_small(nb * q, alloc);
+        hi = idiv_small(nb * (q + 1), alloc);
+    }
+    const int src = bucket < GP ? bucket : 0;
+    lo = __shfl_sync(0xFFFFFFFFu, lo, src);
+    hi = __shfl_sync(0xFFFFFFFFu, hi, src);
+    before = __shfl_sync(0xFFFFFFFFu, before, src);
+    const int nrows = min(hi - lo, kMaxRows);
+    const int rec_rows = min(nrows, h.rec_cap);
+    const uint16_t* s_plane = reinterpret_cast<const uint16_t*>(smem);
+    const uint32_t plane_bytes = static_cast<uint32_t>(L.K) * 2u;
+    uint32_t* s_rec = reinterpret_cast<uint32_t*>(smem + ((plane_bytes + 127u) & ~127u));
+    const uint32_t row_bytes = static_cast<uint32_t>(L.out) * 4u;
+    if (tid == 0 && bucket < GP) {
+        mbar_expect_tx(&s_bar[0], plane_bytes + static_cast<uint32_t>(rec_rows) * row_bytes);
+        bulk_g2s(smem, L.pair8 + static_cast<size_t>(bucket) * L.K, plane_bytes, &s_bar[0]);
+    }
+    // my rows of the bucket in ascending i: within the warp i = 64q + 2l + e
+    if (bucket < GP) {
+        const uint32_t pat = static_cast<uint32_t>(bucket) * 0x01010101u;
+        const uint32_t m0 = __vcmpeq4(w0, pat), m1 = __vcmpeq4(w1, pat);
+        const double nlo = h.node0[bucket], nhi = h.node0[bucket + 1];
+        const unsigned lt = (1u << lane) - 1u;
+        int base = before - lo;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t m = q < 2 ? m0 : m1;
+            const bool e0 = (m >> (16 * (q & 1))) & 1u, e1 = (m >> (16 * (q & 1) + 8)) & 1u;
+            const unsigned B0 = __ballot_sync(0xFFFFFFFFu, e0), B1 = __ballot_sync(0xFFFFFFFFu, e1);
+            int r = base + __popc(B0 & lt) + __popc(B1 & lt);
+            const int i = 256 * warp + 64 * q + 2 * lane;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (e ? e1 : e0) {
+                    if (r >= 0 && r < nrows) {
+                        s_rows[r] = i + e;
+                        s_trow[r] = t_of(L, xr[2 * q + e], nlo, nhi);
+                        if (r < rec_rows)
+                            bulk_g2s(s_rec + static_cast<size_t>(r) * L.out,
+                                     L.rec + static_cast<size_t>(i + e) * L.out, row_bytes, &s_bar[0]);
+                    }
+                    ++r;
+                }
+            }
+            base += __popc(B0) + __popc(B1);
+        }
+    }
+    // while the plane and records land: layer 1's codebook rows of my edges
+    uint4* s_cb = reinterpret_cast<uint4*>(smem + h.cbrow_offset);
+    {
+        const uint32_t* srec1 = reinterpret_cast<const uint32_t*>(s_pref);
+        const int n1 = nr * L1.out;
+        if (tid < n1) {
+            mbar_wait(&s_bar[1], 0);
+            for (int e = tid; e < n1; e += kT)
+                s_cb[e] = __ldg(reinterpret_cast<const uint4*>(L1.cb8 + static_cast<size_t>(srec1[e] & 0xFFFFu) * L1.rs));
+        }
+    }
+    stamp(h, 3);
+    if (h.exit_at == 3) return;
+    __syncthreads();
+    if (bucket < GP) mbar_wait(&s_bar[0], 0);
+    stamp(h, 4);
+    if (h.exit_at == 4) return;
+    // layer 0: thread t owns outputs 4t..4t+3 over this CTA's rows, ascending
+    float* s_out = reinterpret_cast<float*>(smem + h.out_offset);
+    {
+        const int j = tid * 4;
+        if (j < L.out) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            auto edge4 = [&](const uint4& r, float t) {
+                float c0, dc;
+                pair_to_f(s_plane[r.x & 0xFFFFu], c0, dc);
+                a0 = fmaf(gain_of_rec(L, r.x), fmaf(t, dc, c0), a0);
+                pair_to_f(s_plane[r.y & 0xFFFFu], c0, dc);
+                a1 = fmaf(gain_of_rec(L, r.y), fmaf(t, dc, c0), a1);
+                pair_to_f(s_plane[r.z & 0xFFFFu], c0, dc);
+                a2 = fmaf(gain_of_rec(L, r.z), fmaf(t, dc, c0), a2);
+                pair_to_f(s_plane[r.w & 0xFFFFu], c0, dc);
+                a3 = fmaf(gain_of_rec(L, r.w), fmaf(t, dc, c0), a3);
+            };
+            const uint4* srec = reinterpret_cast<const uint4*>(s_rec + j);
+            const int rstride = L.out / 4;
+#pragma unroll 2
+            for (int rr = 0; rr < rec_rows; ++rr) edge4(srec[rr * rstride], s_trow[rr]);
+#pragma unroll 1
+            for (int rr = rec_rows; rr < nrows; ++rr)
+                edge4(__ldg(reinterpret_cast<const uint4*>(L.rec + static_cast<size_t>(s_rows[rr]) * L.out + j)),
+                      s_trow[rr]);
+            *reinterpret_cast<float4*>(s_out + j) = make_float4(a0, a1, a2, a3);
+        }
+    }
+    if (tid < nr) s_bias1[tid] = b1_reg;
+    if (tid < L1.out) s_bfin[tid] = bf_reg;
+    __syncthreads();
+    // consumer-blocked partials: part0[d][c][jl] for layer-1 row r0(d) + jl
+    {
+        const int NR = h.nr1;
+        float* part0 = h.part[0];
+#pragma unroll 1
+        for (int e = tid; e < P * NR; e += kT) {
+            const int d = idiv_small(e, NR), jl = e - d * NR;
+            const int j = idiv_small(L1.in * d, P) + jl;
+            if (j < idiv_small(L1.in * (d + 1), P)) part0[(static_cast<size_t>(d) * P + c) * NR + jl] = s_out[j];
+        }
+    }
+    stamp(h, 5);
+    if (h.exit_at == 5) return;
+    grid_sync();
+    stamp(h, 6);
+    // layer 1: my consumer block (P x NR, contiguous) -> shared memory
+    {
+        const int NR = h.nr1;
+        float* s_red = reinterpret_cast<float*>(smem);
+        float* s_term = s_red + P * NR;
+        const float* blk = h.part[0] + static_cast<size_t>(c) * P * NR;
+        const int n4 = P * NR / 4;
+#pragma unroll 1
+        for (int e = tid; e < n4; e += kT)
+            reinterpret_cast<float4*>(s_red)[e] = __ldcg(reinterpret_cast<const float4*>(blk) + e);
+        for (int e = 4 * n4 + tid; e < P * NR; e += kT) s_red[e] = __ldcg(blk + e);
+        __syncthreads();
+        // warp w: row r10 + w.  Lanes sum z = lane, lane + 32, ... in order, a
+        // fixed butterfly, lane 0's value; locate; lane j forms edge (w, j)
+        if (warp < nr) {
+            double v = 0.0;
+#pragma unroll 1
+            for (int z = lane; z < P; z += 32) v += static_cast<double>(s_red[z * NR + warp]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            v = __shfl_sync(0xFFFFFFFFu, v, 0) + s_bias1[warp];
+            int m;
+            float t;
+            fast_locate(L1, v, h.err, m, t);
+            if (lane < L1.out) {
+                const int e = warp * L1.out + lane;
+                const int8_t* cb = reinterpret_cast<const int8_t*>(s_cb + e);
+                const float c0 = static_cast<float>(cb[m]);
+                const float dc = static_cast<float>(cb[m + 1]) - c0;
+                s_term[e] = gain_of_rec(L1, reinterpret_cast<const uint32_t*>(s_pref)[e]) * fmaf(t, dc, c0);
+            }
+        }
+        __syncthreads();
+        if (tid < L1.out) {
+            float s = 0.f;
+#pragma unroll 1
+            for (int w = 0; w < nr; ++w) s += s_term[w * L1.out + tid];
+            h.part[1][static_cast<size_t>(c) * L1.out + tid] = s;
+        }
+    }
+    stamp(h, 7);
+    if (h.exit_at == 7) return;
+    // the last CTA to arrive reduces the [P][out] block (contiguous)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        const unsigned old = atomicAdd(h.done, 1u);
+        s_last = old - h.epoch == static_cast<unsigned>(P - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    stamp(h, 12);
+    {
+        const float* part = h.part[1];
+        const int total = P * L1.out;
+        float* s_fin = reinterpret_cast<float*>(smem);
+#pragma unroll 1
+        for (int e0 = tid; e0 < total; e0 += 8 * kT) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = e0 + u * kT < total ? __ldcg(part + e0 + u * kT) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (e0 + u * kT < total) s_fin[e0 + u * kT] = v[u];
+        }
+        __syncthreads();
+        int C = 1;
+        while (C < 32 && (C * 2) * L1.out <= kT) C <<= 1;
+        const int cl = tid & (C - 1), groups = kT / C;
+        for (int pass = 0; pass < L1.out; pass += groups) {
+            const int q = pass + tid / C;
+            const int j = min(q, L1.out - 1);
+            double v = 0.0;
+#pragma unroll 4
+            for (int z = cl; z < P; z += C) v += static_cast<double>(s_fin[z * L1.out + j]);
+            for (int o = C >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+            if (cl == 0 && q < L1.out) h.y[j] = v + s_bfin[j];
+        }
+    }
+    stamp(h, 13);
+}
+
 }  // namespace
 
 // Eligibility: every layer int8 with <= 65536-row codebooks (4-byte
@@ -581,6 +931,15 @@ bool head_b1_supported(const DevLayer* L, int nl) {
 // a row-split layer's brackets and per-warp accumulators.  Fills
 // h->planes0 / rec_cap / pref_mask / pref_offset.
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
+    static const int force_v1 = [] {
+        const char* e = std::getenv("SKAN_B1_V1");  // A/B experiment: the general batch-1 kernel
+        return e && e[0] == '1';
+    }();
+    static const int exit_at = [] {
+        const char* e = std::getenv("SKAN_B1_EXIT_AT");  // timing experiment
+        return e ? std::atoi(e) : 0;
+    }();
+    h->exit_at = exit_at;
     const DevLayer& L0 = L[0];
     const size_t kBudget = 218 * 1024;  // dynamic; + ~7 KB static + 1 KB reserved <= 227 KB
     const int spare = num_sms - (L0.G - 1);
@@ -588,9 +947,40 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
                  static_cast<size_t>(L0.K) * 2 <= 160 * 1024 && L0.G - 1 <= 32 &&
                  static_cast<long long>(L0.in) * L0.out >= 256LL * 1024 && spare > 0 &&
                  L0.in / spare + 2 <= kMaxRows;
+    const size_t plane = (static_cast<size_t>(L0.K) * 2 + 127) / 128 * 128;
+    const size_t row = static_cast<size_t>(L0.out) * 4;
+    const int want = spare > 0 ? L0.in / spare + 2 : 0;  // rows per CTA < in / (P - buckets) + 1
+    h->part_floats = static_cast<unsigned>(static_cast<size_t>(num_sms) * 16384);  // refined below
+    // v2: the two-layer head whose last layer is narrow
+    const int nr1 = nl == 2 ? (L[1].in + num_sms - 1) / num_sms : 0;
+    const bool v2 = !force_v1 && h->planes0 && nl == 2 && L0.in <= kPer2 * kT && nr1 <= kW && L[1].out <= 32 &&
+                    L[1].rs == 16;
+    if (v2) {
+        h->version = 2;
+        h->nr1 = nr1;
+        h->pref_mask = 2;
+        h->cbrow_mask = 2;
+        const size_t out_b = (row + 127) / 128 * 128;
+        const size_t pref_b = (static_cast<size_t>(nr1) * L[1].out * 4 + 127) / 128 * 128;
+        const size_t cb_b = static_cast<size_t>(nr1) * L[1].out * 16;
+        const size_t avail = kBudget > plane + out_b + pref_b + cb_b ? kBudget - plane - out_b - pref_b - cb_b : 0;
+        size_t cap = avail / row;
+        if (cap > static_cast<size_t>(want)) cap = want;
+        if (cap > static_cast<size_t>(kMaxRows)) cap = kMaxRows;
+        h->rec_cap = static_cast<int>(cap);
+        const size_t recs = (cap * row + 127) / 128 * 128;
+        h->out_offset = static_cast<uint32_t>(plane + recs);
+        h->pref_offset = static_cast<uint32_t>(plane + recs + out_b);
+        h->cbrow_offset = static_cast<uint32_t>(plane + recs + out_b + pref_b);
+        h->part_floats = static_cast<unsigned>(std::max<size_t>(static_cast<size_t>(num_sms) * num_sms * nr1,
+                                                                static_cast<size_t>(num_sms) * L[1].out));
+        return h->cbrow_offset + cb_b;
+    }
+    h->version = 1;
     // prefetch: row-split layers whose per-CTA record block is small
     size_t pref = 0;
     h->pref_mask = 0;
+    h->cbrow_mask = 0;
     for (int l = h->planes0 ? 1 : 0; l < nl; ++l) {
         const int rows = (L[l].in + num_sms - 1) / num_sms;
         const size_t b = static_cast<size_t>(rows) * L[l].out * 4;
@@ -601,11 +991,10 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
     }
     size_t phase = 0;
     h->rec_cap = 0;
+    int maxw = 0;
+    for (int l = 0; l < nl; ++l) maxw = std::max({maxw, L[l].in, L[l].out});
+    h->part_floats = static_cast<unsigned>(static_cast<size_t>(num_sms) * maxw);
     if (h->planes0) {
-        const size_t plane = (static_cast<size_t>(L0.K) * 2 + 127) / 128 * 128;
-        const size_t row = static_cast<size_t>(L0.out) * 4;
-        // rows per CTA < in / (P - buckets) + 1
-        const int want = L0.in / spare + 2;
         const size_t avail = kBudget > plane + pref ? kBudget - plane - pref : 0;
         size_t cap = avail / row;
         if (cap > static_cast<size_t>(want)) cap = want;
@@ -629,17 +1018,19 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
 }
 
 int head_b1_max_grid(size_t smem, int num_sms) {
-    if (cudaFuncSetAttribute(k_head_b1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-        cudaSuccess) {
+    for (auto k : {k_head_b1, k_head_b1v2})
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    int per_sm = 0, per_sm2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_head_b1, kT, smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_head_b1v2, kT, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_head_b1, kT, smem) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return per_sm >= 1 ? num_sms : 0;
+    return per_sm >= 1 && per_sm2 >= 1 ? num_sms : 0;
 }
 
 cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s) {
@@ -653,7 +1044,7 @@ cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStrea
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_head_b1, h);
+    return h.version == 2 ? cudaLaunchKernelEx(&cfg, k_head_b1v2, h) : cudaLaunchKernelEx(&cfg, k_head_b1, h);
 }
 
 }  // namespace skan

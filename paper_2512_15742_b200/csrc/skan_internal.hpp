@@ -183,6 +183,14 @@ struct HeadB1Args {
     int rec_cap;           // layer-0 rows whose records are staged in shared memory
     unsigned pref_mask;    // row-split layers whose records are prefetched at kernel start
     unsigned pref_offset;  // byte offset of the prefetch region in dynamic shared memory
+    unsigned cbrow_mask;   // v2: row-split layers whose edges' codebook rows are gathered
+                           // into shared memory before the layer's inputs are known
+    unsigned cbrow_offset; // v2: byte offset of that region in dynamic shared memory
+    int version;           // 2 = k_head_b1v2 (static-bucket-free prologue), 1 = k_head_b1
+    int exit_at;           // timing experiment (SKAN_B1_EXIT_AT): return after phase stamp n (0 = off)
+    int nr1;               // v2: layer-1 rows per consumer block (stride of the consumer-blocked partials)
+    unsigned out_offset;   // v2: byte offset of layer 0's per-CTA output staging in dynamic shared memory
+    unsigned part_floats;  // floats per partial buffer (part[0], part[1]) the kernel needs
     double node0[33];      // layer 0's node positions (kan.cpp:21-26), G <= 33
 };
 bool head_b1_supported(const DevLayer* L, int nl);

@@ -16,6 +16,7 @@ tensors on the head's device (device pointers).
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -618,9 +619,10 @@ class BenchRow:
 
 
 def _percentile(sorted_v, q: float) -> float:
-    """lutham.cpp:857-861: nearest-rank on the sorted samples."""
+    """lutham.cpp:857-861: nearest-rank on the sorted samples, the index
+    rounded half away from zero like std::llround (q*(n-1) >= 0)."""
     n = len(sorted_v)
-    return sorted_v[int(round(q * (n - 1)))]
+    return sorted_v[int(math.floor(q * (n - 1) + 0.5))]
 
 
 def bench_model(model: Model, config: BenchConfig = BenchConfig(), mode="fast") -> BenchRow:

@@ -20,8 +20,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--batches", default="1,2,4,8,16,64,256")
-    ap.add_argument("--flush-with", choices=["torch", "memset"], default="torch",
-                    help="L2 flush: a torch fill kernel, or cudaMemsetAsync")
+    ap.add_argument("--flush-with", choices=["torch", "memset", "write+read", "read"], default="torch",
+                    help="L2 flush: a torch fill kernel (256 MiB write), cudaMemsetAsync, the write followed by a "
+                         "256 MiB read (L2 left clean), or the read alone")
     args = ap.parse_args()
     cn = synthetic.synthetic_head()
     model = hq.build_model(cn)
@@ -37,6 +38,17 @@ def main():
             def zero_(self):
                 rt.cudaMemsetAsync(flush.data_ptr(), 0, flush.numel() * 4, torch.cuda.current_stream().cuda_stream)
         flusher = _F()
+    elif args.flush_with in ("write+read", "read"):
+        rd = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
+        acc = torch.zeros(1, dtype=torch.float32, device="cuda")
+        wr = args.flush_with == "write+read"
+
+        class _F2:
+            def zero_(self):
+                if wr:
+                    flush.zero_()
+                torch.sum(rd, dim=0, out=acc[0])
+        flusher = _F2()
     else:
         flusher = flush
     s = torch.cuda.Stream()

@@ -59,8 +59,11 @@ float time_it(F launch, bool flush, int reps = 200) {
         cudaEventElapsedTime(&ms, a, b);
         if (r >= 10) t.push_back(ms * 1e3f);
     }
+    double sum = 0;
+    for (float v : t) sum += v;
     std::sort(t.begin(), t.end());
     cudaStreamDestroy(s);
+    printf("[mean %6.2f] ", sum / t.size());
     return t[t.size() / 2];
 }
 
@@ -105,6 +108,26 @@ int main() {
                    launch_ex(k_empty<Big>, bg, sms, big_smem, false, s);
                    launch_ex(k_empty<Big>, bg, sms, big_smem, false, s);
                }, f));
+        // the same kernel as a one-node CUDA graph (instantiated once)
+        {
+            cudaStream_t cs;
+            cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+            cudaGraph_t g;
+            cudaGraphExec_t ge;
+            cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+            launch_ex(k_empty<Big>, bg, sms, big_smem, false, cs);
+            cudaStreamEndCapture(cs, &g);
+            cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphUpload(ge, cs);
+            printf("  graph of 1 kernel (205 KB) %7.2f us\n", time_it([&](cudaStream_t s) { cudaGraphLaunch(ge, s); }, f));
+            cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+            launch_ex(k_empty<Big>, bg, sms, big_smem, false, cs);
+            launch_ex(k_empty<Big>, bg, sms, big_smem, false, cs);
+            cudaStreamEndCapture(cs, &g);
+            cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphUpload(ge, cs);
+            printf("  graph of 2 kernels          %7.2f us\n", time_it([&](cudaStream_t s) { cudaGraphLaunch(ge, s); }, f));
+        }
     }
     cudaError_t e = cudaDeviceSynchronize();
     printf("status %s\n", cudaGetErrorString(e));
