@@ -203,7 +203,10 @@ skan_status skan_head_plan(const skan_head* head, skan_layer_plan* per_layer,
 uint64_t skan_head_edges(const skan_head* head);
 
 /* Pin the head's resident tables in L2 with a persisting access-policy
- * window on `stream` (cudaStream_t).  fraction in (0,1]; 0 clears it. */
+ * window on `stream` (cudaStream_t).  fraction in (0,1]; 0 clears it.  The
+ * device's persisting carve-out is the sum over the heads that asked for it
+ * (capped at cudaDevAttrMaxPersistingL2CacheSize); skan_forward_multi applies
+ * each head's window on the side stream that runs it. */
 skan_status skan_head_set_l2_persist(const skan_head* head, void* stream, float fraction);
 
 /* ---- workspaces (holoquant::Workspace) --------------------------------- */

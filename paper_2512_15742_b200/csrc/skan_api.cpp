@@ -225,6 +225,9 @@ struct skan_head {
     // (host-buffer calls: until they return); skan_head_swap holds it
     // exclusively, so a swap never races a forward's reads of dl/b1_plan.
     mutable std::shared_mutex swap_mu;
+    // persisting-L2 fraction requested by skan_head_set_l2_persist (0: off);
+    // skan_forward_multi applies it to the side stream that runs this head
+    mutable float l2_frac = 0.f;
 };
 
 struct skan_workspace {
@@ -868,6 +871,36 @@ void check_forward_args(const skan_head* h, const skan_workspace* ws, int batch)
     check_workspace_for(h, ws);
 }
 
+// Persisting-L2 carve-out per device: the sum of the resident bytes of the
+// heads that asked for persistence, capped at the device maximum.
+void update_persist_limit(int device, int64_t delta) {
+    static std::mutex mu;
+    static std::map<int, int64_t> bytes;
+    std::lock_guard<std::mutex> lock(mu);
+    int64_t& b = bytes[device];
+    b = std::max<int64_t>(0, b + delta);
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+    skan::cuda_check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                        static_cast<size_t>(std::min<int64_t>(b, max_persist))),
+                     "persisting L2 limit");
+}
+
+// The access-policy window of a head (empty when it has none).
+cudaStreamAttrValue l2_window(const skan_head* h) {
+    cudaStreamAttrValue v{};
+    if (h->l2_frac > 0.f) {
+        int max_window = 0;
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
+        v.accessPolicyWindow.base_ptr = h->dmem;
+        v.accessPolicyWindow.num_bytes = std::min<size_t>(h->dbytes, static_cast<size_t>(max_window));
+        v.accessPolicyWindow.hitRatio = std::min(1.f, h->l2_frac);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+    return v;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -949,6 +982,7 @@ skan_status skan_head_destroy(skan_head* h) {
         if (!h) return;
         if (h->dmem) {
             DeviceGuard g(h->device);
+            if (h->l2_frac > 0.f) update_persist_limit(h->device, -static_cast<int64_t>(h->dbytes));
             cudaFree(h->dmem);
         }
         delete h;
@@ -982,21 +1016,11 @@ skan_status skan_head_set_l2_persist(const skan_head* h, void* stream, float fra
     return guarded([&] {
         if (!h) raise(SKAN_CONTRACT_ERROR, "null head");
         DeviceGuard g(h->device);
-        cudaStreamAttrValue v{};
-        if (fraction > 0.f) {
-            int max_persist = 0, max_window = 0;
-            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
-            const size_t want = std::min<size_t>(h->dbytes, static_cast<size_t>(max_persist));
-            skan::cuda_check(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want), "persisting L2 limit");
-            v.accessPolicyWindow.base_ptr = h->dmem;
-            v.accessPolicyWindow.num_bytes = std::min<size_t>(h->dbytes, static_cast<size_t>(max_window));
-            v.accessPolicyWindow.hitRatio = std::min(1.f, fraction);
-            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        } else {
-            v.accessPolicyWindow.num_bytes = 0;
-        }
+        const float f = fraction > 0.f ? std::min(1.f, fraction) : 0.f;
+        if ((f > 0.f) != (h->l2_frac > 0.f))
+            update_persist_limit(h->device, f > 0.f ? static_cast<int64_t>(h->dbytes) : -static_cast<int64_t>(h->dbytes));
+        h->l2_frac = f;
+        const cudaStreamAttrValue v = l2_window(h);
         skan::cuda_check(cudaStreamSetAttribute(static_cast<cudaStream_t>(stream),
                                                 cudaStreamAttributeAccessPolicyWindow, &v),
                          "access policy window");
@@ -1281,7 +1305,14 @@ skan_status skan_forward_multi(const skan_head* const* heads, skan_workspace* co
         const int used = std::min(n, P);
         skan::cuda_check(cudaEventRecord(pool.events[0], s), "fork");
         for (int q = 0; q < used; ++q) skan::cuda_check(cudaStreamWaitEvent(pool.streams[q], pool.events[0], 0), "fork");
+        bool persist = false;
+        for (int q = 0; q < n; ++q) persist = persist || heads[q]->l2_frac > 0.f;
         for (int q = 0; q < n; ++q) {
+            if (persist) {  // this head's persisting window (or none) on the side stream it runs on
+                const cudaStreamAttrValue v = l2_window(heads[q]);
+                skan::cuda_check(cudaStreamSetAttribute(pool.streams[q % P], cudaStreamAttributeAccessPolicyWindow, &v),
+                                 "access policy window");
+            }
             const skan_status st =
                 skan_forward_async(heads[q], wss[q], x, batch, ys[q], mode, pool.streams[q % P]);
             if (st != SKAN_OK) raise(st, g_err.msg);

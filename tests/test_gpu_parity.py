@@ -389,7 +389,7 @@ def test_unpack_indices_bitexact(torch_cuda):
 # tensor-core layer GEMM (skan_gemm.cu): every table format, even and odd G,
 # batches that fill and do not fill a 128-sample tile
 
-@pytest.mark.parametrize("batch", [64, 200])
+@pytest.mark.parametrize("batch", [64, 200, 300])
 def test_fast_mode_tensor_core_gemm_formats(torch_cuda, batch):
     rng = np.random.default_rng(300 + batch)
     cases = [

@@ -1,3 +1,7 @@
-python -m pytest -q -x tests/test_gpu_configs.py::test_cfg2_batch1_many_inputs_within_bound tests/test_gpu_parity.py -k "batch1 or headline or swap or zero" 2>&1 | tail -1
-python tools/diag_latency.py --batches 1 --reps 400 2>&1 | grep "flush=True"
-python tools/b1_timeline.py --reps 1
+M=gpu__time_duration.sum,lts__t_sector_hit_rate.pct,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read.sum,lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum
+for p in "" "--persist"; do
+  echo "== persist=$p"
+  ncu --cache-control none --clock-control none -k regex:k_head_b1 -s 20 -c 3 --metrics $M --csv python tools/l2_resident.py $p 2>/dev/null | grep -v "^==" | tail -n +1 | cut -c1-400
+done
+python -m pytest -q -x tests -m gpu 2>&1 | tail -1
+python bench.py > gpurun_out/r2_bench2.json 2> gpurun_out/r2_bench2.err; tail -2 gpurun_out/r2_bench2.err
