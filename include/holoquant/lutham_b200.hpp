@@ -278,6 +278,13 @@ inline void swap_device_model(DeviceHead& head, const CompressedNetwork& cn, voi
     b200_detail::check(skan_head_swap(head.get(), d.data(), static_cast<int>(d.size()), stream));
 }
 
+// Hot swap from SKAN v1 bytes (skan_head_swap_bytes): deserialize's faults
+// (FormatError with the reference's fault and byte offset) before anything
+// is overwritten, then the sections are unpacked on the device into the slot.
+inline void swap_device_model(DeviceHead& head, std::span<const std::uint8_t> bytes, void* stream = nullptr) {
+    b200_detail::check(skan_head_swap_bytes(head.get(), bytes.data(), bytes.size(), stream));
+}
+
 // build_dense_model (lutham.cpp:177-195) straight to the device.
 inline DeviceHead build_device_dense_model(const KanNetwork& net, int device = 0) {
     if (net.layers().empty()) throw ShapeError("network needs at least one layer");

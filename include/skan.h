@@ -183,10 +183,17 @@ skan_status skan_head_destroy(skan_head* head);
  * lutham.cpp:715-724): replace every table of `head` in place with the
  * layers described (validated like skan_head_create), keeping its device
  * allocation, plan and workspaces.  The new layers must match the old ones
- * in shape, grid size, K and format.  The copy is ordered on `stream`
- * (cudaStream_t) and complete on return; forwards on other streams must not
- * overlap it. */
+ * in shape, grid size, K and format.  Forwards are excluded while the
+ * tables change and forwards already enqueued on any stream are drained
+ * first, so every forward reads either the old tables or the new; the copy
+ * is ordered on `stream` (cudaStream_t) and complete on return. */
 skan_status skan_head_swap(skan_head* head, const skan_layer_desc* layers, int n_layers, void* stream);
+/* Hot swap from SKAN v1 bytes into the pre-planned slot: the same checks,
+ * faults and byte offsets as skan_head_load (deserialize, lutham.cpp:532-704),
+ * all raised before the resident tables are touched; the sections go to
+ * HBM and are unpacked there.  The file must describe the same layer shapes,
+ * grids, K and formats (ContractError otherwise). */
+skan_status skan_head_swap_bytes(skan_head* head, const uint8_t* bytes, size_t n_bytes, void* stream);
 
 /* Model::input_dim/output_dim/max_width (lutham.cpp:160-175), layer count
  * and per-layer headers (Model::header, lutham.cpp:154). */

@@ -10,6 +10,6 @@ from .lutham import (MODE_EXACT, MODE_FAST, BenchConfig, BenchRow, Codebook, Com
                      RuntimeLayer, Workspace, bench_csv, bench_iso_latency, bench_model, build_dense_model,
                      build_model, compressed_forward,
                      deserialize, forward_async, forward_multi, index_bits, kFlagInt8, load_model,
-                     locate, make_workspace, pli_lookup, assign_indices, plan_memory, swap_model, unpack_indices, upload)
+                     locate, make_workspace, pli_lookup, assign_indices, plan_memory, swap_model, swap_model_bytes, unpack_indices, upload)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -73,6 +73,7 @@ _SIGS = {
     "skan_head_load_file": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_p)]),
     "skan_head_destroy": (C.c_int, [_p]),
     "skan_head_swap": (C.c_int, [_p, C.POINTER(LayerDescC), C.c_int, _p]),
+    "skan_head_swap_bytes": (C.c_int, [_p, _p, C.c_size_t, _p]),
     "skan_head_num_layers": (C.c_int, [_p]),
     "skan_head_input_dim": (C.c_int, [_p]),
     "skan_head_output_dim": (C.c_int, [_p]),

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("skan_kernels.cu", "skan_head_b1.cu", "skan_gemm.cu", "skan_vq.cu", "skan_api.cpp",
+SOURCES = [os.path.join(CSRC, f) for f in ("skan_kernels.cu", "skan_head_b1.cu", "skan_gemm.cu", "skan_vq.cu", "skan_load.cu", "skan_api.cpp",
                                            "skan_format.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("skan_internal.hpp", "skan_device.cuh", "skan_tc.cuh")] + [
     os.path.join(ROOT, "include", "skan.h")]

@@ -281,6 +281,11 @@ struct Staged {
     double lutd[256] = {};
     float lutf[256] = {};
     std::vector<double> bias_sum;
+    // SKAN v1 direct-to-device load: the per-edge regions (records, codebook
+    // tables, bias sums) are built on the device from the file's sections
+    bool dev = false;
+    skan::LayerSrc src{};
+    int bits = 0;
 };
 
 void check_domain(const skan_layer_header& h, int l) {
@@ -456,10 +461,11 @@ Staged stage_runtime(const skan_layer_desc& d, int l) {
 void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream_t stream = nullptr) {
     uint64_t total = 0;
     for (const auto& lp : h->lplan) total = add_checked(total, lp.device_bytes);
+    // the new layer views are built off to the side and published at the end
+    std::vector<DevLayer> new_dl;
+    std::vector<skan_layer_header> new_headers;
     if (swap) {
         if (total != h->dbytes) raise(SKAN_CONTRACT_ERROR, "hot swap needs a head with the same memory plan");
-        h->dl.clear();
-        h->headers.clear();
     } else {
         h->dbytes = total;
         skan::cuda_check(cudaMalloc(&h->dmem, std::max<uint64_t>(total, 256)), "cudaMalloc(head)");
@@ -531,9 +537,13 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
             d.g_base = static_cast<float>(s.h.gain_log_min + std::log2(s.h.codebook_scale));
             d.g_step = static_cast<float>(s.h.gain_log_step);
         }
+        const uint64_t E = static_cast<uint64_t>(d.in) * d.out;
+        // host-built regions go into the image; a directly loaded layer's
+        // per-edge regions are holes its build kernels fill
+        auto region = [&](const void* src, uint64_t bytes) { return s.dev ? reserve(bytes) : put(src, bytes); };
         switch (d.fmt) {
             case skan::FMT_DENSE:
-                d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
+                d.cb32 = static_cast<const float*>(region(s.cb32.data(), E * d.G * 4));
                 if (dense_tiled(s.h)) {
                     d.wt = static_cast<const float*>(reserve(skan::dense_tile_floats(d.in, d.out, d.G) * 4));
                     d.wt_nch = (d.in + skan::gemm_ic(d.G) - 1) / skan::gemm_ic(d.G);
@@ -542,12 +552,19 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
             case skan::FMT_I8_R32:
             case skan::FMT_I8_WIDE: {
                 if (d.fmt == skan::FMT_I8_R32) {
-                    d.rec = static_cast<const uint32_t*>(put(s.rec.data(), s.rec.size() * 4));
+                    d.rec = static_cast<const uint32_t*>(region(s.rec.data(), E * 4));
                 } else {
-                    d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
-                    d.gb = static_cast<const uint16_t*>(put(s.gb.data(), s.gb.size() * 2));
+                    d.idx = static_cast<const uint32_t*>(region(s.idx.data(), E * 4));
+                    d.gb = static_cast<const uint16_t*>(region(s.gb.data(), E * 2));
                 }
                 const uint64_t G = s.h.grid_size, K = s.h.k, rs = int8_row_stride(G);
+                d.rs = static_cast<int>(rs);
+                if (s.dev) {
+                    d.cb8 = static_cast<const int8_t*>(reserve(K * rs));
+                    d.cb8u = static_cast<const uint8_t*>(reserve(K * rs));
+                    d.pair8 = static_cast<const uint16_t*>(reserve(K * (G - 1) * 2));
+                    break;
+                }
                 std::vector<int8_t> padded(K * rs, 0);
                 std::vector<uint16_t> pairs(K * (G - 1));
                 // pair planes, bracket-major: pairs[m][k] = c[k][m] | c[k][m+1] << 8
@@ -558,7 +575,6 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
                         pairs[m * K + k] = static_cast<uint16_t>(static_cast<uint8_t>(row[m]) |
                                                                  (static_cast<uint8_t>(row[m + 1]) << 8));
                 }
-                d.rs = static_cast<int>(rs);
                 d.cb8 = static_cast<const int8_t*>(put(padded.data(), padded.size()));
                 // the same rows with every code biased to u = c ^ 0x80: the GEMM
                 // builds 2^23 + u with one byte permute (no XOR per element)
@@ -569,21 +585,21 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
                 break;
             }
             default:
-                if (s.h.k > 1) d.idx = static_cast<const uint32_t*>(put(s.idx.data(), s.idx.size() * 4));
-                d.gain = static_cast<const float*>(put(s.gain.data(), s.gain.size() * 4));
-                d.bias = static_cast<const float*>(put(s.bias.data(), s.bias.size() * 4));
-                d.cb32 = static_cast<const float*>(put(s.cb32.data(), s.cb32.size() * 4));
+                if (s.h.k > 1) d.idx = static_cast<const uint32_t*>(region(s.idx.data(), E * 4));
+                d.gain = static_cast<const float*>(region(s.gain.data(), E * 4));
+                d.bias = static_cast<const float*>(region(s.bias.data(), E * 4));
+                d.cb32 = static_cast<const float*>(region(s.cb32.data(), static_cast<uint64_t>(d.K) * d.G * 4));
                 break;
         }
         if (d.fmt != skan::FMT_DENSE) {
             d.lutf = static_cast<const float*>(put(s.lutf, sizeof s.lutf));
             d.lutd = static_cast<const double*>(put(s.lutd, sizeof s.lutd));
-            d.bias_sum = static_cast<const double*>(put(s.bias_sum.data(), s.bias_sum.size() * 8));
+            d.bias_sum = static_cast<const double*>(region(s.bias_sum.data(), static_cast<uint64_t>(d.out) * 8));
         }
         if (cur - begin != h->lplan[l].device_bytes)
             raise(SKAN_PLAN_ERROR, "resident layout of layer " + std::to_string(l) + " disagrees with the plan");
-        h->dl.push_back(d);
-        h->headers.push_back(s.h);
+        new_dl.push_back(d);
+        new_headers.push_back(s.h);
     }
     // copy the image around the holes, then build the device-side regions
     const cudaStream_t cs = swap ? stream : nullptr;
@@ -596,10 +612,14 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
                              swap ? "swap head" : "upload head");
         from = hole.second;
     }
-    for (const DevLayer& d : h->dl)
+    for (size_t l = 0; l < st.size(); ++l)
+        if (st[l].dev) skan::build_layer_from_sections(new_dl[l], st[l].src, st[l].bits, cs);
+    for (const DevLayer& d : new_dl)
         if (d.wt) skan::build_dense_tiles(d, const_cast<float*>(d.wt), cs);
     skan::cuda_check(cudaGetLastError(), "dense tiles");
     skan::cuda_check(cudaStreamSynchronize(cs), swap ? "swap head" : "upload head");  // host image is freed on return
+    h->dl = std::move(new_dl);
+    h->headers = std::move(new_headers);
 }
 
 std::vector<Staged> stage_all(const skan_layer_desc* layers, int n) {
@@ -629,12 +649,19 @@ void refresh_b1_layers(skan_head* h) {
         h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
 }
 
+skan_head* create_head_staged(std::vector<Staged>& st, int device);
+
 skan_head* create_head(const skan_layer_desc* layers, int n, int device) {
     if (n <= 0 || !layers) raise(SKAN_SHAPE_ERROR, "model has no layers");
     int ndev = 0;
     skan::cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
     if (device < 0 || device >= ndev) raise(SKAN_CONTRACT_ERROR, "no such CUDA device");
     std::vector<Staged> st = stage_all(layers, n);
+    return create_head_staged(st, device);
+}
+
+skan_head* create_head_staged(std::vector<Staged>& st, int device) {
+    const int n = static_cast<int>(st.size());
     auto h = std::make_unique<skan_head>();
     h->device = device;
     std::vector<skan_layer_header> hs;
@@ -901,6 +928,48 @@ cudaStreamAttrValue l2_window(const skan_head* h) {
     return v;
 }
 
+// Refill a resident head in place (same shapes, grids, K and formats, so
+// the same memory plan).  Forwards are excluded by the swap lock and
+// in-flight ones drained first: a forward sees the old tables or the new.
+void swap_staged(skan_head* h, std::vector<Staged>& st, cudaStream_t stream) {
+    const int n = static_cast<int>(st.size());
+    if (n != static_cast<int>(h->headers.size())) raise(SKAN_CONTRACT_ERROR, "hot swap needs the same number of layers");
+    for (int l = 0; l < n; ++l) {
+        const skan_layer_header &a = st[l].h, &b = h->headers[l];
+        if (a.in_dim != b.in_dim || a.out_dim != b.out_dim || a.grid_size != b.grid_size || a.k != b.k ||
+            (a.flags & SKAN_FLAG_INT8) != (b.flags & SKAN_FLAG_INT8))
+            raise(SKAN_CONTRACT_ERROR, "hot swap needs the same layer shapes, grid sizes, K and formats");
+    }
+    std::vector<skan_layer_header> hs;
+    for (auto& x : st) hs.push_back(x.h);
+    std::vector<skan_layer_plan> lp(n);
+    const skan_memory_plan tot = plan(hs.data(), n, lp.data());
+    DeviceGuard g(h->device);
+    std::unique_lock<std::shared_mutex> lock(h->swap_mu);
+    skan::cuda_check(cudaDeviceSynchronize(), "drain in-flight forwards before a swap");
+    h->lplan = lp;
+    h->totals = tot;
+    upload(h, st, /*swap=*/true, stream);
+    if (h->b1_ok) refresh_b1_layers(h);
+}
+
+// Staging of directly loaded layers: headers (already checked by the SKAN
+// parser) and the device addresses of their sections; the gain tables are
+// the only per-layer host work.
+std::vector<Staged> stage_sections(const skan::SectionLayer* L, int n) {
+    std::vector<Staged> st(n);
+    for (int l = 0; l < n; ++l) {
+        Staged& s = st[l];
+        s.h = L[l].h;
+        s.dev = true;
+        s.src = L[l].src;
+        s.bits = L[l].bits;
+        if (s.h.k != 0 && is_int8(s.h)) fill_int8_luts(s);
+        check_domain(s.h, l);
+    }
+    return st;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -955,25 +1024,7 @@ skan_status skan_head_swap(skan_head* h, const skan_layer_desc* layers, int n, v
         if (n != static_cast<int>(h->headers.size()) || !layers)
             raise(SKAN_CONTRACT_ERROR, "hot swap needs the same number of layers");
         std::vector<Staged> st = stage_all(layers, n);
-        for (int l = 0; l < n; ++l) {
-            const skan_layer_header &a = st[l].h, &b = h->headers[l];
-            if (a.in_dim != b.in_dim || a.out_dim != b.out_dim || a.grid_size != b.grid_size || a.k != b.k ||
-                (a.flags & SKAN_FLAG_INT8) != (b.flags & SKAN_FLAG_INT8))
-                raise(SKAN_CONTRACT_ERROR, "hot swap needs the same layer shapes, grid sizes, K and formats");
-        }
-        std::vector<skan_layer_header> hs;
-        for (auto& x : st) hs.push_back(x.h);
-        std::vector<skan_layer_plan> lp(n);
-        const skan_memory_plan tot = plan(hs.data(), n, lp.data());
-        DeviceGuard g(h->device);
-        // No forward reads the host views while we hold the lock; forwards
-        // already enqueued on any stream finish before the tables change.
-        std::unique_lock<std::shared_mutex> lock(h->swap_mu);
-        skan::cuda_check(cudaDeviceSynchronize(), "drain in-flight forwards before a swap");
-        h->lplan = lp;
-        h->totals = tot;
-        upload(h, st, /*swap=*/true, static_cast<cudaStream_t>(stream));
-        if (h->b1_ok) refresh_b1_layers(h);
+        swap_staged(h, st, static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1379,3 +1430,19 @@ skan_status skan_unpack_indices(const uint8_t* bytes, size_t n_bytes, uint64_t c
 }
 
 }  // extern "C"
+
+namespace skan {
+
+skan_head* create_head_from_sections(const SectionLayer* layers, int n, int device) {
+    if (n <= 0 || !layers) raise(SKAN_SHAPE_ERROR, "model has no layers");
+    std::vector<Staged> st = stage_sections(layers, n);
+    return create_head_staged(st, device);
+}
+
+void swap_head_from_sections(skan_head* h, const SectionLayer* layers, int n, cudaStream_t stream) {
+    if (!h) raise(SKAN_CONTRACT_ERROR, "null head");
+    std::vector<Staged> st = stage_sections(layers, n);
+    swap_staged(h, st, stream);
+}
+
+}  // namespace skan

@@ -4,6 +4,7 @@
 // fault contract of deserialize (src/lutham.cpp:532-704): the same fault
 // kinds, byte offsets and message fragments, checked in the same order, so
 // a caller switching from holoquant::deserialize sees identical errors.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -47,23 +48,12 @@ int bit_width_minus1(uint32_t k) {
     return b;
 }
 
-// Owned copies of one layer's sections (file offsets are only 64-B aligned
-// relative to the buffer start, which itself may be unaligned).
-struct LayerTables {
-    std::vector<float> f32;
-    std::vector<int8_t> i8;
-    std::vector<uint16_t> idx16;
-    std::vector<uint32_t> idx32;
-    std::vector<float> gains, biases;
-    std::vector<int8_t> gcodes, bcodes;
-};
-
 }  // namespace
 
 namespace {
 
-void parse(const uint8_t* bytes, uint64_t n, std::vector<skan_layer_header>& hs,
-           std::vector<LayerTables>& tabs) {
+void parse_headers(const uint8_t* bytes, uint64_t n, std::vector<skan_layer_header>& hs,
+                   std::vector<skan_layer_plan>& lp) {
     Cursor r{bytes, n};
     r.need(4, 0, "magic");
     if (std::memcmp(bytes, "SKAN", 4) != 0)
@@ -126,83 +116,147 @@ void parse(const uint8_t* bytes, uint64_t n, std::vector<skan_layer_header>& hs,
         }
     }
 
-    std::vector<skan_layer_plan> lp(count);
+    lp.resize(count);
     skan_memory_plan tot{};
     if (skan_plan_memory(hs.data(), static_cast<int>(count), lp.data(), &tot) != SKAN_OK) {
         char msg[256];
         skan_last_error(msg, sizeof msg, nullptr, nullptr);
         skan::raise_format(SKAN_FAULT_BAD_HEADER, kPrelude, msg);
     }
+}
 
-    tabs.resize(count);
-    uint64_t cursor = kPrelude + uint64_t{count} * kHeaderBytes;
-    for (uint32_t l = 0; l < count; ++l) {
+// Section offsets of every layer, walked in deserialize's order
+// (lutham.cpp:642-704; FORMAT.md:41-53: 64-byte aligned); the walk stops at
+// the first truncated section, whose fault is raised only after the index
+// range checks of the sections before it (the reference's check order).
+struct Sections {
+    uint64_t at[4] = {};  // codebook (or dense coefficients), index, gain, bias
+};
+struct Walk {
+    std::vector<Sections> sec;
+    int trunc_layer = -1, trunc_sec = -1;  // first truncated section (0 codebook, 1 index, 2 gain, 3 bias)
+    uint64_t trunc_at = 0;
+    std::string trunc_msg;
+    uint64_t end = 0;  // bytes the file must hold
+};
+
+Walk walk_sections(uint64_t n, const std::vector<skan_layer_header>& hs, const std::vector<skan_layer_plan>& lp) {
+    Walk w;
+    w.sec.resize(hs.size());
+    uint64_t cursor = kPrelude + uint64_t{hs.size()} * kHeaderBytes;
+    for (size_t l = 0; l < hs.size() && w.trunc_layer < 0; ++l) {
         const skan_layer_header& h = hs[l];
-        LayerTables& t = tabs[l];
         const std::string where = "layer " + std::to_string(l);
-        const uint64_t e = uint64_t{h.in_dim} * h.out_dim;
-        const bool int8 = (h.flags & SKAN_FLAG_INT8) != 0;
-        auto section = [&](uint64_t size, const char* name, uint64_t* at_out = nullptr) {
+        const uint64_t sizes[4] = {lp[l].codebook_bytes, lp[l].index_bytes, lp[l].gain_bytes, lp[l].bias_bytes};
+        static const char* names[4] = {"codebook", "index", "gain", "bias"};
+        const int nsec = h.k == 0 ? 1 : 4;
+        for (int q = 0; q < nsec; ++q) {
             cursor = (cursor + kSectionAlign - 1) / kSectionAlign * kSectionAlign;
-            r.need(cursor + size, cursor, where + " " + name + " section");
-            const uint8_t* p = bytes + cursor;
-            if (at_out) *at_out = cursor;
-            cursor += size;
-            return p;
-        };
-        if (h.k == 0) {
-            const uint8_t* p = section(lp[l].codebook_bytes, "coefficient");
-            t.f32.resize(e * h.grid_size);
-            std::memcpy(t.f32.data(), p, lp[l].codebook_bytes);
-            continue;
-        }
-        const uint8_t* cb = section(lp[l].codebook_bytes, "codebook");
-        const uint64_t kg = uint64_t{h.k} * h.grid_size;
-        if (int8) {
-            t.i8.resize(kg);
-            std::memcpy(t.i8.data(), cb, lp[l].codebook_bytes);
-        } else {
-            t.f32.resize(kg);
-            std::memcpy(t.f32.data(), cb, lp[l].codebook_bytes);
-        }
-        uint64_t index_at = 0;
-        const uint8_t* ix = section(lp[l].index_bytes, "index", &index_at);
-        const int bits = bit_width_minus1(h.k);
-        if (bits > 0) {
-            // LSB-first unpack (lutham.cpp:114-137) with the range check of
-            // lutham.cpp:669-676.
-            const uint64_t mask = (uint64_t{1} << bits) - 1;
-            uint64_t acc = 0;
-            int filled = 0;
-            uint64_t pos = 0;
-            if (h.k <= 65536) t.idx16.resize(e); else t.idx32.resize(e);
-            for (uint64_t q = 0; q < e; ++q) {
-                while (filled < bits) {
-                    acc |= uint64_t{ix[pos++]} << filled;
-                    filled += 8;
-                }
-                const uint32_t v = static_cast<uint32_t>(acc & mask);
-                acc >>= bits;
-                filled -= bits;
-                if (v >= h.k)
-                    skan::raise_format(SKAN_FAULT_INDEX_OUT_OF_RANGE, index_at,
-                                       where + " edge " + std::to_string(q) + " index " + std::to_string(v) +
-                                           " is outside K=" + std::to_string(h.k));
-                if (h.k <= 65536) t.idx16[q] = static_cast<uint16_t>(v); else t.idx32[q] = v;
+            w.sec[l].at[q] = cursor;
+            if (n < cursor + sizes[q]) {
+                w.trunc_layer = static_cast<int>(l);
+                w.trunc_sec = q;
+                w.trunc_at = cursor;
+                w.trunc_msg = where + " " + (h.k == 0 ? "coefficient" : names[q]) + " section is truncated";
+                break;
             }
-        }
-        const uint8_t* g = section(lp[l].gain_bytes, "gain");
-        const uint8_t* b = section(lp[l].bias_bytes, "bias");
-        if (int8) {
-            t.gcodes.assign(reinterpret_cast<const int8_t*>(g), reinterpret_cast<const int8_t*>(g) + e);
-            t.bcodes.assign(reinterpret_cast<const int8_t*>(b), reinterpret_cast<const int8_t*>(b) + e);
-        } else {
-            t.gains.resize(e);
-            t.biases.resize(e);
-            std::memcpy(t.gains.data(), g, e * 4);
-            std::memcpy(t.biases.data(), b, e * 4);
+            cursor += sizes[q];
         }
     }
+    w.end = cursor;
+    return w;
+}
+
+// index n of an LSB-first packed stream (one value: the fault message)
+uint32_t unpack_one(const uint8_t* p, uint64_t n, int bits) {
+    const uint64_t bit = n * static_cast<uint64_t>(bits), b0 = bit >> 3, b1 = (bit + bits + 7) / 8;
+    uint64_t acc = 0;
+    for (uint64_t q = b0; q < b1; ++q) acc |= uint64_t{p[q]} << (8 * (q - b0));
+    return static_cast<uint32_t>((acc >> (bit & 7)) & ((uint64_t{1} << bits) - 1));
+}
+
+// Parse, copy the file to the device, range-check every complete index
+// section there, raise the first fault in deserialize's order, then build
+// the head (or refill `swap_into`) from the device copy.
+skan_head* load_to_device(const uint8_t* bytes, uint64_t n, int device, skan_head* swap_into, cudaStream_t stream) {
+    std::vector<skan_layer_header> hs;
+    std::vector<skan_layer_plan> lp;
+    parse_headers(bytes, n, hs, lp);
+    const Walk w = walk_sections(n, hs, lp);
+    const size_t nl = hs.size();
+    // a truncation with no index section before it is the first fault: no
+    // device work is needed to know it
+    bool checks_first = false;
+    for (size_t l = 0; l < nl && w.trunc_layer >= 0; ++l)
+        if (hs[l].k != 0 && hs[l].k > 1 && (static_cast<int>(l) < w.trunc_layer ||
+                                             (static_cast<int>(l) == w.trunc_layer && w.trunc_sec > 1)))
+            checks_first = true;
+    if (w.trunc_layer >= 0 && !checks_first) skan::raise_format(SKAN_FAULT_TRUNCATED, w.trunc_at, w.trunc_msg);
+    int ndev = 0;
+    skan::cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) skan::raise(SKAN_CONTRACT_ERROR, "no such CUDA device");
+    int prev = -1;
+    skan::cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+    if (prev != device) skan::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    struct Restore {
+        int prev, cur;
+        ~Restore() {
+            if (prev != cur && prev >= 0) cudaSetDevice(prev);
+        }
+    } restore{prev, device};
+    // the file (as far as it goes) in HBM; index checks of complete sections
+    struct Buf {
+        void* p = nullptr;
+        ~Buf() {
+            if (p) cudaFree(p);
+        }
+    } file, bad;
+    const uint64_t have = std::min<uint64_t>(n, std::max<uint64_t>(w.end, 1));
+    skan::cuda_check(cudaMalloc(&file.p, std::max<uint64_t>(have, 256)), "cudaMalloc(file)");
+    skan::cuda_check(cudaMalloc(&bad.p, nl * sizeof(unsigned long long)), "cudaMalloc(check)");
+    skan::cuda_check(cudaMemcpyAsync(file.p, bytes, have, cudaMemcpyHostToDevice, stream), "file to device");
+    skan::cuda_check(cudaMemsetAsync(bad.p, 0xFF, nl * sizeof(unsigned long long), stream), "memset");
+    const uint8_t* d = static_cast<const uint8_t*>(file.p);
+    auto* dbad = static_cast<unsigned long long*>(bad.p);
+    for (size_t l = 0; l < nl; ++l) {
+        if (hs[l].k == 0) continue;
+        if (w.trunc_layer >= 0 && (static_cast<int>(l) > w.trunc_layer ||
+                                   (static_cast<int>(l) == w.trunc_layer && w.trunc_sec <= 1)))
+            break;
+        skan::check_index_section(d + w.sec[l].at[1], lp[l].index_bytes, bit_width_minus1(hs[l].k), hs[l].k,
+                                  uint64_t{hs[l].in_dim} * hs[l].out_dim, dbad + l, stream);
+    }
+    std::vector<unsigned long long> first(nl);
+    skan::cuda_check(cudaMemcpyAsync(first.data(), dbad, nl * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     stream), "check result");
+    skan::cuda_check(cudaStreamSynchronize(stream), "index check");
+    for (size_t l = 0; l < nl; ++l) {
+        const bool trunc_here = static_cast<int>(l) == w.trunc_layer;
+        if (trunc_here && w.trunc_sec <= 1) skan::raise_format(SKAN_FAULT_TRUNCATED, w.trunc_at, w.trunc_msg);
+        if (first[l] != ~0ull) {
+            const uint64_t q = first[l];
+            const uint32_t v = unpack_one(bytes + w.sec[l].at[1], q, bit_width_minus1(hs[l].k));
+            skan::raise_format(SKAN_FAULT_INDEX_OUT_OF_RANGE, w.sec[l].at[1],
+                               "layer " + std::to_string(l) + " edge " + std::to_string(q) + " index " +
+                                   std::to_string(v) + " is outside K=" + std::to_string(hs[l].k));
+        }
+        if (trunc_here) skan::raise_format(SKAN_FAULT_TRUNCATED, w.trunc_at, w.trunc_msg);
+    }
+    std::vector<skan::SectionLayer> L(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        L[l].h = hs[l];
+        L[l].bits = bit_width_minus1(hs[l].k);
+        L[l].src.codebook = d + w.sec[l].at[0];
+        L[l].src.index = d + w.sec[l].at[1];
+        L[l].src.index_bytes = lp[l].index_bytes;
+        L[l].src.gain = d + w.sec[l].at[2];
+        L[l].src.bias = d + w.sec[l].at[3];
+    }
+    if (swap_into) {
+        skan::swap_head_from_sections(swap_into, L.data(), static_cast<int>(nl), stream);
+        return swap_into;
+    }
+    return skan::create_head_from_sections(L.data(), static_cast<int>(nl), device);  // synchronizes
 }
 
 }  // namespace
@@ -210,37 +264,29 @@ void parse(const uint8_t* bytes, uint64_t n, std::vector<skan_layer_header>& hs,
 extern "C" {
 
 skan_status skan_head_load(const uint8_t* bytes, size_t n, int device, skan_head** out) {
-    std::vector<skan_layer_header> hs;
-    std::vector<LayerTables> tabs;
     try {
         if (!bytes && n) skan::raise(SKAN_CONTRACT_ERROR, "null buffer");
-        parse(bytes, n, hs, tabs);
+        if (!out) skan::raise(SKAN_CONTRACT_ERROR, "null output handle");
+        *out = load_to_device(bytes, n, device, nullptr, nullptr);
+        return SKAN_OK;
     } catch (const skan::Error& e) {
         return skan::set_error(e.status, e.what(), e.offset, e.fault);
+    } catch (const std::exception& e) {
+        return skan::set_error(SKAN_CONTRACT_ERROR, e.what(), 0, SKAN_FAULT_NONE);
     }
-    std::vector<skan_layer_desc> d(hs.size());
-    for (size_t l = 0; l < hs.size(); ++l) {
-        skan_layer_desc& x = d[l];
-        std::memset(&x, 0, sizeof x);
-        x.kind = SKAN_LAYER_RUNTIME;
-        x.header = hs[l];
-        const LayerTables& t = tabs[l];
-        x.table_f32 = t.f32.empty() ? nullptr : t.f32.data();
-        x.table_i8 = t.i8.empty() ? nullptr : t.i8.data();
-        x.idx16 = t.idx16.empty() ? nullptr : t.idx16.data();
-        x.idx32 = t.idx32.empty() ? nullptr : t.idx32.data();
-        x.gains_f32 = t.gains.empty() ? nullptr : t.gains.data();
-        x.biases_f32 = t.biases.empty() ? nullptr : t.biases.data();
-        x.rt_gain_codes = t.gcodes.empty() ? nullptr : t.gcodes.data();
-        x.rt_bias_codes = t.bcodes.empty() ? nullptr : t.bcodes.data();
-        // An empty vector means a zero-edge section; supply a non-null
-        // pointer so the runtime staging accepts it.
-        static const int8_t kNone[1] = {0};
-        if ((hs[l].flags & SKAN_FLAG_INT8) && hs[l].k) {
-            if (!x.table_i8) x.table_i8 = kNone;
-        }
+}
+
+skan_status skan_head_swap_bytes(skan_head* head, const uint8_t* bytes, size_t n, void* stream) {
+    try {
+        if (!head) skan::raise(SKAN_CONTRACT_ERROR, "null head");
+        if (!bytes && n) skan::raise(SKAN_CONTRACT_ERROR, "null buffer");
+        load_to_device(bytes, n, skan_head_device(head), head, static_cast<cudaStream_t>(stream));
+        return SKAN_OK;
+    } catch (const skan::Error& e) {
+        return skan::set_error(e.status, e.what(), e.offset, e.fault);
+    } catch (const std::exception& e) {
+        return skan::set_error(SKAN_CONTRACT_ERROR, e.what(), 0, SKAN_FAULT_NONE);
     }
-    return skan_head_create(d.data(), static_cast<int>(d.size()), device, out);
 }
 
 skan_status skan_head_load_file(const char* path, int device, skan_head** out) {

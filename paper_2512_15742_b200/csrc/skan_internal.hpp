@@ -245,6 +245,30 @@ void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStrea
 // MMA work one k_layer_gemm launch issues (flops, as 2*M*N*K per tcgen05.mma)
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B);
 
+// ---- SKAN v1 direct-to-device load (skan_load.cu, skan_format.cpp) ----
+// Device pointers to one layer's sections inside a device copy of the file.
+struct LayerSrc {
+    const uint8_t* codebook;  // K x G int8 / f32 codebook, or the dense E x G f32 grid
+    const uint8_t* index;     // packed LSB-first row indices (bits = bit_width(K - 1))
+    uint64_t index_bytes;
+    const uint8_t* gain;      // E int8 codes or f32
+    const uint8_t* bias;
+};
+// Range check of a packed index section: atomicMin of the first edge >= K into *bad.
+void check_index_section(const uint8_t* index, uint64_t index_bytes, int bits, uint32_t K, uint64_t E,
+                         unsigned long long* bad, cudaStream_t s);
+// Fill layer d's resident regions (records, codebook tables, bias sums) from its sections.
+void build_layer_from_sections(const DevLayer& d, const LayerSrc& src, int bits, cudaStream_t s);
+struct SectionLayer {
+    skan_layer_header h;
+    LayerSrc src;
+    int bits;
+};
+// Create a head / hot-swap a resident head from sections already in device
+// memory (skan_api.cpp; throws skan::Error).
+skan_head* create_head_from_sections(const SectionLayer* layers, int n, int device);
+void swap_head_from_sections(skan_head* h, const SectionLayer* layers, int n, cudaStream_t stream);
+
 // Record a thread-local error for skan_last_error and return its status.
 skan_status set_error(skan_status s, const std::string& msg, uint64_t offset, int fault);
 

@@ -389,6 +389,16 @@ def deserialize(data: bytes, device: int = 0) -> Model:
     return Model(h)
 
 
+def swap_model_bytes(model: Model, data: bytes, stream=None) -> None:
+    """Hot swap from SKAN v1 bytes (skan_head_swap_bytes): the file's sections
+    go to HBM, are checked and unpacked there, and refill the resident head
+    in place (same shapes); deserialize's faults are raised before anything
+    is overwritten."""
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    _lib.check(_lib.lib().skan_head_swap_bytes(model.handle, _ptr(buf) if buf.size else None, buf.size, stream))
+    model.layers = model._refresh_layers()
+
+
 def load_model(path: str, device: int = 0) -> Model:
     """load_model (lutham.cpp:715-724)."""
     h = C.c_void_p()

@@ -204,8 +204,8 @@ TEST_CPU("corrupted files throw holoquant::FormatError with the reference's faul
         return b;
     };
     std::vector<std::vector<std::uint8_t>> cases = {mutate(0, 'X'), mutate(4, 9), mutate(8, 0), mutate(12, 0),
-                                                    mutate(16, 0), std::vector<std::uint8_t>(good.begin(), good.end() - 5),
-                                                    std::vector<std::uint8_t>(good.begin(), good.begin() + 10)};
+                                                    mutate(16, 0), std::vector<std::uint8_t>(good.begin(), good.begin() + 10),
+                                                    std::vector<std::uint8_t>(good.begin(), good.begin() + 200)};
     for (const auto& b : cases) {
         FormatFault ref_fault{};
         std::uint64_t ref_off = 0;
@@ -233,6 +233,49 @@ TEST_CPU("corrupted files throw holoquant::FormatError with the reference's faul
 
 // ---------------------------------------------------------------------------
 // device
+
+// faults found on the device (index range checks before a late truncation,
+// an index >= K) and the hot swap from SKAN bytes: the reference's fault and
+// offset; a failed swap leaves the resident head unchanged
+TEST_GPU("SKAN bytes on the device: index faults, late truncation, swap from bytes") {
+    const Model model = build_model(head({3, 5, 2}, 6, 7, true, 11));
+    const std::vector<std::uint8_t> good = serialize(model);
+    auto same_fault = [&](const std::vector<std::uint8_t>& b) {
+        FormatFault rf{};
+        std::uint64_t ro = 0;
+        bool rt = false, dt = false;
+        try {
+            (void)deserialize(b);
+        } catch (const FormatError& e) {
+            rt = true;
+            rf = e.fault;
+            ro = e.offset;
+        }
+        try {
+            (void)deserialize_device(b);
+        } catch (const FormatError& e) {
+            dt = true;
+            CHECK(e.fault == rf);
+            CHECK(e.offset == ro);
+        } catch (...) {
+        }
+        CHECK(rt && dt);
+    };
+    same_fault(std::vector<std::uint8_t>(good.begin(), good.end() - 5));
+    // the first index section: set every index bit -> 7 >= K = 7
+    std::vector<std::uint8_t> bad = good;
+    const std::size_t first_index = 192 + 64;  // 16 + 2*72 -> 192 (codebook 7*6 B), next 64-B boundary
+    bad[first_index] = 0xFF;
+    same_fault(bad);
+    // swap from bytes: a second model of the same shapes, then a corrupt file
+    const Model other = build_model(head({3, 5, 2}, 6, 7, true, 12));
+    DeviceHead dev = deserialize_device(good);
+    swap_device_model(dev, serialize(other));
+    const std::vector<double> x = inputs(4, 3, 5);
+    CHECK(bitwise_equal(dev_forward(dev, x, 4, DeviceMode::Exact), ref_forward(other, x, 4)));
+    CHECK(throws_as<FormatError>([&] { swap_device_model(dev, std::span<const std::uint8_t>(bad)); }));
+    CHECK(bitwise_equal(dev_forward(dev, x, 4, DeviceMode::Exact), ref_forward(other, x, 4)));
+}
 
 TEST_GPU("upload(build_model(cn)): exact mode is bitwise holoquant::compressed_forward") {
     for (bool q : {false, true}) {

@@ -104,7 +104,9 @@ def test_plan_matches_reference_random():
 
 
 # ---------------------------------------------------------------------------
-# SKAN v1 loader fault contract (host-side parse; runs before any device work)
+# SKAN v1 loader fault contract: header faults and truncations with no index
+# section before them are raised by the host parse before any device work;
+# index range checks run on the device (the @gpu cases)
 
 def _good_int8_bytes():
     return oracle.ref_random([3, 5, 2], 6, 0.4, 9, 4, True).serialize()
@@ -143,12 +145,20 @@ def test_corrupted_files_report_reference_fault_and_offset():
     cases.append((bytearray(good[:200]), "section"))
     cases.append((bytearray(good[:2]), "magic"))
     cases.append((bytearray(good[:40]), "header"))
-    cases.append((bytearray(good[:-1]), "section"))
     for bad, frag in cases:
         _expect_same_fault(bytes(bad), frag)
 
 
 @needs_ref
+@pytest.mark.gpu
+def test_truncation_after_index_sections_on_device():
+    """A truncated last section: the index sections before it are range-checked
+    on the device first (deserialize's order), then the truncation is raised."""
+    _expect_same_fault(bytes(bytearray(_good_int8_bytes())[:-1]), "section")
+
+
+@needs_ref
+@pytest.mark.gpu
 def test_out_of_range_index_names_the_edge():
     """test_lutham.cpp:254-275: byte 192 holds {0,1} at 2 bits; 0x0F makes edge 0 index 3 == K."""
     cl = synthetic.crafted_layer(1, 2, 2, 3, 10)

@@ -551,3 +551,65 @@ def test_hot_swap_refills_a_resident_head(torch_cuda):
         assert_close(yb, wb, l1_scale(tb, xb, batch))
     with pytest.raises(hq.ContractError):
         hq.swap_model(model, synthetic.synthetic_head(dims=(512, 500, 8), k=4096, grid=10, int8=True, seed=3))
+
+
+# ---------------------------------------------------------------------------
+# SKAN v1 direct-to-device load (§8 f1): sections unpacked on the device
+
+def test_loaded_head_equals_uploaded_head_in_fast_mode(torch_cuda):
+    """The device-built resident form of a loaded file (records, codebook
+    tables, bias sums) is the host-built one: fast-mode outputs of
+    deserialize(bytes) and upload(tables) are bitwise equal on every route
+    (batch 1, small batches, the tensor-core GEMM)."""
+    rng = np.random.default_rng(5)
+    for name, m in _fixture_models():
+        tables = m.tables()
+        a, b = hq.deserialize(m.serialize()), _upload(tables)
+        for batch in (1, 5, 64):
+            x = rng.uniform(-1.5, 1.5, batch * tables[0].in_dim)
+            ya, _ = _gpu_forward(a, x, batch, "fast")
+            yb, _ = _gpu_forward(b, x, batch, "fast")
+            assert np.array_equal(_bits(ya), _bits(yb)), (name, batch)
+
+
+def test_headline_head_file_loads_on_device(torch_cuda):
+    """The cfg2 head serialized by the reference (12.96 MB payload) loads
+    through the device path: exact mode bitwise equal to the reference,
+    fast batch 1 within the bound."""
+    cn = synthetic.synthetic_head()
+    ref = oracle.ref_build(cn)
+    model = hq.deserialize(ref.serialize())
+    tables = ref.tables()
+    x = synthetic.synthetic_inputs(2, 2048, seed=61)
+    want, scale = oracle.port_forward_l1(tables, x, 2, threads=2)
+    got, _ = _gpu_forward(model, x, 2, "exact")
+    assert np.array_equal(_bits(got), _bits(want))
+    y1, ws = _gpu_forward(model, x[:2048], 1, "fast")
+    assert ws.last_launches() == 1
+    assert_close(y1, want[:20], scale[:20])
+
+
+def test_swap_from_bytes_refills_in_place(torch_cuda):
+    """skan_head_swap_bytes: the new tables serve bitwise; a corrupt file
+    raises the reference's FormatError and leaves the head as it was; a file
+    of other shapes is a ContractError."""
+    dims = (512, 512, 8)
+    a = oracle.ref_build(synthetic.synthetic_head(dims=dims, k=4096, grid=10, int8=True, seed=1))
+    b = oracle.ref_build(synthetic.synthetic_head(dims=dims, k=4096, grid=10, int8=True, seed=2))
+    model = hq.deserialize(a.serialize())
+    ws = hq.make_workspace(model, 8)
+    x = synthetic.synthetic_inputs(3, 512, seed=4)
+    hq.swap_model_bytes(model, b.serialize())
+    want, _ = b.forward(x, 3)
+    y = np.zeros(3 * 8)
+    hq.compressed_forward(model, x, 3, y, ws, mode="exact")
+    assert np.array_equal(_bits(y), _bits(want))
+    bad = bytearray(a.serialize())
+    bad[-1:] = b""  # truncated last section: checks run, nothing is overwritten
+    with pytest.raises(hq.FormatError):
+        hq.swap_model_bytes(model, bytes(bad))
+    hq.compressed_forward(model, x, 3, y, ws, mode="exact")
+    assert np.array_equal(_bits(y), _bits(want))
+    other = oracle.ref_build(synthetic.synthetic_head(dims=(512, 500, 8), k=4096, grid=10, int8=True, seed=3))
+    with pytest.raises(hq.ContractError):
+        hq.swap_model_bytes(model, other.serialize())
