@@ -437,6 +437,72 @@ def main():
                                       "algorithmic_bytes": b4}}
         del dm, dws
 
+    # ---- multi-GPU partitionings (N > 1): cfg5 head-sharded, cfg4 column-sharded
+    if world > 1 and not args.no_extra:
+        from paper_2512_15742_b200 import sharding
+        barrier()
+        # cfg5: 4 cfg2 heads per GPU (4N in all; 32 at N = 8), one feature
+        # batch of 256 broadcast from rank 0 over NCCL, outputs all-gathered
+        nh = 4 * world
+        lo_h, hi_h = sharding.shard_ranges(nh, world)[rank]
+        runners = [sharding.DeviceRunner(
+            hq.build_model(synthetic.synthetic_head(dims=DIMS, k=K, grid=G, int8=True, seed=2026 + 7 * h), device=local),
+            max_batch=256, mode=args.mode) for h in range(lo_h, hi_h)]
+        hs = sharding.HeadSharded(runners, nh, DIMS[-1], rank, world)
+        xh = torch.from_numpy(synthetic.synthetic_inputs(256, DIMS[0], seed=777)).to(dev)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                hs.forward(xh, 256, DIMS[0])
+        barrier()
+        t_h = []
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                flush.zero_()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                hs.forward(xh, 256, DIMS[0])
+                e1.record(stream)
+                stream.synchronize()
+                t_h.append(e0.elapsed_time(e1) * 1e3)
+        us_h = sync_max(statistics.median(t_h))
+        del runners, hs
+        # cfg4: layer 0's 13,664 columns split over the ranks, hidden
+        # activations all-gathered over NCCL, the 13664 -> 20 tail replicated
+        dl = synthetic.dense_runtime_head()
+        shard, tail = sharding.column_sharded_layers(dl, rank, world)
+        del dl
+        cs = sharding.ColumnSharded(sharding.DeviceRunner(hq.upload(shard, device=local), 64, args.mode),
+                                    sharding.DeviceRunner(hq.upload(tail, device=local), 64, args.mode),
+                                    13664, rank, world)
+        del shard, tail
+        x4s = torch.from_numpy(synthetic.synthetic_inputs(64, DIMS[0], seed=6)).to(dev)
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                cs.forward(x4s, 64)
+        t_c = []
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                flush.zero_()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                cs.forward(x4s, 64)
+                e1.record(stream)
+                stream.synchronize()
+                t_c.append(e0.elapsed_time(e1) * 1e3)
+        us_c = sync_max(statistics.median(t_c))
+        del cs
+        if rank == 0:
+            extra["sharded"] = {
+                "cfg5_head_sharded": {"heads": nh, "batch": 256, "us_per_step": us_h,
+                                      "head_samples_per_s": nh * 256 / us_h * 1e6,
+                                      "how": "HeadSharded: NCCL broadcast of the f64 features, 4 heads per GPU on "
+                                             "skan_forward_multi, NCCL all-gather of the outputs; max over ranks"},
+                "cfg4_column_sharded": {"batch": 64, "us_per_step": us_c, "samples_per_s": 64 / us_c * 1e6,
+                                        "how": "ColumnSharded: layer-0 columns split over the GPUs, NCCL all-gather "
+                                               "of the hidden activations, tail replicated; max over ranks"}}
+
     # ---- exact mode (f64, the reference's operation order, bitwise equal) ---
     if not args.no_extra and rank == 0:
         ex1 = event_us(lambda: _lib.check(L.skan_forward_async(model.handle, ws.handle, d_x.data_ptr(), B,

@@ -18,10 +18,13 @@ The reference forward has no cross-sample state (lutham.cpp:837-848), so:
     bit-exact layer-0 knot selection needs the caller's doubles), each rank
     runs its group on one device batch, outputs are gathered.
 
-A "runner" is anything with ``forward(x: np.ndarray[f64], batch) ->
-np.ndarray[f64]``; :class:`DeviceRunner` is the product's (libskan on the
-rank's GPU).  The partitioning and exchange logic here never computes
-edges itself.
+A "runner" is anything with ``forward_dev(x: Tensor[f64], batch) ->
+Tensor[f64]`` on its rank's device; :class:`DeviceRunner` is the product's
+(libskan on the rank's GPU, no host round trip).  Exchanges are
+torch.distributed collectives on those tensors: NCCL moves them GPU to GPU
+over NVLink/NVSwitch; under gloo (the CPU tests, or two ranks sharing one
+GPU) they are staged through host memory.  The partitioning and exchange
+logic here never computes edges itself.
 """
 from __future__ import annotations
 
@@ -98,25 +101,40 @@ def column_slice_dense(kl: KanLayer, lo: int, hi: int) -> KanLayer:
 
 
 # ---------------------------------------------------------------------------
-# runners and collectives
+# runners and collectives (device-resident data path)
 
 class DeviceRunner:
-    """A resident head on this rank's GPU behind the product C ABI."""
+    """A resident head on this rank's GPU behind the product C ABI.
+    ``forward_dev`` takes and returns f64 tensors on the head's device: the
+    forward is enqueued on the current stream (skan_forward_async), nothing
+    crosses to the host."""
 
     def __init__(self, model, max_batch: int = 256, mode: str = "fast"):
         from . import lutham
         self.model = model
         self.ws = lutham.make_workspace(model, max_batch=max_batch)
         self.mode = mode
-        self._fwd = lutham.compressed_forward
+        self._lutham = lutham
 
     @property
     def output_dim(self) -> int:
         return self.model.output_dim()
 
+    def forward_dev(self, x, batch: int):
+        import torch
+        y = torch.empty(batch * self.model.output_dim(), dtype=torch.float64, device=x.device)
+        self._lutham.forward_async(self.model, x.contiguous(), batch, y, self.ws, mode=self.mode)
+        return y
+
+    def check(self) -> None:
+        """Synchronize and raise ValueError for a non-finite input (kan.cpp:29)."""
+        self.ws.check()
+
     def forward(self, x: np.ndarray, batch: int) -> np.ndarray:
+        """Host-buffer convenience (skan_forward with SKAN_PTR_HOST)."""
         y = np.zeros(batch * self.model.output_dim())
-        self._fwd(self.model, np.ascontiguousarray(x, np.float64), batch, y, self.ws, mode=self.mode)
+        self._lutham.compressed_forward(self.model, np.ascontiguousarray(x, np.float64), batch, y, self.ws,
+                                        mode=self.mode)
         return y
 
 
@@ -125,42 +143,67 @@ def _dist():
     return dist
 
 
-def _tensor(a: np.ndarray, device):
+def _staged(t):
+    """NCCL moves CUDA tensors directly (NVLink/NVSwitch); gloo (CPU tests,
+    or two ranks sharing one GPU) exchanges through host memory."""
+    dist = _dist()
+    return t.is_cuda and dist.get_backend() != "nccl"
+
+
+def all_gather_tensor(t) -> list:
+    """every rank's tensor of t's shape, in rank order, on t's device"""
     import torch
-    return torch.from_numpy(np.ascontiguousarray(a)).to(device)
+    dist = _dist()
+    world = dist.get_world_size()
+    src = t.cpu() if _staged(t) else t.contiguous()
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src)
+    return [p.to(t.device) for p in parts] if _staged(t) else parts
 
 
-def all_gather_rows(y_local: np.ndarray, counts: Sequence[int], width: int, device="cpu") -> np.ndarray:
+def broadcast_tensor(t, src: int = 0):
+    dist = _dist()
+    if _staged(t):
+        h = t.cpu()
+        dist.broadcast(h, src=src)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src)
+    return t
+
+
+def all_gather_rows(y_local, counts: Sequence[int], width: int):
     """Concatenate every rank's [counts[r], width] block in rank order
-    (uneven counts padded to the largest)."""
+    (uneven counts padded to the largest); device tensors in, device out."""
     import torch
-    dist = _dist()
     mx = max(counts)
-    buf = np.zeros((mx, width))
-    buf[: y_local.size // max(width, 1)] = y_local.reshape(-1, width)
-    t = _tensor(buf, device)
-    parts = [torch.empty_like(t) for _ in counts]
-    dist.all_gather(parts, t)
-    return np.concatenate([p.cpu().numpy()[:c] for p, c in zip(parts, counts)], axis=0)
+    buf = torch.zeros((mx, width), dtype=y_local.dtype, device=y_local.device)
+    n = y_local.numel() // max(width, 1)
+    buf[:n] = y_local.reshape(n, width)
+    parts = all_gather_tensor(buf)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
 
 
-def all_gather_columns(y_local: np.ndarray, batch: int, widths: Sequence[int], device="cpu") -> np.ndarray:
+def all_gather_columns(y_local, batch: int, widths: Sequence[int]):
     """[batch, widths[r]] column blocks of every rank -> [batch, sum(widths)]
-    in rank (= column) order."""
+    in rank (= column) order, contiguous on the device."""
     import torch
-    dist = _dist()
     mx = max(widths)
-    buf = np.zeros((batch, mx))
-    w = y_local.size // max(batch, 1)
+    buf = torch.zeros((batch, mx), dtype=y_local.dtype, device=y_local.device)
+    w = y_local.numel() // max(batch, 1)
     buf[:, :w] = y_local.reshape(batch, w)
-    t = _tensor(buf, device)
-    parts = [torch.empty_like(t) for _ in widths]
-    dist.all_gather(parts, t)
-    return np.concatenate([p.cpu().numpy()[:, :c] for p, c in zip(parts, widths)], axis=1)
+    parts = all_gather_tensor(buf)
+    return torch.cat([p[:, :c] for p, c in zip(parts, widths)], dim=1).contiguous()
+
+
+def _check(*runners):
+    for r in runners:
+        if hasattr(r, "check"):
+            r.check()
 
 
 # ---------------------------------------------------------------------------
-# the three partitionings
+# the three partitionings (rank-local runners, device tensors throughout)
 
 @dataclass
 class BatchSharded:
@@ -168,36 +211,38 @@ class BatchSharded:
     runner: object
     rank: int
     world: int
-    device: object = "cpu"
 
-    def forward_local(self, x_global: np.ndarray, batch: int, in_dim: int) -> Tuple[np.ndarray, Tuple[int, int]]:
+    def forward_local(self, x_global, batch: int, in_dim: int):
         lo, hi = shard_ranges(batch, self.world)[self.rank]
-        return self.runner.forward(x_global[lo * in_dim:hi * in_dim], hi - lo), (lo, hi)
+        return self.runner.forward_dev(x_global[lo * in_dim:hi * in_dim], hi - lo), (lo, hi)
 
-    def forward(self, x_global: np.ndarray, batch: int, in_dim: int) -> np.ndarray:
-        """Every rank returns the full [batch, out] result (one all-gather)."""
+    def forward(self, x_global, batch: int, in_dim: int):
+        """Every rank returns the full [batch * out] result (one all-gather)."""
         y, _ = self.forward_local(x_global, batch, in_dim)
         counts = [hi - lo for lo, hi in shard_ranges(batch, self.world)]
-        return all_gather_rows(y, counts, self.runner.output_dim, self.device).reshape(-1)
+        out = all_gather_rows(y, counts, self.runner.output_dim).reshape(-1)
+        _check(self.runner)
+        return out
 
 
 @dataclass
 class ColumnSharded:
     """cfg4: rank r owns layer-0 output columns shard_ranges(out0, world)[r]
-    (``shard_runner``); the hidden activations are all-gathered once, then
-    the replicated tail (``tail_runner``, layers 1..) finishes."""
+    (``shard_runner``); the hidden activations are all-gathered once on the
+    device, then the replicated tail (``tail_runner``, layers 1..) finishes."""
     shard_runner: object
     tail_runner: object
     out0: int
     rank: int
     world: int
-    device: object = "cpu"
 
-    def forward(self, x: np.ndarray, batch: int) -> np.ndarray:
-        h_local = self.shard_runner.forward(x, batch)
+    def forward(self, x, batch: int):
+        h_local = self.shard_runner.forward_dev(x, batch)
         widths = [hi - lo for lo, hi in shard_ranges(self.out0, self.world)]
-        hidden = all_gather_columns(h_local, batch, widths, self.device)
-        return self.tail_runner.forward(hidden.reshape(-1), batch)
+        hidden = all_gather_columns(h_local, batch, widths)
+        y = self.tail_runner.forward_dev(hidden.reshape(-1), batch)
+        _check(self.shard_runner, self.tail_runner)
+        return y
 
 
 def column_sharded_layers(layers: Sequence, rank: int, world: int,
@@ -210,24 +255,30 @@ def column_sharded_layers(layers: Sequence, rank: int, world: int,
 
 @dataclass
 class HeadSharded:
-    """cfg5: heads shard_ranges(H, world)[rank] on this rank, one shared
-    feature batch broadcast from rank 0."""
+    """cfg5: heads shard_ranges(H, world)[rank] on this rank, one shared f64
+    feature batch broadcast from rank 0 (f64: the bit-exact layer-0 knot
+    selection needs the caller's doubles).  Device runners of one GPU run
+    their heads concurrently (skan_forward_multi)."""
     runners: List[object]  # this rank's heads, in global head order
     n_heads: int
     out_dim: int           # shared by all heads
     rank: int
     world: int
-    device: object = "cpu"
 
-    def forward(self, x: np.ndarray, batch: int, in_dim: int) -> np.ndarray:
+    def forward(self, x, batch: int, in_dim: int):
         """Returns [H, batch, out] on every rank (heads must share out_dim)."""
         import torch
-        dist = _dist()
-        t = _tensor(x if self.rank == 0 else np.zeros(batch * in_dim), self.device)
-        dist.broadcast(t, src=0)
-        xb = t.cpu().numpy()
-        ys = [r.forward(xb, batch) for r in self.runners]
+        x = broadcast_tensor(x.contiguous(), src=0)
+        if self.runners and all(isinstance(r, DeviceRunner) for r in self.runners):
+            from . import lutham
+            ys = [torch.empty(batch * self.out_dim, dtype=torch.float64, device=x.device) for _ in self.runners]
+            lutham.forward_multi([r.model for r in self.runners], [r.ws for r in self.runners], x, batch, ys,
+                                 mode=self.runners[0].mode)
+        else:
+            ys = [r.forward_dev(x, batch) for r in self.runners]
         counts = [hi - lo for lo, hi in shard_ranges(self.n_heads, self.world)]
         width = batch * self.out_dim
-        local = np.concatenate(ys) if ys else np.zeros(0)
-        return all_gather_rows(local, counts, width, self.device).reshape(self.n_heads, batch, self.out_dim)
+        local = torch.cat(ys) if ys else torch.zeros(0, dtype=torch.float64, device=x.device)
+        out = all_gather_rows(local, counts, width).reshape(self.n_heads, batch, self.out_dim)
+        _check(*self.runners)
+        return out

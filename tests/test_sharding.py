@@ -17,13 +17,16 @@ from paper_2512_15742_b200 import sharding, synthetic
 
 
 class OracleRunner:
+    """Test infrastructure: the oracle as a rank-local runner on CPU tensors."""
+
     def __init__(self, runtime_layers):
         self.tables = [oracle.Tables.from_runtime(rl) for rl in runtime_layers]
         self.output_dim = self.tables[-1].out_dim
 
-    def forward(self, x, batch):
-        y, _ = oracle.port_forward(self.tables, np.asarray(x, np.float64), batch)
-        return y
+    def forward_dev(self, x, batch):
+        import torch
+        y, _ = oracle.port_forward(self.tables, x.cpu().numpy().astype(np.float64), batch)
+        return torch.from_numpy(y).to(x.device)
 
 
 def _free_port():
@@ -41,22 +44,33 @@ def _worker(rank, world, port, case, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        import torch
+        gpu = case.startswith("gpu_")
+        kind = case[4:] if gpu else case
+        dev = torch.device("cuda", 0) if gpu else torch.device("cpu")
+        if gpu:
+            import paper_2512_15742_b200 as hq
+            runner = lambda rl: sharding.DeviceRunner(hq.upload(rl, device=0), max_batch=8)  # noqa: E731
+        else:
+            runner = OracleRunner
         layers = _head()
-        x = synthetic.synthetic_inputs(5, 24, seed=3, grid=7)
-        if case == "batch":
-            bs = sharding.BatchSharded(OracleRunner(layers), rank, world)
+        x = torch.from_numpy(synthetic.synthetic_inputs(5, 24, seed=3, grid=7)).to(dev)
+        if kind == "batch":
+            bs = sharding.BatchSharded(runner(layers), rank, world)
             y = bs.forward(x, 5, 24)
-        elif case == "columns":
+        elif kind == "columns":
             shard, tail = sharding.column_sharded_layers(layers, rank, world)
-            cs = sharding.ColumnSharded(OracleRunner(shard), OracleRunner(tail), layers[0].header.out_dim, rank, world)
+            cs = sharding.ColumnSharded(runner(shard), runner(tail), layers[0].header.out_dim, rank, world)
             y = cs.forward(x, 5)
         else:  # heads
             heads = [synthetic.runtime_layers(synthetic.synthetic_head(dims=(24, 9, 3), k=30, grid=7, int8=True,
                                                                        seed=50 + h)) for h in range(5)]
             lo, hi = sharding.shard_ranges(5, world)[rank]
-            hs = sharding.HeadSharded([OracleRunner(heads[h]) for h in range(lo, hi)], 5, 3, rank, world)
-            y = hs.forward(x if rank == 0 else np.zeros_like(x), 5, 24)
-        q.put((rank, np.asarray(y).tobytes()))
+            hs = sharding.HeadSharded([runner(heads[h]) for h in range(lo, hi)], 5, 3, rank, world)
+            y = hs.forward(x if rank == 0 else torch.zeros_like(x), 5, 24)
+        if gpu:
+            assert y.is_cuda  # the result stays on the device
+        q.put((rank, y.cpu().numpy().astype(np.float64).tobytes()))
     finally:
         dist.destroy_process_group()
 
@@ -100,6 +114,10 @@ def test_column_slices_reassemble_the_layer_bitwise():
 
 @pytest.mark.parametrize("case", ["batch", "columns"])
 def test_two_rank_partitioning_equals_unsharded_forward(case):
+    _two_rank_equals_unsharded(case)
+
+
+def _two_rank_equals_unsharded(case):
     layers = _head()
     x = synthetic.synthetic_inputs(5, 24, seed=3, grid=7)
     want, _ = oracle.port_forward([oracle.Tables.from_runtime(rl) for rl in layers], x, 5)
@@ -118,3 +136,36 @@ def test_two_rank_head_sharding_broadcasts_features_and_gathers_heads():
     ys = _run("heads")
     for y in ys:
         assert np.array_equal(y, np.concatenate(want))
+
+
+# ---------------------------------------------------------------------------
+# the product runner: two ranks (gloo) sharing the one GPU, DeviceRunner on
+# cuda:0, device tensors end to end; exact mode would be bitwise, fast mode
+# (the runner's default) is checked against the oracle's tolerance scale
+
+def _device_runner_case(case):
+    from helpers import assert_close
+    layers = _head()
+    x = synthetic.synthetic_inputs(5, 24, seed=3, grid=7)
+    tables = [oracle.Tables.from_runtime(rl) for rl in layers]
+    want, scale = oracle.port_forward_l1(tables, x, 5)
+    for y in _run("gpu_" + case):
+        assert_close(y, want, scale)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["batch", "columns"])
+def test_two_rank_device_runner_partitioning(case):
+    _device_runner_case(case)
+
+
+@pytest.mark.gpu
+def test_two_rank_device_runner_head_sharding():
+    from helpers import assert_close
+    x = synthetic.synthetic_inputs(5, 24, seed=3, grid=7)
+    ys = _run("gpu_heads")
+    for h in range(5):
+        rl = synthetic.runtime_layers(synthetic.synthetic_head(dims=(24, 9, 3), k=30, grid=7, int8=True, seed=50 + h))
+        want, scale = oracle.port_forward_l1([oracle.Tables.from_runtime(r) for r in rl], x, 5)
+        for y in ys:
+            assert_close(y.reshape(5, -1)[h], want, scale)
