@@ -221,6 +221,7 @@ struct skan_head {
     int b1_grid = 0;
     size_t b1_smem = 0;
     skan::HeadB1Args b1_plan{};  // layers + shared-memory plan; per-call pointers filled at launch
+    void* b1_rows = nullptr;     // v2: layer 1's per-edge codebook rows (derived from the head's tables)
     // Forwards hold it shared while they read the layer views and enqueue
     // (host-buffer calls: until they return); skan_head_swap holds it
     // exclusively, so a swap never races a forward's reads of dl/b1_plan.
@@ -641,12 +642,20 @@ std::vector<Staged> stage_all(const skan_layer_desc* layers, int n) {
 }
 
 // Kernel-side copies of the layer views for the persistent batch-1 plan.
-void refresh_b1_layers(skan_head* h) {
+void refresh_b1_layers(skan_head* h, cudaStream_t stream = nullptr) {
     const int nl = static_cast<int>(h->dl.size());
     for (int l = 0; l < nl && l < skan::kMaxHeadLayers; ++l) h->b1_plan.L[l] = h->dl[l];
     const DevLayer& L0 = h->dl[0];
     for (int i = 0; i < L0.G && i < 33; ++i)  // node_position, kan.cpp:21-26
         h->b1_plan.node0[i] = i == 0 ? L0.lo : (i == L0.G - 1 ? L0.hi : L0.lo + static_cast<double>(i) * L0.dx);
+    const size_t rb = skan::head_b1_rows_bytes(h->b1_plan);
+    if (rb) {  // rebuilt from the current tables (creation, hot swap)
+        if (!h->b1_rows) skan::cuda_check(cudaMalloc(&h->b1_rows, rb), "cudaMalloc (batch-1 layer-1 rows)");
+        h->b1_plan.l1rows = static_cast<const uint4*>(h->b1_rows);
+        skan::cuda_check(skan::head_b1_build_rows(h->b1_plan, static_cast<uint4*>(h->b1_rows), stream),
+                         "batch-1 layer-1 rows");
+        skan::cuda_check(cudaStreamSynchronize(stream), "batch-1 layer-1 rows");
+    }
 }
 
 skan_head* create_head_staged(std::vector<Staged>& st, int device);
@@ -950,7 +959,7 @@ void swap_staged(skan_head* h, std::vector<Staged>& st, cudaStream_t stream) {
     h->lplan = lp;
     h->totals = tot;
     upload(h, st, /*swap=*/true, stream);
-    if (h->b1_ok) refresh_b1_layers(h);
+    if (h->b1_ok) refresh_b1_layers(h, stream);
 }
 
 // Staging of directly loaded layers: headers (already checked by the SKAN
@@ -1035,6 +1044,7 @@ skan_status skan_head_destroy(skan_head* h) {
             DeviceGuard g(h->device);
             if (h->l2_frac > 0.f) update_persist_limit(h->device, -static_cast<int64_t>(h->dbytes));
             cudaFree(h->dmem);
+            if (h->b1_rows) cudaFree(h->b1_rows);
         }
         delete h;
     });

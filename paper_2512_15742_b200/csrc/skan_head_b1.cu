@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "skan_device.cuh"
 #include "skan_internal.hpp"
@@ -599,8 +600,11 @@ __device__ __forceinline__ float t_of(const DevLayer& L, double x, double nlo, d
 
 __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ HeadB1Args hp) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const HeadB1Args& h = hp;
-    __shared__ __align__(8) uint64_t s_bar[2];  // [0] plane + layer-0 records, [1] layer-1 records
+    // The parameters this kernel reads (layers 0-1 and the launch fields) are
+    // copied into shared memory once, all words in parallel: afterwards no
+    // phase pays a constant-cache miss on a parameter line it touches first.
+    __shared__ __align__(16) HeadB1Args s_h;
+    __shared__ __align__(8) uint64_t s_bar[2];  // [0] plane + layer-0 records, [1] layer-1 records + rows
     __shared__ int s_wcnt[kW][32];              // per-warp bracket counts
     __shared__ int s_rows[kMaxRows];
     __shared__ float s_trow[kMaxRows];
@@ -609,43 +613,59 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
     __shared__ int s_last;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int P = gridDim.x, c = blockIdx.x;
-    const DevLayer& L = h.L[0];
-    const DevLayer& L1 = h.L[1];
-    // x first: four coalesced loads per thread
+    // x first: four coalesced loads per thread (straight from the parameters)
     double xr[kPer2];
     {
+        const int in0 = hp.L[0].in;
+        const double* x = hp.x;
         const int base = 256 * warp + 2 * lane;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int i = base + 64 * q;
-            if (h.x_tma && i + 1 < L.in) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(h.x + i));
+            if (hp.x_tma && i + 1 < in0) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(x + i));
                 xr[2 * q] = v.x;
                 xr[2 * q + 1] = v.y;
             } else {
-                xr[2 * q] = i < L.in ? h.x[i] : 0.0;
-                xr[2 * q + 1] = i + 1 < L.in ? h.x[i + 1] : 0.0;
+                xr[2 * q] = i < in0 ? x[i] : 0.0;
+                xr[2 * q + 1] = i + 1 < in0 ? x[i + 1] : 0.0;
             }
         }
     }
-    stamp(hp, 0);
-    if (hp.exit_at == 100) return;
+    {
+        constexpr int a1 = static_cast<int>((offsetof(HeadB1Args, L) + 2 * sizeof(DevLayer)) / 4);
+        constexpr int b0 = static_cast<int>(offsetof(HeadB1Args, planes0) / 4);
+        constexpr int b1 = static_cast<int>(sizeof(HeadB1Args) / 4);
+        static_assert(offsetof(HeadB1Args, planes0) % 4 == 0 && a1 + (b1 - b0) <= kT, "parameter copy");
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(&hp);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(&s_h);
+        if (tid < a1) dst[tid] = src[tid];
+        else if (tid - a1 < b1 - b0) dst[b0 + tid - a1] = src[b0 + tid - a1];
+    }
+    __syncthreads();
+    const HeadB1Args& h = s_h;
+    const DevLayer& L = h.L[0];
+    const DevLayer& L1 = h.L[1];
+    stamp(h, 0);
+    if (h.exit_at == 100) return;
     unsigned char* s_pref = smem + h.pref_offset;
+    uint4* s_cb = reinterpret_cast<uint4*>(smem + h.cbrow_offset);
     int r10, r11;
     rows_of(L1, c, P, r10, r11);
     const int nr = r11 - r10;
     if (tid == 0) {
+        // layer 1's records and its edges' codebook rows (pre-gathered at
+        // upload, one 16-byte row per edge) for my rows: no dependent gather
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
-        const uint32_t bytes = static_cast<uint32_t>(nr) * L1.out * 4u;
-        mbar_expect_tx(&s_bar[1], bytes);
-        bulk_g2s(s_pref, L1.rec + static_cast<size_t>(r10) * L1.out, bytes, &s_bar[1]);
-    } else if (warp == 1 && lane < 4) {
-        // the whole head streams HBM -> L2 from the first microsecond, sliced over the CTAs
+        const uint32_t n1 = static_cast<uint32_t>(nr) * L1.out;
+        mbar_expect_tx(&s_bar[1], n1 * 4u + n1 * 16u);
+        bulk_g2s(s_pref, L1.rec + static_cast<size_t>(r10) * L1.out, n1 * 4u, &s_bar[1]);
+        bulk_g2s(s_cb, h.l1rows + static_cast<size_t>(r10) * L1.out, n1 * 16u, &s_bar[1]);
+    } else if (warp == 1 && lane < 2) {
+        // layer 0 streams HBM -> L2 from the first microsecond, sliced over the CTAs
         if (lane == 0) prefetch_l2_slice(L.rec, static_cast<size_t>(L.in) * L.out * 4, c, P);
-        else if (lane == 1) prefetch_l2_slice(L.pair8, static_cast<size_t>(L.K) * (L.G - 1) * 2, c, P);
-        else if (lane == 2) prefetch_l2_slice(L1.rec, static_cast<size_t>(L1.in) * L1.out * 4, c, P);
-        else prefetch_l2_slice(L1.cb8, static_cast<size_t>(L1.K) * L1.rs, c, P);
+        else prefetch_l2_slice(L.pair8, static_cast<size_t>(L.K) * (L.G - 1) * 2, c, P);
     }
     const double b1_reg = tid < nr ? L.bias_sum[r10 + tid] : 0.0;
     const double bf_reg = tid < L1.out ? L1.bias_sum[tid] : 0.0;
@@ -738,6 +758,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
         mbar_expect_tx(&s_bar[0], plane_bytes + static_cast<uint32_t>(rec_rows) * row_bytes);
         bulk_g2s(smem, L.pair8 + static_cast<size_t>(bucket) * L.K, plane_bytes, &s_bar[0]);
     }
+    stamp(h, 8);
     // my rows of the bucket in ascending i: within the warp i = 64q + 2l + e
     if (bucket < GP) {
         const uint32_t pat = static_cast<uint32_t>(bucket) * 0x01010101u;
@@ -768,39 +789,30 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
             base += __popc(B0) + __popc(B1);
         }
     }
-    // while the plane and records land: layer 1's codebook rows of my edges
-    uint4* s_cb = reinterpret_cast<uint4*>(smem + h.cbrow_offset);
-    {
-        const uint32_t* srec1 = reinterpret_cast<const uint32_t*>(s_pref);
-        const int n1 = nr * L1.out;
-        if (tid < n1) {
-            mbar_wait(&s_bar[1], 0);
-            for (int e = tid; e < n1; e += kT)
-                s_cb[e] = __ldg(reinterpret_cast<const uint4*>(L1.cb8 + static_cast<size_t>(srec1[e] & 0xFFFFu) * L1.rs));
-        }
-    }
+    stamp(h, 9);
     stamp(h, 3);
     if (h.exit_at == 3) return;
     __syncthreads();
     if (bucket < GP) mbar_wait(&s_bar[0], 0);
     stamp(h, 4);
     if (h.exit_at == 4) return;
-    // layer 0: thread t owns outputs 4t..4t+3 over this CTA's rows, ascending
-    float* s_out = reinterpret_cast<float*>(smem + h.out_offset);
+    // layer 0: thread t owns outputs 4t..4t+3 over this CTA's rows, ascending;
+    // its four sums go straight to the consumer-blocked partials
+    // part0[d][c][j - r0(d)], d = the CTA whose layer-1 rows hold j
     {
         const int j = tid * 4;
         if (j < L.out) {
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
             auto edge4 = [&](const uint4& r, float t) {
                 float c0, dc;
                 pair_to_f(s_plane[r.x & 0xFFFFu], c0, dc);
-                a0 = fmaf(gain_of_rec(L, r.x), fmaf(t, dc, c0), a0);
+                a[0] = fmaf(gain_of_rec(L, r.x), fmaf(t, dc, c0), a[0]);
                 pair_to_f(s_plane[r.y & 0xFFFFu], c0, dc);
-                a1 = fmaf(gain_of_rec(L, r.y), fmaf(t, dc, c0), a1);
+                a[1] = fmaf(gain_of_rec(L, r.y), fmaf(t, dc, c0), a[1]);
                 pair_to_f(s_plane[r.z & 0xFFFFu], c0, dc);
-                a2 = fmaf(gain_of_rec(L, r.z), fmaf(t, dc, c0), a2);
+                a[2] = fmaf(gain_of_rec(L, r.z), fmaf(t, dc, c0), a[2]);
                 pair_to_f(s_plane[r.w & 0xFFFFu], c0, dc);
-                a3 = fmaf(gain_of_rec(L, r.w), fmaf(t, dc, c0), a3);
+                a[3] = fmaf(gain_of_rec(L, r.w), fmaf(t, dc, c0), a[3]);
             };
             const uint4* srec = reinterpret_cast<const uint4*>(s_rec + j);
             const int rstride = L.out / 4;
@@ -810,23 +822,21 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
             for (int rr = rec_rows; rr < nrows; ++rr)
                 edge4(__ldg(reinterpret_cast<const uint4*>(L.rec + static_cast<size_t>(s_rows[rr]) * L.out + j)),
                       s_trow[rr]);
-            *reinterpret_cast<float4*>(s_out + j) = make_float4(a0, a1, a2, a3);
+            stamp(h, 10);
+            const int NR = h.nr1;
+            float* part0 = h.part[0];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int jj = j + u;
+                // largest d with floor(in1 * d / P) <= jj
+                const int d = idiv_small((jj + 1) * P - 1, L1.in);
+                const int r0 = idiv_small(L1.in * d, P);
+                part0[(static_cast<size_t>(d) * P + c) * NR + (jj - r0)] = a[u];
+            }
         }
     }
     if (tid < nr) s_bias1[tid] = b1_reg;
     if (tid < L1.out) s_bfin[tid] = bf_reg;
-    __syncthreads();
-    // consumer-blocked partials: part0[d][c][jl] for layer-1 row r0(d) + jl
-    {
-        const int NR = h.nr1;
-        float* part0 = h.part[0];
-#pragma unroll 1
-        for (int e = tid; e < P * NR; e += kT) {
-            const int d = idiv_small(e, NR), jl = e - d * NR;
-            const int j = idiv_small(L1.in * d, P) + jl;
-            if (j < idiv_small(L1.in * (d + 1), P)) part0[(static_cast<size_t>(d) * P + c) * NR + jl] = s_out[j];
-        }
-    }
     stamp(h, 5);
     if (h.exit_at == 5) return;
     grid_sync();
@@ -843,6 +853,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
             reinterpret_cast<float4*>(s_red)[e] = __ldcg(reinterpret_cast<const float4*>(blk) + e);
         for (int e = 4 * n4 + tid; e < P * NR; e += kT) s_red[e] = __ldcg(blk + e);
         __syncthreads();
+        mbar_wait(&s_bar[1], 0);
         // warp w: row r10 + w.  Lanes sum z = lane, lane + 32, ... in order, a
         // fixed butterfly, lane 0's value; locate; lane j forms edge (w, j)
         if (warp < nr) {
@@ -960,7 +971,7 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
         h->nr1 = nr1;
         h->pref_mask = 2;
         h->cbrow_mask = 2;
-        const size_t out_b = (row + 127) / 128 * 128;
+        const size_t out_b = 0;
         const size_t pref_b = (static_cast<size_t>(nr1) * L[1].out * 4 + 127) / 128 * 128;
         const size_t cb_b = static_cast<size_t>(nr1) * L[1].out * 16;
         const size_t avail = kBudget > plane + out_b + pref_b + cb_b ? kBudget - plane - out_b - pref_b - cb_b : 0;
@@ -969,9 +980,9 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
         if (cap > static_cast<size_t>(kMaxRows)) cap = kMaxRows;
         h->rec_cap = static_cast<int>(cap);
         const size_t recs = (cap * row + 127) / 128 * 128;
-        h->out_offset = static_cast<uint32_t>(plane + recs);
-        h->pref_offset = static_cast<uint32_t>(plane + recs + out_b);
-        h->cbrow_offset = static_cast<uint32_t>(plane + recs + out_b + pref_b);
+        h->out_offset = 0;
+        h->pref_offset = static_cast<uint32_t>(plane + recs);
+        h->cbrow_offset = static_cast<uint32_t>(plane + recs + pref_b);
         h->part_floats = static_cast<unsigned>(std::max<size_t>(static_cast<size_t>(num_sms) * num_sms * nr1,
                                                                 static_cast<size_t>(num_sms) * L[1].out));
         return h->cbrow_offset + cb_b;
@@ -1018,12 +1029,26 @@ size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h) {
 }
 
 int head_b1_max_grid(size_t smem, int num_sms) {
-    for (auto k : {k_head_b1, k_head_b1v2})
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return 0;
+    // The attribute is per function and device, shared by every head: only
+    // ever raise it, so a head planned later with a smaller footprint cannot
+    // make an earlier head's launch exceed the limit.
+    static std::mutex mu;
+    static size_t set_max[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 0 || dev >= 64) return 0;
+        if (smem > set_max[dev]) {
+            for (auto k : {k_head_b1, k_head_b1v2})
+                if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+                    cudaSuccess) {
+                    cudaGetLastError();
+                    return 0;
+                }
+            set_max[dev] = smem;
         }
+    }
     int per_sm = 0, per_sm2 = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_head_b1, kT, smem) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, k_head_b1v2, kT, smem) != cudaSuccess) {
@@ -1031,6 +1056,23 @@ int head_b1_max_grid(size_t smem, int num_sms) {
         return 0;
     }
     return per_sm >= 1 && per_sm2 >= 1 ? num_sms : 0;
+}
+
+__global__ void k_b1_rows(const uint32_t* __restrict__ rec, const int8_t* __restrict__ cb8, int rs, uint4* dst,
+                          int n) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x)
+        dst[e] = *reinterpret_cast<const uint4*>(cb8 + static_cast<size_t>(rec[e] & 0xFFFFu) * rs);
+}
+
+size_t head_b1_rows_bytes(const HeadB1Args& h) {
+    return h.version == 2 ? static_cast<size_t>(h.L[1].in) * h.L[1].out * 16 : 0;
+}
+
+cudaError_t head_b1_build_rows(const HeadB1Args& h, uint4* dst, cudaStream_t s) {
+    const int n = h.L[1].in * h.L[1].out;
+    k_b1_rows<<<std::max(1, std::min((n + 255) / 256, 148 * 8)), 256, 0, s>>>(h.L[1].rec, h.L[1].cb8, h.L[1].rs, dst,
+                                                                              n);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s) {

@@ -191,6 +191,8 @@ struct HeadB1Args {
     int nr1;               // v2: layer-1 rows per consumer block (stride of the consumer-blocked partials)
     unsigned out_offset;   // v2: byte offset of layer 0's per-CTA output staging in dynamic shared memory
     unsigned part_floats;  // floats per partial buffer (part[0], part[1]) the kernel needs
+    const uint4* l1rows;   // v2: layer 1's edges' codebook rows, edge-major [in1*out1] x 16 B (built at
+                           // upload from layer 1's records: head_b1_build_rows)
     double node0[33];      // layer 0's node positions (kan.cpp:21-26), G <= 33
 };
 bool head_b1_supported(const DevLayer* L, int nl);
@@ -198,6 +200,9 @@ bool head_b1_supported(const DevLayer* L, int nl);
 // pref_mask, pref_offset.
 size_t head_b1_smem(const DevLayer* L, int nl, int num_sms, HeadB1Args* h);
 cudaError_t launch_head_b1(const HeadB1Args& h, int grid, size_t smem, cudaStream_t s);
+// v2: fill dst[e] = layer 1's codebook row of edge e (16 B) for all in1*out1 edges
+size_t head_b1_rows_bytes(const HeadB1Args& h);
+cudaError_t head_b1_build_rows(const HeadB1Args& h, uint4* dst, cudaStream_t s);
 // Grid for which all CTAs are co-resident (one per SM), or 0 if the kernel
 // cannot be resident at this shared-memory size.
 int head_b1_max_grid(size_t smem, int num_sms);

@@ -182,12 +182,17 @@ def test_fast_mode_bitwise_reproducible(torch_cuda):
 def test_fast_mode_batch1_pair_planes(torch_cuda):
     """Batch 1 routes big int8 layers through the shared-memory pair-plane
     kernel (k_fwd_planes) and the next layer's consumer-side reduction:
-    within tolerance, bitwise reproducible, several heads and seeds."""
-    for dims, k, G, seed in [((512, 512, 8), 4096, 10, 1), ((1024, 700, 12), 8192, 6, 2),
-                             ((2048, 1408, 20), 65536, 10, 3), ((640, 1536, 24, 3), 1000, 16, 4)]:
+    within tolerance, bitwise reproducible, several heads and seeds.  All
+    heads are created before any of them runs: a head planned later with a
+    smaller shared-memory footprint must not break an earlier head's launch."""
+    heads = []
+    for dims, k, G, seed in [((2048, 1408, 20), 65536, 10, 3), ((512, 512, 8), 4096, 10, 1),
+                             ((1024, 700, 12), 8192, 6, 2), ((640, 1536, 24, 3), 1000, 16, 4),
+                             ((2048, 128, 20), 4096, 10, 7)]:
         cn = synthetic.synthetic_head(dims=dims, k=k, grid=G, int8=True, seed=seed)
         tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
-        model = hq.build_model(cn)
+        heads.append((dims, G, seed, tables, hq.build_model(cn)))
+    for dims, G, seed, tables, model in heads:
         for xs in (1, 2):
             x = synthetic.synthetic_inputs(1, dims[0], seed=10 * seed + xs, grid=G)
             want, _ = oracle.port_forward(tables, x, 1)

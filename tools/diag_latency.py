@@ -73,7 +73,7 @@ def main():
             s.synchronize()
             ws.check()
             t = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
-            print(f"B={B:4d} flush={fl!s:5} launches={ws.last_launches()} median {statistics.median(t):8.2f} us "
+            print(f"B={B:4d} flush={fl!s:5} launches={ws.last_launches()} mean {statistics.mean(t):8.2f} median {statistics.median(t):8.2f} us "
                   f"p10 {t[len(t) // 10]:8.2f} p90 {t[9 * len(t) // 10]:8.2f}  -> {B / statistics.median(t) * 1e6:,.0f} samples/s",
                   flush=True)
 
