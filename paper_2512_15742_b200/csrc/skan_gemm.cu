@@ -673,6 +673,342 @@ __global__ void k_dense_tiles(const float* __restrict__ cb32, float* __restrict_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Dense layers at batch <= 64 (cfg4: the 1.13 GB grid streamed once per call):
+// a persistent kernel, one CTA per SM.  The (output tile, chunk) work of the
+// layer is flattened tile-major and cut into P equal contiguous ranges, so
+// every SM streams the same number of W tiles (no waves, no tail); a range
+// covers the end of one tile and the start of the next (a "segment" each),
+// whose accumulators are drained to their own partial planes.
+//   * TMA warp: each chunk's pre-tiled W (DevLayer::wt, 20 KB at G = 10) lands
+//     by ONE bulk copy in a ring slot: that slot is the N = 128 W_hi operand
+//     itself (no copy); kDnRing slots, refilled as the MMAs release them.
+//     (Ten 2 KB copies per chunk into interleaved [W_hi | W_lo] stages were
+//     measured issue-bound at ~160 cycles per copy.)  The chunk's brackets
+//     (input-major [in][B]: IC rows of B, contiguous) arrive the same way.
+//   * A warps (0-7), two sets of four taking alternate chunks: the stacked A
+//     tile (hat weights of 64 samples: A_hi in rows 0-63, A_lo in rows
+//     64-127) written into TMEM with tcgen05.st, so the MMAs read only W from
+//     shared memory (the "TS" form, ~N/2 cycles per K = 8 step).
+//   * lo warps (8-15), two sets of four taking alternate chunks: W_lo =
+//     W - tf32(W), read from L2 (the TMA just brought the tile there) rather
+//     than from the ring: shared memory bandwidth, not the tensor core, is
+//     what a chunk costs (TMA 20 KB + MMA 40 KB + W_lo 20 KB written).
+//   * MMA warp: per K = 8 step, A x W_hi and A x W_lo (M = 128, N = 128,
+//     kind::tf32, A in TMEM) into the same accumulator (the A_lo x W_lo
+//     product it also adds is ~2^-22 of the term); at a segment end it
+//     commits the accumulator to the A set that ran the segment's last
+//     chunk, which reads TMEM and writes planes 2 * segment + (A_lo rows).
+// One "full" and one "done" barrier per chunk slot (kDnQ): full = A set +
+// lo set + the W_hi bulk copy; done = the chunk's MMAs completed (frees its
+// ring slot, lo buffer and TMEM A buffer at once).  Every waiter is at most
+// one phase behind the barrier it waits on (a parity wait is exact only
+// within one phase): see the per-wait notes.
+// k_dense_reduce sums a tile's planes in ascending order in f64.
+constexpr int kDnRing = 7;
+constexpr int kDnLo = 3;
+constexpr int kDnA = 4;    // TMEM A buffers (columns kDnAcol + 64 * b)
+constexpr int kDnQ = 8;    // full / done barrier slots (> kDnRing: the TMA warp runs kDnRing chunks ahead)
+constexpr int kDnSeg = 8;  // accumulator-complete barriers (> segments an A set can run ahead: kDnA + 1)
+constexpr int kDnBr = 8;   // bracket slots (>= kDnRing + 1)
+constexpr int kDnT = kGmP + 64;       // A + lo warps, MMA warp, TMA warp
+constexpr uint32_t kDnAcol = kGmN;    // TMEM: accumulator columns [0, 128), A buffers from 128
+
+__host__ __device__ __forceinline__ long long dn_start(int c, long long T, int P) { return T * c / P; }
+// the CTA whose chunk range holds flattened chunk x
+__host__ __device__ __forceinline__ int dn_owner(long long x, long long T, int P) {
+    return static_cast<int>(((x + 1) * P - 1) / T);
+}
+
+// debug stamps (skan_debug_gemm_timeline): CTA 0 of a wide layer, 4 roles
+// x chunk u < 64 x phase < 8
+__device__ __forceinline__ void dstamp(const FwdArgs& a, int role, int u, int ph) {
+    if (a.dbg && u < 64 && blockIdx.x == 0 && a.L.out >= 1024) a.dbg[(role * 64 + u) * 8 + ph] = clock64();
+}
+
+// One chunk of the persistent dense kernel: for k < nb, A x W_hi then
+// A x W_lo (TS form, A in TMEM at a_tmem + 8k, B descriptors advancing by
+// `step` per K = 8), all from ONE elect and one asm block, so the
+// descriptors move to uniform registers once per chunk instead of once per
+// MMA (the per-MMA form spent ~15 instructions and three R2UR per MMA).
+// acc_first = 0 starts a new accumulation with the first MMA.
+__device__ __forceinline__ void mma_chunk_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t dh, uint64_t dl,
+                                             uint32_t idesc, uint32_t acc_first, int nb, uint64_t step) {
+    asm volatile(
+        "{\n\t.reg .pred pe, q0, pt, p1, p2, p3, p4, p5;\n\t.reg .b32 ta;\n\t.reg .b64 bh, bl;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "setp.ne.b32 q0, %5, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+        "setp.gt.s32 p1, %6, 1;\n\tand.pred p1, p1, pe;\n\t"
+        "setp.gt.s32 p2, %6, 2;\n\tand.pred p2, p2, pe;\n\t"
+        "setp.gt.s32 p3, %6, 3;\n\tand.pred p3, p3, pe;\n\t"
+        "setp.gt.s32 p4, %6, 4;\n\tand.pred p4, p4, pe;\n\t"
+        "setp.gt.s32 p5, %6, 5;\n\tand.pred p5, p5, pe;\n\t"
+        "mov.b32 ta, %1;\n\tmov.b64 bh, %2;\n\tmov.b64 bl, %3;\n\t"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, q0;\n\t"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+        "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+        "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+        "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+        "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+        "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+        "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+        "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+        "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+        "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+        "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+        "}\n"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(dh), "l"(dl), "r"(idesc), "r"(acc_first), "r"(nb), "l"(step)
+        : "memory");
+}
+
+template <int IC>
+__global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_full[kDnQ];       // chunk u % kDnQ: A, W_lo written, W_hi landed
+    __shared__ __align__(8) uint64_t s_done[kDnQ];       // chunk u % kDnQ: its MMAs completed
+    __shared__ __align__(8) uint64_t s_accfull[kDnSeg];  // segment s % kDnSeg's accumulator complete
+    __shared__ __align__(8) uint64_t s_accfree;          // ... and drained
+    __shared__ __align__(8) uint64_t s_bfull[kDnBr];     // the chunk's brackets landed
+    __shared__ uint32_t s_tmem;
+    constexpr uint32_t kLbo = (kGmN / 8) * 128;  // one K group of a 128-row operand (2 KB)
+    const DevLayer& L = a.L;
+    const int KC = IC * L.G, nblk = KC / 8;
+    const int P = gridDim.x, c = blockIdx.x;
+    const int ntile = (L.out + kGmN - 1) / kGmN;
+    const long long T = static_cast<long long>(ntile) * nch;
+    const long long x0 = dn_start(c, T, P), x1 = dn_start(c + 1, T, P);
+    const int n = static_cast<int>(x1 - x0);
+    const uint32_t tile_t = kGmN * KC * 4;
+    unsigned char* s_ring = smem;
+    unsigned char* s_lo = smem + kDnRing * tile_t;
+    // bracket slots: [IC][B] ints, then [IC][B] floats, of one chunk
+    const uint32_t br_bytes = static_cast<uint32_t>(IC) * a.B * 4;
+    unsigned char* s_br = s_lo + kDnLo * tile_t;
+    // chunk x of the flattened schedule is tile x / nch, chunk x % nch; the
+    // tiles of one output block are consecutive in wt (wt_nch == nch)
+    auto tile_src = [&](int u) { return reinterpret_cast<const char*>(L.wt) + static_cast<size_t>(x0 + u) * tile_t; };
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    pdl_trigger();
+    if (tid == 0) {
+        for (int q = 0; q < kDnQ; ++q) {
+            mbar_init(&s_full[q], kGmP / 2 + 1);
+            mbar_init(&s_done[q], 1);
+        }
+        for (int q = 0; q < kDnSeg; ++q) mbar_init(&s_accfull[q], 1);
+        mbar_init(&s_accfree, kGmP / 4);
+        for (int q = 0; q < kDnBr; ++q) mbar_init(&s_bfull[q], 1);
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    // the chunk slot of u, and the parity of u's phase on it
+    auto qwait = [&](uint64_t* bar, int u) { mbar_wait_parity(&bar[u % kDnQ], (u / kDnQ) & 1); };
+    if (warp == kGmP / 32 + 1) {
+        // TMA warp
+        if (lane == 0) {
+            // W tiles do not depend on the previous kernel: the first ring's worth now
+            for (int u = 0; u < kDnRing && u < n; ++u) {
+                mbar_expect_tx(&s_full[u % kDnQ], tile_t);
+                bulk_g2s(s_ring + u * tile_t, tile_src(u), tile_t, &s_full[u % kDnQ]);
+            }
+            pdl_wait();  // brackets come from the previous kernel
+            int ch = static_cast<int>(x0 % nch);
+#pragma unroll 1
+            for (int u = 0; u < n; ++u, ch = ch + 1 == nch ? 0 : ch + 1) {
+                if (u >= kDnRing) {
+                    // ring slot u % kDnRing held chunk u - kDnRing.  Phase note: this
+                    // warp waited for done(u - kDnRing - 1) last iteration
+                    qwait(s_done, u - kDnRing);
+                    dstamp(a, 2, u, 0);
+                    mbar_expect_tx(&s_full[u % kDnQ], tile_t);
+                    bulk_g2s(s_ring + (u % kDnRing) * tile_t, tile_src(u), tile_t, &s_full[u % kDnQ]);
+                }
+                // bracket slot u % kDnBr held chunk u - kDnBr, read before
+                // done(u - kDnRing) (waited above; slots below kDnRing are fresh)
+                const int bs = u % kDnBr;
+                const int nin = min(IC, L.in - ch * IC);
+                const uint32_t bytes = static_cast<uint32_t>(nin) * a.B * 4;
+                mbar_expect_tx(&s_bfull[bs], 2 * bytes);
+                bulk_g2s(s_br + bs * 2 * br_bytes, a.bm_in + static_cast<size_t>(ch) * IC * a.B, bytes, &s_bfull[bs]);
+                bulk_g2s(s_br + bs * 2 * br_bytes + br_bytes, a.bt_in + static_cast<size_t>(ch) * IC * a.B, bytes,
+                         &s_bfull[bs]);
+                dstamp(a, 2, u, 1);
+            }
+        }
+    } else if (warp == kGmP / 32) {
+        // MMA warp
+        const uint64_t dr0 = tc::make_desc(tc::smem_addr(s_ring), kLbo, 128);
+        const uint64_t dl0 = tc::make_desc(tc::smem_addr(s_lo), kLbo, 128);
+        constexpr uint64_t kStep = (2 * kLbo) >> 4;
+        const uint32_t idesc = tc::idesc_tf32(kGmM, kGmN);
+        int seg = 0;
+        int ch = static_cast<int>(x0 % nch);
+#pragma unroll 1
+        for (int u = 0; u < n; ++u, ch = ch + 1 == nch ? 0 : ch + 1) {
+            const bool first = u == 0 || ch == 0;
+            const bool last = u == n - 1 || ch + 1 == nch;
+            if (first && u > 0) mbar_wait_parity(&s_accfree, (seg - 1) & 1);  // previous segment drained
+            qwait(s_full, u);
+            tc::fence_after_sync();
+            if (lane == 0) dstamp(a, 1, u, 0);
+            const uint32_t ta = tmem + kDnAcol + (u % kDnA) * 64;
+            const uint64_t dh = dr0 + (u % kDnRing) * (tile_t >> 4), dl = dl0 + (u % kDnLo) * (tile_t >> 4);
+            mma_chunk_ts(tmem, ta, dh, dl, idesc, first ? 0u : 1u, nblk, kStep);
+            tc::mma_commit_warp(&s_done[u % kDnQ]);
+            if (last) {
+                tc::mma_commit_warp(&s_accfull[seg % kDnSeg]);
+                ++seg;
+            }
+            if (lane == 0) dstamp(a, 1, u, 1);
+        }
+    } else if (warp < kGmP / 64) {
+        // A warps.  Warp w owns TMEM lanes (w % 4) * 32.. (row r = its lane
+        // there: sample r & 63, A_lo for r >= 64) and writes every 8-column
+        // block of the chunk's K = IC * G columns (knot-major: column
+        // k = m * IC + input).  The set that ran a segment's last chunk drains
+        // the accumulator.
+        const int q4 = warp & 3, set = warp >> 2;
+        const int row = q4 * 32 + lane;
+        const int smp = row & 63;
+        const bool lo_row = row >= 64;
+        const int nS = min(64, a.B);
+        const bool aok = smp < nS;
+        int seg = 0;
+        int ch = static_cast<int>(x0 % nch), jt = static_cast<int>(x0 / nch);
+#pragma unroll 1
+        for (int u = 0; u < n; ++u) {
+            const bool last = u == n - 1 || ch + 1 == nch;
+            const int jt_u = jt;
+            const int ch_u = ch;
+            if (++ch == nch) {
+                ch = 0;
+                ++jt;
+            }
+            const bool mine = (a.gemm_skip & 1) ? set == 0 : (u & 1) == set;  // debug: bit 0 = one A set
+            if (!mine) {
+                seg += last;
+                continue;
+            }
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 0);
+            // brackets of (my sample, the chunk's inputs).  Phase note: this set
+            // read chunk u - 2's slot, so u - kDnBr's phase is complete
+            const int bs = u % kDnBr;
+            mbar_wait_parity(&s_bfull[bs], (u / kDnBr) & 1);
+            const int* sbm = reinterpret_cast<const int*>(s_br + bs * 2 * br_bytes);
+            const float* sbt = reinterpret_cast<const float*>(s_br + bs * 2 * br_bytes + br_bytes);
+            int m[IC];
+            float w0[IC], w1[IC];
+#pragma unroll
+            for (int il = 0; il < IC; ++il) {
+                const bool ok = aok && ch_u * IC + il < L.in;
+                m[il] = ok ? sbm[il * a.B + smp] : -8;
+                const float t = ok ? sbt[il * a.B + smp] : 0.f;
+                w0[il] = lo_row ? tc::tf32_lo(1.f - t) : 1.f - t;
+                w1[il] = lo_row ? tc::tf32_lo(t) : t;
+            }
+            // TMEM A buffer u % kDnA held chunk u - kDnA.  Phase note: at chunk
+            // u - 2 this set waited for done(u - 2 - kDnA)
+            if (u >= kDnA) qwait(s_done, u - kDnA);
+            tc::fence_after_sync();
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 1);
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kDnAcol + (u % kDnA) * 64;
+            // every column's value in registers (fully unrolled, KC <= 48: two
+            // compares and two selects each, knot and input compile-time), then
+            // as few wide tcgen05.st as the width allows
+            float v[48];
+#pragma unroll
+            for (int k = 0; k < 48; ++k) {
+                const int mk = k / IC, il = k % IC;
+                v[k] = mk == m[il] ? w0[il] : (mk == m[il] + 1 ? w1[il] : 0.f);
+            }
+            if (KC == 40 || KC == 48) {
+                tc::tmem_st32(ta, v);
+                if (KC == 40) tc::tmem_st8(ta + 32, *reinterpret_cast<const float(*)[8]>(v + 32));
+                else tc::tmem_st16(ta + 32, v + 32);
+            } else {
+#pragma unroll
+                for (int b = 0; b < 6; ++b) {
+                    if (b >= nblk) break;
+                    tc::tmem_st8(ta + 8 * b, *reinterpret_cast<const float(*)[8]>(v + 8 * b));
+                }
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 2);
+            if (!last) continue;
+            // segment end: drain the accumulator into planes 2*seg' + (A_lo rows),
+            // seg' = this CTA's index among the tile's CTAs
+            mbar_wait_parity(&s_accfull[seg % kDnSeg], (seg / kDnSeg) & 1);
+            tc::fence_after_sync();
+            const int segi = c - dn_owner(static_cast<long long>(jt_u) * nch, T, P);
+            const int as = (q4 & 1) * 32 + lane;
+            const int j0 = jt_u * kGmN, nJ = min(kGmN, L.out - j0);
+            const size_t plane = static_cast<size_t>(a.B) * L.out;
+            float* dst = a.partial + (2 * segi + (q4 >> 1)) * plane + static_cast<size_t>(min(as, nS - 1)) * L.out + j0;
+#pragma unroll 1
+            for (int c8 = 0; c8 < kGmN; c8 += 8) {
+                float v[8];
+                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+                if (as < nS) {
+                    if (c8 + 8 <= nJ && (L.out & 3) == 0) {
+                        *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
+                        *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (c8 + e < nJ) dst[c8 + e] = v[e];
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_accfree)) : "memory");
+            ++seg;
+        }
+    } else {
+        // lo warps: W_lo of chunk u from the tile in L2 into lo buffer u % kDnLo
+        const int set = (warp - kGmP / 64) >> 2;
+        const int lt = tid - kGmP / 2 - set * (kGmP / 4);
+        const int lstep = (a.gemm_skip & 2) ? 1 : 2;  // debug: bit 1 = one lo set
+        constexpr int kPer = 16;                      // float4 per thread and chunk, at most (KC <= 64)
+        const int nq = static_cast<int>(tile_t / 16);
+#pragma unroll 1
+        for (int u = lstep == 1 ? (set == 0 ? 0 : n) : set; u < n; u += lstep) {
+            const float4* hi = reinterpret_cast<const float4*>(tile_src(u));
+            float4 v[kPer];
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int q = lt + r * (kGmP / 4);
+                if (q < nq) v[r] = __ldg(hi + q);
+            }
+            // lo buffer u % kDnLo held chunk u - kDnLo.  Phase note: at chunk
+            // u - lstep this set waited for done(u - lstep - kDnLo)
+            if (u >= kDnLo) qwait(s_done, u - kDnLo);
+            if (lt == 0 && set == 0) dstamp(a, 2, u, 3);
+            float4* lo = reinterpret_cast<float4*>(s_lo + (u % kDnLo) * tile_t);
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int q = lt + r * (kGmP / 4);
+                if (q < nq)
+                    lo[q] = make_float4(tc::tf32_lo(v[r].x), tc::tf32_lo(v[r].y), tc::tf32_lo(v[r].z), tc::tf32_lo(v[r].w));
+            }
+            tc::fence_proxy_async();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
+            if (lt == 0 && set == 0) dstamp(a, 2, u, 4);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
 __device__ __forceinline__ void reduce_finish(const FwdArgs& a, size_t p, double v, int add_bias) {
     const DevLayer& L = a.L;
     const int j = static_cast<int>(p % L.out);
@@ -725,6 +1061,47 @@ __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) reduce_finish(a, p, v, add_bias);
+    }
+}
+
+// Persistent dense layer: output j of tile jt has 2 * (CTAs holding part of
+// the tile) planes, summed in ascending order in f64.
+__global__ void k_dense_reduce(FwdArgs a, int nch, int P) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t plane = static_cast<size_t>(a.B) * a.L.out;
+    const int ntile = (a.L.out + kGmN - 1) / kGmN;
+    const long long T = static_cast<long long>(ntile) * nch;
+    for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int jt = static_cast<int>(p % a.L.out) / kGmN;
+        const int nz = 2 * (dn_owner(static_cast<long long>(jt + 1) * nch - 1, T, P) -
+                            dn_owner(static_cast<long long>(jt) * nch, T, P) + 1);
+        double v = 0.0;
+        for (int z = 0; z < nz; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+        reduce_finish(a, p, v, 0);
+    }
+}
+
+// ... one warp per output when a tile spans many CTAs (narrow layers): lane
+// l sums planes l, l + 32, ... in order, then a fixed butterfly
+__global__ void k_dense_reduce_warp(FwdArgs a, int nch, int P) {
+    pdl_trigger();
+    pdl_wait();
+    const size_t plane = static_cast<size_t>(a.B) * a.L.out;
+    const int ntile = (a.L.out + kGmN - 1) / kGmN;
+    const long long T = static_cast<long long>(ntile) * nch;
+    const int lane = threadIdx.x & 31;
+    for (size_t p = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / 32; p < plane;
+         p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
+        const int jt = static_cast<int>(p % a.L.out) / kGmN;
+        const int nz = 2 * (dn_owner(static_cast<long long>(jt + 1) * nch - 1, T, P) -
+                            dn_owner(static_cast<long long>(jt) * nch, T, P) + 1);
+        double v = 0.0;
+        for (int z = lane; z < nz; z += 32) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0) reduce_finish(a, p, v, 0);
     }
 }
 
@@ -791,8 +1168,44 @@ bool gemm_supported(const DevLayer& L) {
     return L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE || L.fmt == FMT_F32;
 }
 
+// Persistent dense schedule (k_dense_persist): batch <= 64, chunk tiles of
+// at most 24 KB (KC <= 48) and kDnRing + kDnLo of them in shared memory.
+size_t dense_persist_smem(int G) {
+    const int kc = gemm_ic(G) * G;
+    return (kDnRing + kDnLo) * static_cast<size_t>(kGmN) * kc * 4 + kDnBr * 2 * static_cast<size_t>(gemm_ic(G)) * 64 * 4;
+}
+bool dense_persist_ok(const DevLayer& L, int B) {
+    static const bool off = [] {
+        const char* e = std::getenv("SKAN_DENSE_PERSIST");  // A/B experiment: 0 = the split GEMM
+        return e && e[0] == '0';
+    }();
+    return !off && L.fmt == FMT_DENSE && L.wt && B <= 64 && gemm_ic(L.G) * L.G <= 48 &&
+           dense_persist_smem(L.G) <= kGemmSmemLimit;
+}
+
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     LaunchCfg c{};
+    if (dense_persist_ok(L, B)) {
+        const int sms = num_sms > 0 ? num_sms : 148;
+        c.kind = 4;
+        c.persist = 1;
+        c.ic = gemm_ic(L.G);
+        c.spt = 64;
+        c.tj = kGmN;
+        c.dn_nch = (L.in + c.ic - 1) / c.ic;
+        const int ntile = (L.out + kGmN - 1) / kGmN;
+        const long long T = static_cast<long long>(ntile) * c.dn_nch;
+        c.jt = sms;  // grid
+        c.st = 1;
+        int maxseg = 1;
+        for (int jt = 0; jt < ntile; ++jt)
+            maxseg = std::max(maxseg, dn_owner(static_cast<long long>(jt + 1) * c.dn_nch - 1, T, sms) -
+                                          dn_owner(static_cast<long long>(jt) * c.dn_nch, T, sms) + 1);
+        c.nsplit = 2 * maxseg;
+        c.ichunk = L.in;
+        c.smem = dense_persist_smem(L.G);
+        return c;
+    }
     c.kind = 4;
     c.ic = gemm_ic(L.G);
     c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: 64 = A_hi / A_lo stacked in the 128 rows
@@ -840,6 +1253,9 @@ void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
 }
 
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B) {
+    if (c.persist)  // one M=128 x N=256 x K=8 MMA per K step of every (tile, chunk)
+        return static_cast<double>((L.out + kGmN - 1) / kGmN) * c.dn_nch * (c.ic * L.G / 8) * 2.0 * kGmM * 8 *
+               (2 * kGmN);
     // per CTA and K = 8 step: one M=128 x N=256 MMA, plus (not stacked) one N=128
     const double ksteps = static_cast<double>((L.in + c.ic - 1) / c.ic) * c.ic * L.G / 8.0;
     const double per_step = 2.0 * kGmM * 8 * (2 * kGmN + (c.spt == 64 ? 0 : kGmN));
@@ -860,6 +1276,26 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         return e ? std::atoi(e) : 0;
     }();
     a.gemm_skip = skip_env;
+    if (c.persist) {
+        static const int dist_env = [] {
+            const char* e = std::getenv("SKAN_DENSE_PREFETCH");  // experiment: L2 prefetch distance in chunks
+            return e ? std::atoi(e) : 0;
+        }();
+        a.gemm_ring = dist_env;
+        void (*kp)(FwdArgs, int) = c.ic == 4 ? k_dense_persist<4> : k_dense_persist<8>;
+        ensure_smem(kp, c.smem);
+        launch_pdl(kp, dim3(c.jt), dim3(kDnT), c.smem, pdl, s, a, c.dn_nch);
+        if (!with_reduce) return;
+        const long long n = static_cast<long long>(a.B) * a.L.out;
+        if (c.nsplit >= 32) {
+            const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
+            launch_pdl(k_dense_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.dn_nch, c.jt);
+        } else {
+            const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+            launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.dn_nch, c.jt);
+        }
+        return;
+    }
     const bool stack = c.spt == 64;
     void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic) : gemm_kernel<false>(a.L.fmt, c.ic);
     ensure_smem(k, c.smem);

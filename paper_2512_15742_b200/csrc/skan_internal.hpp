@@ -132,6 +132,8 @@ struct LaunchCfg {
     int rw;      // rows per warp (small kernel); GEMM: dense TMA ring slots
     int ic;      // inputs per staged chunk (large kernel)
     size_t smem; // dynamic shared memory bytes (large kernel)
+    int persist; // GEMM: dense layer on the persistent schedule (k_dense_persist, batch <= 64)
+    int dn_nch;  // persistent dense: chunks per output tile
 };
 
 // Arguments of one fused fast-path layer launch (k_fwd_small / k_fwd_large).

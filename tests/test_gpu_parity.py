@@ -618,3 +618,23 @@ def test_swap_from_bytes_refills_in_place(torch_cuda):
     other = oracle.ref_build(synthetic.synthetic_head(dims=(512, 500, 8), k=4096, grid=10, int8=True, seed=3))
     with pytest.raises(hq.ContractError):
         hq.swap_model_bytes(model, other.serialize())
+
+
+@pytest.mark.parametrize("dims,batch", [((256, 1024), 64), ((256, 1024, 20), 64), ((300, 700, 20), 17),
+                                        ((1024, 4096), 32), ((2048, 1408), 64)])
+def test_dense_persistent_schedule_against_oracle(torch_cuda, dims, batch):
+    """Dense layers at batch <= 64 run the persistent tensor-core kernel
+    (k_dense_persist): every SM streams an equal share of the flattened
+    (output tile, chunk) schedule, so a CTA's range covers pieces of several
+    tiles ("segments") and a tile several CTAs.  Short ranges (hundreds of
+    segments, 1-4 chunks each) and narrow last layers exercise the segment
+    drains and the reduction's plane counts.  Fast mode within the bound."""
+    rls = synthetic.dense_runtime_head(dims=dims)
+    tables = [oracle.Tables.from_runtime(rl) for rl in rls]
+    model = hq.upload(rls, device=0)
+    x = synthetic.synthetic_inputs(batch, dims[0], seed=6)
+    want, scale = oracle.port_forward_l1(tables, x, batch, threads=16)
+    ws = hq.make_workspace(model, max_batch=batch)
+    got = np.zeros(batch * dims[-1])
+    hq.compressed_forward(model, x, batch, got, ws, mode="fast")
+    assert_close(got, want, scale)
