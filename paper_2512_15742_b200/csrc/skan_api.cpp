@@ -1121,8 +1121,9 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         if (h->b1_ok) {
             const size_t n = h->b1_plan.part_floats;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
-            ws->b1_done = static_cast<unsigned*>(alloc(sizeof(unsigned)));
-            skan::cuda_check(cudaMemset(ws->b1_done, 0, sizeof(unsigned)), "cudaMemset");
+            // [0] last-layer arrivals, [1] the v2 kernel's grid barrier (both monotonic)
+            ws->b1_done = static_cast<unsigned*>(alloc(2 * sizeof(unsigned)));
+            skan::cuda_check(cudaMemset(ws->b1_done, 0, 2 * sizeof(unsigned)), "cudaMemset");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));

@@ -63,6 +63,30 @@ __device__ __forceinline__ void stamp_clock(const HeadB1Args& h, int slot) {
 
 __device__ __forceinline__ void grid_sync() { cooperative_groups::this_grid().sync(); }
 
+// Grid barrier on a monotonic counter (the launch is cooperative, so all
+// CTAs are co-resident): one release add and an acquire poll by thread 0,
+// block barriers either side.  `target` = the counter's value at launch + P.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        } while (static_cast<int>(v - target) < 0);
+    }
+    __syncthreads();
+}
+
+// Last-arriver test on a monotonic counter: acq_rel add (the CTA's writes,
+// ordered before by the block barrier, are released; the last arriver
+// acquires everyone else's).
+__device__ __forceinline__ unsigned arrive_acq_rel(unsigned* ctr) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+}
+
 // float(gain(code) * codebook_scale) for the fast path (see DevLayer::g_base);
 // the record's gain code is byte 2
 __device__ __forceinline__ float gain_of_rec(const DevLayer& L, uint32_t r) {
@@ -703,6 +727,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
         for (int u = 0; u < kPer2; ++u)
             if (u == q) mb[u] = mm;
     }
+    stamp(h, 11);
     const uint32_t w0 = static_cast<uint32_t>(mb[0]) | mb[1] << 8 | mb[2] << 16 | static_cast<uint32_t>(mb[3]) << 24;
     const uint32_t w1 = static_cast<uint32_t>(mb[4]) | mb[5] << 8 | mb[6] << 16 | static_cast<uint32_t>(mb[7]) << 24;
 #pragma unroll 1
@@ -839,7 +864,7 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
     if (tid < L1.out) s_bfin[tid] = bf_reg;
     stamp(h, 5);
     if (h.exit_at == 5) return;
-    grid_sync();
+    grid_barrier(h.done + 1, h.epoch + static_cast<unsigned>(P));
     stamp(h, 6);
     // layer 1: my consumer block (P x NR, contiguous) -> shared memory
     {
@@ -886,14 +911,9 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
     if (h.exit_at == 7) return;
     // the last CTA to arrive reduces the [P][out] block (contiguous)
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        const unsigned old = atomicAdd(h.done, 1u);
-        s_last = old - h.epoch == static_cast<unsigned>(P - 1);
-    }
+    if (tid == 0) s_last = arrive_acq_rel(h.done) - h.epoch == static_cast<unsigned>(P - 1);
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     stamp(h, 12);
     {
         const float* part = h.part[1];

@@ -20,7 +20,7 @@ from paper_2512_15742_b200 import _lib, synthetic  # noqa: E402
 PHASES_V1 = {0: "start", 1: "tables", 2: "x ready", 3: "locate+hist", 4: "rowlist+tma", 5: "plane ready",
              6: "L0 partial", 7: "grid sync 1", 9: "L1 reduce+locate", 10: "L1 rows", 11: "grid sync 2",
              12: "final start", 13: "end"}
-PHASES_V2 = {0: "x issued", 1: "tables issued", 2: "brackets+counts", 8: "alloc (plane TMA)",
+PHASES_V2 = {0: "x issued", 1: "tables issued", 11: "brackets", 2: "brackets+counts", 8: "alloc (plane TMA)",
              9: "rows ranked+TMA", 4: "plane+rec ready", 10: "L0 FMA done", 5: "L0 partials out",
              6: "grid sync", 7: "L1 done", 12: "final start", 13: "end"}
 PHASES = PHASES_V1 if os.environ.get("SKAN_B1_V1") == "1" else PHASES_V2
