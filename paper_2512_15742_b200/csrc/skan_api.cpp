@@ -118,10 +118,10 @@ uint64_t device_bytes(const skan_layer_header& h) {
     const int fmt = device_format(h);
     // node positions + their integer keys (fast knot selection), every format
     uint64_t b = 2 * align_up(mul_checked(h.grid_size, 8));
-    if (fmt == skan::FMT_DENSE) {
-        b = add_checked(b, align_up(mul_checked(mul_checked(e, h.grid_size), 4)));
-        if (dense_tiled(h)) b = add_checked(b, align_up(mul_checked(skan::dense_tile_floats(h.in_dim, h.out_dim, h.grid_size), 4)));
-        return b;
+    if (fmt == skan::FMT_DENSE) {  // one copy of the grid: the GEMM's tiled layout, or the natural one
+        if (dense_tiled(h))
+            return add_checked(b, align_up(mul_checked(skan::dense_tile_floats(h.in_dim, h.out_dim, h.grid_size), 4)));
+        return add_checked(b, align_up(mul_checked(mul_checked(e, h.grid_size), 4)));
     }
     const uint64_t kg = mul_checked(h.k, h.grid_size);
     // int8 codebook: rows padded to 16 B (one 128-bit load per row) plus the
@@ -544,10 +544,11 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
         auto region = [&](const void* src, uint64_t bytes) { return s.dev ? reserve(bytes) : put(src, bytes); };
         switch (d.fmt) {
             case skan::FMT_DENSE:
-                d.cb32 = static_cast<const float*>(region(s.cb32.data(), E * d.G * 4));
-                if (dense_tiled(s.h)) {
+                if (dense_tiled(s.h)) {  // built on the device from the natural grid (below)
                     d.wt = static_cast<const float*>(reserve(skan::dense_tile_floats(d.in, d.out, d.G) * 4));
                     d.wt_nch = (d.in + skan::gemm_ic(d.G) - 1) / skan::gemm_ic(d.G);
+                } else {
+                    d.cb32 = static_cast<const float*>(region(s.cb32.data(), E * d.G * 4));
                 }
                 break;
             case skan::FMT_I8_R32:
@@ -615,8 +616,28 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
     }
     for (size_t l = 0; l < st.size(); ++l)
         if (st[l].dev) skan::build_layer_from_sections(new_dl[l], st[l].src, st[l].bits, cs);
-    for (const DevLayer& d : new_dl)
-        if (d.wt) skan::build_dense_tiles(d, const_cast<float*>(d.wt), cs);
+    // host-staged tiled dense layers: the natural grid goes up in slices of
+    // whole input chunks through a bounded staging buffer and is tiled there
+    for (size_t l = 0; l < st.size(); ++l) {
+        const DevLayer& d = new_dl[l];
+        if (!d.wt || st[l].dev) continue;
+        const int ic = skan::gemm_ic(d.G);
+        const uint64_t chunk_bytes = static_cast<uint64_t>(ic) * d.out * d.G * 4;
+        const int per = static_cast<int>(std::max<uint64_t>(1, (64ull << 20) / chunk_bytes));
+        void* tmp = nullptr;
+        skan::cuda_check(cudaMalloc(&tmp, std::min<uint64_t>(static_cast<uint64_t>(per), d.wt_nch) * chunk_bytes),
+                         "cudaMalloc (dense staging)");
+        for (int ch0 = 0; ch0 < d.wt_nch; ch0 += per) {
+            const int ch1 = std::min(d.wt_nch, ch0 + per);
+            const uint64_t i0 = static_cast<uint64_t>(ch0) * ic, i1 = std::min<uint64_t>(d.in, static_cast<uint64_t>(ch1) * ic);
+            skan::cuda_check(cudaMemcpyAsync(tmp, st[l].cb32.data() + i0 * d.out * d.G, (i1 - i0) * d.out * d.G * 4,
+                                             cudaMemcpyHostToDevice, cs),
+                             "dense grid slice");
+            skan::build_dense_tiles(d, const_cast<float*>(d.wt), static_cast<const float*>(tmp), ch0, ch1, cs);
+            skan::cuda_check(cudaStreamSynchronize(cs), "dense tiles");  // the slice buffer is reused
+        }
+        cudaFree(tmp);
+    }
     skan::cuda_check(cudaGetLastError(), "dense tiles");
     skan::cuda_check(cudaStreamSynchronize(cs), swap ? "swap head" : "upload head");  // host image is freed on return
     h->dl = std::move(new_dl);

@@ -171,6 +171,21 @@ __device__ __forceinline__ void fast_locate(const DevLayer& L, double x, int* er
     }
 }
 
+// Element (i, j, m) of a dense layer's grid.  Layers the tensor-core GEMM
+// takes keep ONLY the GEMM's pre-tiled layout (DevLayer::wt: 128-output x
+// IC-input tiles, K-major within a tile, k = m * IC + input, IC = 4 for even
+// G, 8 for odd); the others keep the natural [in][out][G] layout (cb32).
+__device__ __forceinline__ float dense_at(const DevLayer& L, int i, int j, int m) {
+    if (L.wt) {
+        const int IC = (L.G & 1) ? 8 : 4;
+        const int ch = i / IC, il = i - ch * IC, jt = j >> 7, r = j & 127, k = m * IC + il;
+        const size_t off = (static_cast<size_t>(jt) * L.wt_nch + ch) * (128 * IC * L.G) +
+                           static_cast<size_t>((k >> 2) * 512 + (r >> 3) * 32 + (r & 7) * 4 + (k & 3));
+        return __ldg(L.wt + off);
+    }
+    return __ldg(L.cb32 + (static_cast<size_t>(i) * L.out + j) * L.G + m);
+}
+
 // int8 codebook pair p = c0 | c1 << 8  ->  (c0, c1 - c0) as floats without
 // the quarter-rate I2F pipe: 0x4B000000 | (u ^ 0x80) is the float
 // 2^23 + u^0x80, so subtracting 2^23 + 128 yields the signed value; the

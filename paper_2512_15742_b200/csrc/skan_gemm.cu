@@ -653,23 +653,27 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     if (warp == 0) tc::tmem_free<2 * kGmN>(tmem);
 }
 
-// Pre-tiled copy of a dense grid for the layer GEMM (built once at upload):
-// tile (jt, ch) = the chunk's KC x 128 W block in exactly the shared-memory
-// byte layout above, zero-padded past `out` and `in`, tiles of one output
-// block consecutive along the inputs (one TMA bulk copy per chunk).
-__global__ void k_dense_tiles(const float* __restrict__ cb32, float* __restrict__ wt, int in, int out, int G,
-                              int IC, int nch, size_t total) {
+// Pre-tiled dense grid for the layer GEMM (built at upload; the only
+// resident copy of such a layer): tile (jt, ch) = the chunk's KC x 128 W
+// block in exactly the shared-memory byte layout above, zero-padded past
+// `out` and `in`, tiles of one output block consecutive along the inputs (one
+// TMA bulk copy per chunk).  Builds the chunks [ch0, ch1) of every output
+// block from `src`, the natural [i][out][G] grid whose row 0 is input ch0 * IC.
+__global__ void k_dense_tiles(const float* __restrict__ src, float* __restrict__ wt, int in, int out, int G,
+                              int IC, int nch, int ch0, int ch1, size_t total) {
     const int KC = IC * G;
     const size_t per = static_cast<size_t>(kGmN) * KC;
+    const int nc = ch1 - ch0;
     for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < total;
          q += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const size_t tile = q / per;
         const int f = static_cast<int>(q % per);
-        const int jt = static_cast<int>(tile / nch), ch = static_cast<int>(tile % nch);
+        const int jt = static_cast<int>(tile / nc), ch = ch0 + static_cast<int>(tile % nc);
         // invert kmajor_off(r, k, 128) / 4 = (k/4)*512 + (r/8)*32 + (r%8)*4 + k%4
         const int k = (f >> 9) * 4 + (f & 3), r = ((f >> 5) & 15) * 8 + ((f >> 2) & 7);
         const int m = k / IC, i = ch * IC + k % IC, j = jt * kGmN + r;
-        wt[q] = (i < in && j < out) ? cb32[(static_cast<size_t>(i) * out + j) * G + m] : 0.f;
+        wt[(static_cast<size_t>(jt) * nch + ch) * per + f] =
+            (i < in && j < out) ? src[(static_cast<size_t>(i - ch0 * IC) * out + j) * G + m] : 0.f;
     }
 }
 
@@ -1318,19 +1322,21 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     }
 }
 
-// Dense layers keep a GEMM-tiled copy of their grid (DevLayer::wt) next to
-// the natural one: number of floats, and the device-side build.
+// Dense layers the GEMM takes keep their grid ONLY in its pre-tiled layout
+// (DevLayer::wt; every other kernel reads it through dense_at): number of
+// floats, and the device-side build of input chunks [ch0, ch1) from a natural
+// layout source (rows from input ch0 * IC).
 uint64_t dense_tile_floats(int in, int out, int G) {
     const int ic = gemm_ic(G);
     return static_cast<uint64_t>((out + kGmN - 1) / kGmN) * ((in + ic - 1) / ic) * kGmN * ic * G;
 }
 
-void build_dense_tiles(const DevLayer& L, float* wt, cudaStream_t s) {
+void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s) {
     const int ic = gemm_ic(L.G);
     const int nch = (L.in + ic - 1) / ic;
-    const uint64_t total = dense_tile_floats(L.in, L.out, L.G);
+    const uint64_t total = static_cast<uint64_t>((L.out + kGmN - 1) / kGmN) * (ch1 - ch0) * kGmN * ic * L.G;
     const int blocks = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
-    k_dense_tiles<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L.cb32, wt, L.in, L.out, L.G, ic, nch, total);
+    k_dense_tiles<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, wt, L.in, L.out, L.G, ic, nch, ch0, ch1, total);
 }
 
 }  // namespace skan

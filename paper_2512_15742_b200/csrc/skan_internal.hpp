@@ -247,7 +247,7 @@ bool gemm_supported(const DevLayer& L);
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms);
 int gemm_ic(int G);
 uint64_t dense_tile_floats(int in, int out, int G);
-void build_dense_tiles(const DevLayer& L, float* wt, cudaStream_t s);
+void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s);
 void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce = true);
 // MMA work one k_layer_gemm launch issues (flops, as 2*M*N*K per tcgen05.mma)
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B);

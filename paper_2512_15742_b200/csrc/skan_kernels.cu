@@ -363,9 +363,8 @@ __global__ void __launch_bounds__(256) k_fwd_small(FwdArgs a) {
                         c0 = __ldg(row);
                         c1 = __ldg(row + 1);
                     } else {
-                        const float* row = L.cb32 + (static_cast<size_t>(r0 + rl) * L.out + j0 + v) * G + m;
-                        c0 = __ldg(row);
-                        c1 = __ldg(row + 1);
+                        c0 = dense_at(L, r0 + rl, j0 + v, m);
+                        c1 = dense_at(L, r0 + rl, j0 + v, m + 1);
                     }
                     acc[s][v] = fmaf(g, fmaf(t, c1 - c0, c0), acc[s][v]);
                 }
@@ -800,9 +799,10 @@ struct Edge<FMT_F32> {
 
 template <>
 struct Edge<FMT_DENSE> {
-    const float* row;
+    int i, j;
     __device__ __forceinline__ void load(const DevLayer& L, size_t e) {
-        row = L.cb32 + e * static_cast<size_t>(L.G);
+        i = static_cast<int>(e / static_cast<size_t>(L.out));
+        j = static_cast<int>(e - static_cast<size_t>(i) * L.out);
     }
 };
 
@@ -870,6 +870,9 @@ __global__ void __launch_bounds__(kThreads)
                 if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
                     c0 = __dmul_rn(static_cast<double>(__ldg(ed.row + m)), L.cs);
                     c1 = __dmul_rn(static_cast<double>(__ldg(ed.row + m + 1)), L.cs);
+                } else if constexpr (FMT == FMT_DENSE) {
+                    c0 = static_cast<double>(dense_at(L, ed.i, ed.j, m));
+                    c1 = static_cast<double>(dense_at(L, ed.i, ed.j, m + 1));
                 } else {
                     c0 = static_cast<double>(__ldg(ed.row + m));
                     c1 = static_cast<double>(__ldg(ed.row + m + 1));

@@ -113,8 +113,13 @@ void check_index_section(const uint8_t* index, uint64_t index_bytes, int bits, u
 void build_layer_from_sections(const DevLayer& d, const LayerSrc& src, int bits, cudaStream_t s) {
     const uint64_t E = static_cast<uint64_t>(d.in) * d.out;
     if (d.fmt == FMT_DENSE) {
-        cuda_check(cudaMemcpyAsync(const_cast<float*>(d.cb32), src.codebook, E * d.G * sizeof(float),
-                                   cudaMemcpyDeviceToDevice, s), "dense coefficients");
+        if (d.wt) {  // the GEMM's tiled layout is the only resident copy: tiled straight from the section
+            build_dense_tiles(d, const_cast<float*>(d.wt), reinterpret_cast<const float*>(src.codebook), 0, d.wt_nch, s);
+            cuda_check(cudaGetLastError(), "dense tiles");
+        } else {
+            cuda_check(cudaMemcpyAsync(const_cast<float*>(d.cb32), src.codebook, E * d.G * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, s), "dense coefficients");
+        }
         return;
     }
     switch (d.fmt) {
