@@ -639,6 +639,8 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
         cudaFree(tmp);
     }
     skan::cuda_check(cudaGetLastError(), "dense tiles");
+    for (DevLayer& d : new_dl)  // the fp16 dense GEMM's per-layer scale
+        if (d.wt) d.wsc = skan::dense_fp16_scale(d.wt, skan::dense_tile_floats(d.in, d.out, d.G), cs);
     skan::cuda_check(cudaStreamSynchronize(cs), swap ? "swap head" : "upload head");  // host image is freed on return
     h->dl = std::move(new_dl);
     h->headers = std::move(new_headers);

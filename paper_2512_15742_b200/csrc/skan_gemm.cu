@@ -8,11 +8,14 @@
 // k_debug_gemm is the self-test of the building blocks in skan_tc.cuh: one
 // CTA, 128 x N (N <= 256) x K (K <= 64) from row-major f32 A [128][K] and
 // B [K][N] staged by plain threads into the canonical K-major layout.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <cmath>
 
 #include "skan_internal.hpp"
 #include "skan_tc.cuh"
@@ -730,44 +733,77 @@ __device__ __forceinline__ void dstamp(const FwdArgs& a, int role, int u, int ph
     if (a.dbg && u < 64 && blockIdx.x == 0 && a.L.out >= 1024) a.dbg[(role * 64 + u) * 8 + ph] = clock64();
 }
 
-// One chunk of the persistent dense kernel: for k < nb, A x W_hi then
+// One chunk of a persistent dense kernel: for k < nb, A x W_hi then
 // A x W_lo (TS form, A in TMEM at a_tmem + 8k, B descriptors advancing by
-// `step` per K = 8), all from ONE elect and one asm block, so the
-// descriptors move to uniform registers once per chunk instead of once per
-// MMA (the per-MMA form spent ~15 instructions and three R2UR per MMA).
-// acc_first = 0 starts a new accumulation with the first MMA.
+// `step` per K step: K = 8 for kind::tf32, 16 for kind::f16, both 8 TMEM
+// columns of A and two core-matrix columns of B), all from ONE elect and one
+// asm block.  acc_first = 0 starts a new accumulation with the first MMA.
+template <bool F16>
 __device__ __forceinline__ void mma_chunk_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t dh, uint64_t dl,
                                              uint32_t idesc, uint32_t acc_first, int nb, uint64_t step) {
-    asm volatile(
-        "{\n\t.reg .pred pe, q0, pt, p1, p2, p3, p4, p5;\n\t.reg .b32 ta;\n\t.reg .b64 bh, bl;\n\t"
-        "elect.sync _|pe, 0xffffffff;\n\t"
-        "setp.ne.b32 q0, %5, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
-        "setp.gt.s32 p1, %6, 1;\n\tand.pred p1, p1, pe;\n\t"
-        "setp.gt.s32 p2, %6, 2;\n\tand.pred p2, p2, pe;\n\t"
-        "setp.gt.s32 p3, %6, 3;\n\tand.pred p3, p3, pe;\n\t"
-        "setp.gt.s32 p4, %6, 4;\n\tand.pred p4, p4, pe;\n\t"
-        "setp.gt.s32 p5, %6, 5;\n\tand.pred p5, p5, pe;\n\t"
-        "mov.b32 ta, %1;\n\tmov.b64 bh, %2;\n\tmov.b64 bl, %3;\n\t"
-        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, q0;\n\t"
-        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
-        "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
-        "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
-        "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
-        "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
-        "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
-        "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
-        "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
-        "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
-        "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
-        "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
-        "}\n"
-        ::"r"(d_tmem), "r"(a_tmem), "l"(dh), "l"(dl), "r"(idesc), "r"(acc_first), "r"(nb), "l"(step)
-        : "memory");
+    if constexpr (F16) {
+        asm volatile(
+            "{\n\t.reg .pred pe, q0, pt, p1, p2, p3, p4, p5;\n\t.reg .b32 ta;\n\t.reg .b64 bh, bl;\n\t"
+            "elect.sync _|pe, 0xffffffff;\n\t"
+            "setp.ne.b32 q0, %5, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+            "setp.gt.s32 p1, %6, 1;\n\tand.pred p1, p1, pe;\n\t"
+            "setp.gt.s32 p2, %6, 2;\n\tand.pred p2, p2, pe;\n\t"
+            "setp.gt.s32 p3, %6, 3;\n\tand.pred p3, p3, pe;\n\t"
+            "setp.gt.s32 p4, %6, 4;\n\tand.pred p4, p4, pe;\n\t"
+            "setp.gt.s32 p5, %6, 5;\n\tand.pred p5, p5, pe;\n\t"
+            "mov.b32 ta, %1;\n\tmov.b64 bh, %2;\n\tmov.b64 bl, %3;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, q0;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p1 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, pt;\n\t"
+            "@p1 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p2 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, pt;\n\t"
+            "@p2 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p3 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, pt;\n\t"
+            "@p3 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p4 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, pt;\n\t"
+            "@p4 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p5 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bh, %4, pt;\n\t"
+            "@p5 tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], bl, %4, pt;\n\t"
+            "}\n"
+            ::"r"(d_tmem), "r"(a_tmem), "l"(dh), "l"(dl), "r"(idesc), "r"(acc_first), "r"(nb), "l"(step)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred pe, q0, pt, p1, p2, p3, p4, p5;\n\t.reg .b32 ta;\n\t.reg .b64 bh, bl;\n\t"
+            "elect.sync _|pe, 0xffffffff;\n\t"
+            "setp.ne.b32 q0, %5, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"
+            "setp.gt.s32 p1, %6, 1;\n\tand.pred p1, p1, pe;\n\t"
+            "setp.gt.s32 p2, %6, 2;\n\tand.pred p2, p2, pe;\n\t"
+            "setp.gt.s32 p3, %6, 3;\n\tand.pred p3, p3, pe;\n\t"
+            "setp.gt.s32 p4, %6, 4;\n\tand.pred p4, p4, pe;\n\t"
+            "setp.gt.s32 p5, %6, 5;\n\tand.pred p5, p5, pe;\n\t"
+            "mov.b32 ta, %1;\n\tmov.b64 bh, %2;\n\tmov.b64 bl, %3;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, q0;\n\t"
+            "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+            "@p1 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+            "@p2 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+            "@p3 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+            "@p4 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "add.u32 ta, ta, 8;\n\tadd.s64 bh, bh, %7;\n\tadd.s64 bl, bl, %7;\n\t"
+            "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bh, %4, pt;\n\t"
+            "@p5 tcgen05.mma.cta_group::1.kind::tf32 [%0], [ta], bl, %4, pt;\n\t"
+            "}\n"
+            ::"r"(d_tmem), "r"(a_tmem), "l"(dh), "l"(dl), "r"(idesc), "r"(acc_first), "r"(nb), "l"(step)
+            : "memory");
+    }
 }
 
 template <int IC>
@@ -864,7 +900,7 @@ __global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
             if (lane == 0) dstamp(a, 1, u, 0);
             const uint32_t ta = tmem + kDnAcol + (u % kDnA) * 64;
             const uint64_t dh = dr0 + (u % kDnRing) * (tile_t >> 4), dl = dl0 + (u % kDnLo) * (tile_t >> 4);
-            mma_chunk_ts(tmem, ta, dh, dl, idesc, first ? 0u : 1u, nblk, kStep);
+            mma_chunk_ts<false>(tmem, ta, dh, dl, idesc, first ? 0u : 1u, nblk, kStep);
             tc::mma_commit_warp(&s_done[u % kDnQ]);
             if (last) {
                 tc::mma_commit_warp(&s_accfull[seg % kDnSeg]);
@@ -1068,6 +1104,313 @@ __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// The same persistent dense schedule in fp16 split precision (kind::f16: K =
+// 16 per MMA at the tf32 instruction's cycles, so half the tensor time):
+//     W * S = W_hi + W_lo,  t = t_hi + t_lo   (fp16 each, round to nearest)
+// with S = 2^e the layer's scale (DevLayer::wsc) putting max|W| * S in
+// [2^14, 2^15): both halves keep 11 significant bits like tf32's, and values
+// the fp16 range cuts off are below 2^-40 of the layer's largest entry.  The
+// MMAs add A_hi W_hi + A_lo W_hi (stacked A rows) + A W_lo; the epilogue
+// multiplies by 1/S (exact).  A "pair chunk" is two consecutive IC = 4 tiles
+// of the resident layout (K = 80 at G = 10): the TMA lands both f32 tiles in a
+// ring slot, the conversion warps write the fp16 W_hi / W_lo operands (K order
+// = tile a's columns, then tile b's), and the A warps write the hat weights in
+// the same K order into TMEM as fp16 pairs.  The f32 tiles land by TMA in a
+// ring (reading them from L2 in the conversion warps instead was measured
+// latency-bound).
+constexpr int kD16Ring = 3;   // pair slots of the f32 ring (two IC = 4 tiles each)
+constexpr int kD16Stg = 2;    // fp16 [W_hi | W_lo] operand stages
+constexpr int kD16Br = 4;     // bracket slots (8 inputs x B each)
+constexpr int kD16Cv = 2;     // conversion warp sets (of four), taking pairs in turn
+constexpr int kD16T = kGmP / 2 + kD16Cv * 128 + 64;  // A sets + conversion sets + MMA warp + TMA warp
+constexpr int kD16Mma = kD16T / 32 - 2, kD16Tma = kD16T / 32 - 1;
+
+__host__ __device__ __forceinline__ int d16_nch2(int nch) { return (nch + 1) / 2; }
+
+template <int KC>
+__global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_tfull[kD16Ring];  // pair u % kD16Ring: f32 tiles landed
+    __shared__ __align__(8) uint64_t s_full[kDnQ];       // pair u % kDnQ: A and the fp16 W written
+    __shared__ __align__(8) uint64_t s_done[kDnQ];       // pair u % kDnQ: its MMAs completed
+    __shared__ __align__(8) uint64_t s_accfull[kDnSeg];
+    __shared__ __align__(8) uint64_t s_accfree;
+    __shared__ __align__(8) uint64_t s_bfull[kD16Br];
+    __shared__ uint32_t s_tmem;
+    constexpr int IC = 4;
+    constexpr uint32_t kLbo = (kGmN / 8) * 128;  // one core-matrix column of a 128-row operand (2 KB)
+    const DevLayer& L = a.L;
+    constexpr int KC2 = 2 * KC, nstep = KC2 / 16;  // KC = IC * G (G = KC / 4, even)
+    const int P = gridDim.x, c = blockIdx.x;
+    const int ntile = (L.out + kGmN - 1) / kGmN;
+    const int nch2 = d16_nch2(nch);
+    const long long T = static_cast<long long>(ntile) * nch2;
+    const long long x0 = dn_start(c, T, P), x1 = dn_start(c + 1, T, P);
+    const int n = static_cast<int>(x1 - x0);
+    const uint32_t tile_t = kGmN * KC * 4;         // one f32 IC = 4 tile
+    const uint32_t half_t = kGmN * KC2 * 2;        // one fp16 operand (W_hi or W_lo) of a pair
+    unsigned char* s_ring = smem;                                  // kD16Ring x 2 f32 tiles
+    unsigned char* s_stg = smem + kD16Ring * 2 * tile_t;           // kD16Stg x [W_hi | W_lo]
+    const uint32_t br_bytes = static_cast<uint32_t>(2 * IC) * a.B * 4;
+    unsigned char* s_br = s_stg + kD16Stg * 2 * half_t;            // kD16Br x [int m | float t] x 8 x B
+    const float wsc = L.wsc, wsc_inv = 1.0f / L.wsc;
+    // pair x = (tile jt = x / nch2, pair q = x % nch2): IC = 4 tiles 2q, 2q + 1 of block jt
+    auto tile_src = [&](int jt, int ch) {
+        return reinterpret_cast<const char*>(L.wt) + (static_cast<size_t>(jt) * nch + ch) * tile_t;
+    };
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    pdl_trigger();
+    if (tid == 0) {
+        for (int q = 0; q < kD16Ring; ++q) mbar_init(&s_tfull[q], 1);
+        for (int q = 0; q < kDnQ; ++q) {
+            mbar_init(&s_full[q], kGmP / 2);
+            mbar_init(&s_done[q], 1);
+        }
+        for (int q = 0; q < kDnSeg; ++q) mbar_init(&s_accfull[q], 1);
+        mbar_init(&s_accfree, kGmP / 4);
+        for (int q = 0; q < kD16Br; ++q) mbar_init(&s_bfull[q], 1);
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    auto qwait = [&](uint64_t* bar, int u) { mbar_wait_parity(&bar[u % kDnQ], (u / kDnQ) & 1); };
+    if (warp == kD16Tma) {
+        // TMA warp: the pair's f32 tiles into a ring slot, its brackets into a slot
+        if (lane == 0) {
+            int jt = static_cast<int>(x0 / nch2), q2 = static_cast<int>(x0 % nch2);
+            auto issue = [&](int u, int jt_, int q_) {
+                const int s = u % kD16Ring;
+                const int nt = min(2, nch - 2 * q_);
+                mbar_expect_tx(&s_tfull[s], nt * tile_t);
+                for (int h = 0; h < nt; ++h)
+                    bulk_g2s(s_ring + (s * 2 + h) * tile_t, tile_src(jt_, 2 * q_ + h), tile_t, &s_tfull[s]);
+            };
+            {  // the first ring's worth of W tiles before the previous kernel ends
+                int jj = jt, qq = q2;
+                for (int u = 0; u < kD16Ring && u < n; ++u) {
+                    issue(u, jj, qq);
+                    if (++qq == nch2) {
+                        qq = 0;
+                        ++jj;
+                    }
+                }
+            }
+            pdl_wait();  // brackets come from the previous kernel
+            int jr = jt, qr = q2;  // ring refill position: pair u
+#pragma unroll 1
+            for (int u = 0; u < n; ++u) {
+                if (u >= kD16Ring) {
+                    // ring slot u % kD16Ring held pair u - kD16Ring: converted before its MMAs
+                    qwait(s_done, u - kD16Ring);
+                    dstamp(a, 2, u, 0);
+                    issue(u, jr, qr);
+                }
+                if (++qr == nch2) {
+                    qr = 0;
+                    ++jr;
+                }
+                // brackets of pair u: 8 input rows of B; slot u % kD16Br held pair
+                // u - kD16Br, read before done(u - kD16Ring) (waited above)
+                const int bs = u % kD16Br;
+                const int nin = min(2 * IC, L.in - q2 * 2 * IC);
+                const uint32_t bytes = static_cast<uint32_t>(nin) * a.B * 4;
+                mbar_expect_tx(&s_bfull[bs], 2 * bytes);
+                bulk_g2s(s_br + bs * 2 * br_bytes, a.bm_in + static_cast<size_t>(q2) * 2 * IC * a.B, bytes, &s_bfull[bs]);
+                bulk_g2s(s_br + bs * 2 * br_bytes + br_bytes, a.bt_in + static_cast<size_t>(q2) * 2 * IC * a.B, bytes,
+                         &s_bfull[bs]);
+                if (++q2 == nch2) {
+                    q2 = 0;
+                    ++jt;
+                }
+            }
+        }
+    } else if (warp == kD16Mma) {
+        // MMA warp: per K = 16 step, A x W_hi and A x W_lo (M = 128, N = 128, kind::f16)
+        const uint64_t dg0 = tc::make_desc(tc::smem_addr(s_stg), kLbo, 128);
+        constexpr uint64_t kStep = (2 * kLbo) >> 4;
+        const uint32_t idesc = tc::idesc_f16(kGmM, kGmN);
+        int seg = 0;
+        int q2 = static_cast<int>(x0 % nch2);
+#pragma unroll 1
+        for (int u = 0; u < n; ++u, q2 = q2 + 1 == nch2 ? 0 : q2 + 1) {
+            const bool first = u == 0 || q2 == 0;
+            const bool last = u == n - 1 || q2 + 1 == nch2;
+            if (first && u > 0) mbar_wait_parity(&s_accfree, (seg - 1) & 1);
+            qwait(s_full, u);
+            tc::fence_after_sync();
+            if (lane == 0) dstamp(a, 1, u, 0);
+            const uint32_t ta = tmem + kDnAcol + (u % kDnA) * 64;
+            const uint64_t dh = dg0 + (u % kD16Stg) * ((2 * half_t) >> 4), dl = dh + (half_t >> 4);
+            mma_chunk_ts<true>(tmem, ta, dh, dl, idesc, first ? 0u : 1u, nstep, kStep);
+            tc::mma_commit_warp(&s_done[u % kDnQ]);
+            if (lane == 0) dstamp(a, 1, u, 1);
+            if (last) {
+                tc::mma_commit_warp(&s_accfull[seg % kDnSeg]);
+                ++seg;
+            }
+        }
+    } else if (warp < kGmP / 64) {
+        // A warps, two sets of four taking alternate pairs: lane row r (sample
+        // r & 63, t_lo for r >= 64), every column k of the pair (k < KC: tile
+        // a, knot k / 4, input k % 4; k >= KC: tile b), fp16 pairs in TMEM
+        const int q4 = warp & 3, set = warp >> 2;
+        const int row = q4 * 32 + lane;
+        const int smp = row & 63;
+        const bool lo_row = row >= 64;
+        const int nS = min(64, a.B);
+        const bool aok = smp < nS;
+        int seg = 0;
+        int q2 = static_cast<int>(x0 % nch2), jt = static_cast<int>(x0 / nch2);
+#pragma unroll 1
+        for (int u = 0; u < n; ++u) {
+            const bool last = u == n - 1 || q2 + 1 == nch2;
+            const int jt_u = jt, q2_u = q2;
+            if (++q2 == nch2) {
+                q2 = 0;
+                ++jt;
+            }
+            if ((u & 1) != set) {
+                seg += last;
+                continue;
+            }
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 0);
+            const int bs = u % kD16Br;
+            mbar_wait_parity(&s_bfull[bs], (u / kD16Br) & 1);
+            const int* sbm = reinterpret_cast<const int*>(s_br + bs * 2 * br_bytes);
+            const float* sbt = reinterpret_cast<const float*>(s_br + bs * 2 * br_bytes + br_bytes);
+            int m[2 * IC];
+            __half w0[2 * IC], w1[2 * IC];
+#pragma unroll
+            for (int il = 0; il < 2 * IC; ++il) {
+                const bool ok = aok && q2_u * 2 * IC + il < L.in;
+                m[il] = ok ? sbm[il * a.B + smp] : -8;
+                const float t = ok ? sbt[il * a.B + smp] : 0.f;
+                const float u0 = 1.f - t;
+                const __half h0 = __float2half_rn(u0), h1 = __float2half_rn(t);
+                w0[il] = lo_row ? __float2half_rn(u0 - __half2float(h0)) : h0;
+                w1[il] = lo_row ? __float2half_rn(t - __half2float(h1)) : h1;
+            }
+            // TMEM A buffer u % kDnA held pair u - kDnA (this set waited for
+            // done(u - 2 - kDnA) at its previous pair)
+            if (u >= kDnA) qwait(s_done, u - kDnA);
+            tc::fence_after_sync();
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 1);
+            const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kDnAcol + (u % kDnA) * 64;
+            // KC2 fp16 = KC columns of fp16 pairs (compile-time knot and input of each)
+            float v[KC];
+#pragma unroll
+            for (int cc = 0; cc < KC; ++cc) {
+                __half e2[2];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int k = 2 * cc + hh;
+                    const int half = k >= KC ? 1 : 0, kk = k - KC * half;
+                    const int mk = kk / IC, il = IC * half + kk % IC;
+                    e2[hh] = mk == m[il] ? w0[il] : (mk == m[il] + 1 ? w1[il] : __float2half_rn(0.f));
+                }
+                v[cc] = __uint_as_float(static_cast<uint32_t>(__half_as_ushort(e2[0])) |
+                                        static_cast<uint32_t>(__half_as_ushort(e2[1])) << 16);
+            }
+            if constexpr (KC == 40) {
+                tc::tmem_st32(ta, v);
+                tc::tmem_st8(ta + 32, *reinterpret_cast<const float(*)[8]>(v + 32));
+            } else if constexpr (KC == 32) {
+                tc::tmem_st32(ta, v);
+            } else {
+                static_assert(KC == 24, "fp16 dense: G in {6, 8, 10}");
+                tc::tmem_st16(ta, v);
+                tc::tmem_st8(ta + 16, *reinterpret_cast<const float(*)[8]>(v + 16));
+            }
+            tc::tmem_wait_st();
+            tc::fence_before_sync();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
+            if (q4 == 0 && lane == 0) dstamp(a, set == 0 ? 0 : 3, u, 2);
+            if (!last) continue;
+            mbar_wait_parity(&s_accfull[seg % kDnSeg], (seg / kDnSeg) & 1);
+            tc::fence_after_sync();
+            const int segi = c - dn_owner(static_cast<long long>(jt_u) * nch2, T, P);
+            const int as = (q4 & 1) * 32 + lane;
+            const int j0 = jt_u * kGmN, nJ = min(kGmN, L.out - j0);
+            const size_t plane = static_cast<size_t>(a.B) * L.out;
+            float* dst = a.partial + (2 * segi + (q4 >> 1)) * plane + static_cast<size_t>(min(as, nS - 1)) * L.out + j0;
+#pragma unroll 1
+            for (int c8 = 0; c8 < kGmN; c8 += 8) {
+                float vv[8];
+                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, vv);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) vv[e] *= wsc_inv;
+                if (as < nS) {
+                    if (c8 + 8 <= nJ && (L.out & 3) == 0) {
+                        *reinterpret_cast<float4*>(dst + c8) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                        *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (c8 + e < nJ) dst[c8 + e] = vv[e];
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_accfree)) : "memory");
+            ++seg;
+        }
+    } else {
+        // conversion warps, kD16Cv sets of four taking pairs in turn: the f32
+        // tiles of the pair (ring) -> fp16 W_hi and W_lo (scaled) in a stage
+        const int set = (warp - kGmP / 64) >> 2;
+        const int lt = tid - kGmP / 2 - set * 128;
+        const int nq = static_cast<int>(tile_t / 16);  // float4 per tile
+        int q2 = static_cast<int>(x0 % nch2);
+        auto advance = [&]() { q2 = q2 + 1 == nch2 ? 0 : q2 + 1; };
+        for (int r = 0; r < set; ++r) advance();
+#pragma unroll 1
+        for (int u = set; u < n; u += kD16Cv) {
+            const int nt = min(2, nch - 2 * q2);
+            // stage u % kD16Stg held pair u - kD16Stg; done(u - kD16Stg) also
+            // completes the ring slot's phase of pair u - kD16Ring
+            if (lt == 0 && set == 0) dstamp(a, 2, u, 2);
+            if (u >= kD16Stg) qwait(s_done, u - kD16Stg);
+            mbar_wait_parity(&s_tfull[u % kD16Ring], (u / kD16Ring) & 1);
+            if (lt == 0 && set == 0) dstamp(a, 2, u, 3);
+            unsigned char* stg = s_stg + (u % kD16Stg) * 2 * half_t;
+            const float4* src = reinterpret_cast<const float4*>(s_ring + (u % kD16Ring) * 2 * tile_t);
+#pragma unroll 4
+            for (int qq = lt; qq < 2 * nq; qq += 128) {
+                const int hsel = qq >= nq ? 1 : 0, q = qq - hsel * nq;
+                // float4 q of an f32 tile: core-matrix column g = q / 128 (K
+                // 4g..4g+3), row (q % 128): fp16 K index k = KC * h + 4g ..
+                const int g = q >> 7, rr = q & 127;
+                const int k = KC * hsel + 4 * g;
+                const uint32_t o = (k >> 3) * kLbo + (rr >> 3) * 128 + (rr & 7) * 16 + (k & 7) * 2;
+                uint2 hi = make_uint2(0, 0), lo = make_uint2(0, 0);
+                if (hsel < nt) {
+                    // packed: f32x2 scale, two-at-a-time fp16 rounding, f32x2 remainder
+                    const float4 w = src[qq];
+                    const float2 sc = make_float2(wsc, wsc), neg = make_float2(-1.f, -1.f);
+                    const float2 a2 = __fmul2_rn(make_float2(w.x, w.y), sc), b2 = __fmul2_rn(make_float2(w.z, w.w), sc);
+                    const __half2 ha = __float22half2_rn(a2), hb = __float22half2_rn(b2);
+                    const __half2 la = __float22half2_rn(__ffma2_rn(__half22float2(ha), neg, a2));
+                    const __half2 lb = __float22half2_rn(__ffma2_rn(__half22float2(hb), neg, b2));
+                    hi = make_uint2(*reinterpret_cast<const uint32_t*>(&ha), *reinterpret_cast<const uint32_t*>(&hb));
+                    lo = make_uint2(*reinterpret_cast<const uint32_t*>(&la), *reinterpret_cast<const uint32_t*>(&lb));
+                }
+                *reinterpret_cast<uint2*>(stg + o) = hi;
+                *reinterpret_cast<uint2*>(stg + half_t + o) = lo;
+            }
+            tc::fence_proxy_async();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
+            if (lt == 0 && set == 0) dstamp(a, 2, u, 4);
+            for (int r = 0; r < kD16Cv; ++r) advance();
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<512>(tmem);
+}
+
 // Persistent dense layer: output j of tile jt has 2 * (CTAs holding part of
 // the tile) planes, summed in ascending order in f64.
 __global__ void k_dense_reduce(FwdArgs a, int nch, int P) {
@@ -1178,6 +1521,20 @@ size_t dense_persist_smem(int G) {
     const int kc = gemm_ic(G) * G;
     return (kDnRing + kDnLo) * static_cast<size_t>(kGmN) * kc * 4 + kDnBr * 2 * static_cast<size_t>(gemm_ic(G)) * 64 * 4;
 }
+// fp16 variant (k_dense_persist16): even G in {6, 8, 10} (IC = 4 tiles,
+// pair chunks of K = 8G), a finite grid (DevLayer::wsc > 0)
+bool dense_f16_ok(const DevLayer& L) {
+    static const bool off = [] {
+        const char* e = std::getenv("SKAN_DENSE_F16");  // A/B experiment: 0 = the tf32 persistent kernel
+        return e && e[0] == '0';
+    }();
+    return !off && L.wsc > 0.f && (L.G == 6 || L.G == 8 || L.G == 10);
+}
+size_t dense_f16_smem(int G) {
+    const size_t kc = 4 * static_cast<size_t>(G);
+    return kD16Ring * 2 * kGmN * kc * 4 + kD16Stg * 2 * kGmN * (2 * kc) * 2 + kD16Br * 2 * 8 * 64 * 4;
+}
+
 bool dense_persist_ok(const DevLayer& L, int B) {
     static const bool off = [] {
         const char* e = std::getenv("SKAN_DENSE_PERSIST");  // A/B experiment: 0 = the split GEMM
@@ -1197,17 +1554,19 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
         c.spt = 64;
         c.tj = kGmN;
         c.dn_nch = (L.in + c.ic - 1) / c.ic;
+        c.persist = dense_f16_ok(L) ? 2 : 1;
         const int ntile = (L.out + kGmN - 1) / kGmN;
-        const long long T = static_cast<long long>(ntile) * c.dn_nch;
+        const int units = c.persist == 2 ? d16_nch2(c.dn_nch) : c.dn_nch;  // schedule units per tile
+        const long long T = static_cast<long long>(ntile) * units;
         c.jt = sms;  // grid
         c.st = 1;
         int maxseg = 1;
         for (int jt = 0; jt < ntile; ++jt)
-            maxseg = std::max(maxseg, dn_owner(static_cast<long long>(jt + 1) * c.dn_nch - 1, T, sms) -
-                                          dn_owner(static_cast<long long>(jt) * c.dn_nch, T, sms) + 1);
+            maxseg = std::max(maxseg, dn_owner(static_cast<long long>(jt + 1) * units - 1, T, sms) -
+                                          dn_owner(static_cast<long long>(jt) * units, T, sms) + 1);
         c.nsplit = 2 * maxseg;
         c.ichunk = L.in;
-        c.smem = dense_persist_smem(L.G);
+        c.smem = c.persist == 2 ? dense_f16_smem(L.G) : dense_persist_smem(L.G);
         return c;
     }
     c.kind = 4;
@@ -1287,16 +1646,19 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         }();
         a.gemm_ring = dist_env;
         void (*kp)(FwdArgs, int) = c.ic == 4 ? k_dense_persist<4> : k_dense_persist<8>;
+        if (c.persist == 2)
+            kp = a.L.G == 10 ? k_dense_persist16<40> : (a.L.G == 8 ? k_dense_persist16<32> : k_dense_persist16<24>);
         ensure_smem(kp, c.smem);
-        launch_pdl(kp, dim3(c.jt), dim3(kDnT), c.smem, pdl, s, a, c.dn_nch);
+        launch_pdl(kp, dim3(c.jt), dim3(c.persist == 2 ? kD16T : kDnT), c.smem, pdl, s, a, c.dn_nch);
         if (!with_reduce) return;
+        const int units = c.persist == 2 ? d16_nch2(c.dn_nch) : c.dn_nch;  // the reduction's schedule unit
         const long long n = static_cast<long long>(a.B) * a.L.out;
         if (c.nsplit >= 32) {
             const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
-            launch_pdl(k_dense_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.dn_nch, c.jt);
+            launch_pdl(k_dense_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         } else {
             const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
-            launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.dn_nch, c.jt);
+            launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         }
         return;
     }
@@ -1329,6 +1691,39 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
 uint64_t dense_tile_floats(int in, int out, int G) {
     const int ic = gemm_ic(G);
     return static_cast<uint64_t>((out + kGmN - 1) / kGmN) * ((in + ic - 1) / ic) * kGmN * ic * G;
+}
+
+// max |v| as float bits (non-negative floats order like their bits; NaN
+// sorts above +inf)
+__global__ void k_absmax_bits(const float* __restrict__ p, size_t n, unsigned* out) {
+    unsigned m = 0;
+    for (size_t q = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<size_t>(gridDim.x) * blockDim.x)
+        m = max(m, __float_as_uint(p[q]) & 0x7FFFFFFFu);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// The fp16 GEMM's power-of-two scale of a tiled dense grid: max|W| * S in
+// [2^14, 2^15); 0 when the grid holds a non-finite value (no fp16 path).
+float dense_fp16_scale(const float* wt, uint64_t n, cudaStream_t s) {
+    unsigned* d = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned), s), "cudaMallocAsync");
+    cuda_check(cudaMemsetAsync(d, 0, sizeof(unsigned), s), "cudaMemsetAsync");
+    const int blocks = static_cast<int>(std::min<uint64_t>((n + 255) / 256, 148ull * 16));
+    k_absmax_bits<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(wt, n, d);
+    unsigned bits = 0;
+    cuda_check(cudaMemcpyAsync(&bits, d, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "absmax");
+    cuda_check(cudaFreeAsync(d, s), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(s), "absmax");
+    float mx;
+    std::memcpy(&mx, &bits, 4);
+    if (!std::isfinite(mx)) return 0.f;
+    if (mx == 0.f) return 1.f;
+    int ex = 0;
+    std::frexp(mx, &ex);  // mx = f * 2^ex, f in [0.5, 1)
+    return std::ldexp(1.0f, 15 - ex);
 }
 
 void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s) {

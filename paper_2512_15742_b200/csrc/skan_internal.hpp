@@ -116,6 +116,9 @@ struct DevLayer {
     // output block
     const float* wt;
     int wt_nch;
+    // dense tiled layers: power-of-two scale putting max|W| * wsc in [2^14, 2^15)
+    // for the fp16 split-precision GEMM (0: no fp16 path, e.g. non-finite grid)
+    float wsc;
 };
 
 // Per-layer launch plan for one batch size (chosen on the host).
@@ -248,6 +251,7 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms);
 int gemm_ic(int G);
 uint64_t dense_tile_floats(int in, int out, int G);
 void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s);
+float dense_fp16_scale(const float* wt, uint64_t n, cudaStream_t s);
 void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce = true);
 // MMA work one k_layer_gemm launch issues (flops, as 2*M*N*K per tcgen05.mma)
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B);

@@ -50,6 +50,16 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
            | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
 }
 
+// kind::f16 with fp16 A and B (K-major), f32 accumulation, shape M x N
+// (K = 16 per instruction).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4)                                  // D format: f32
+           | (0u << 7)                                // A format: f16
+           | (0u << 10)                               // B format: f16
+           | (static_cast<uint32_t>(N >> 3) << 17)    // N / 8
+           | (static_cast<uint32_t>(M >> 4) << 24);   // M / 16
+}
+
 // D[tmem] (+)= A[smem] * B[smem]^T, one elected thread.
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                          bool accumulate) {
