@@ -290,6 +290,7 @@ int skan_head_b1_grid(const skan_head* head);
  * D[128][N] = A[128][K] * B[K][N] (row-major f32, device pointers) on
  * tcgen05 kind::tf32 with `passes` = 1 (plain tf32) or 3 (split-precision
  * 3xTF32).  N in [16, 256] step 16, K in [8, 64] step 8. */
+/* passes == 1000: one kind::f16 pass with both operands rounded to fp16 in shared memory (M = 128) */
 skan_status skan_debug_gemm_tf32(const float* d_a, const float* d_b, float* d_d, int n, int k, int passes,
                                  void* stream);
 

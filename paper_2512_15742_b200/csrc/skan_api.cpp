@@ -593,6 +593,18 @@ void upload(skan_head* h, std::vector<Staged>& st, bool swap = false, cudaStream
                 d.cb32 = static_cast<const float*>(region(s.cb32.data(), static_cast<uint64_t>(d.K) * d.G * 4));
                 break;
         }
+        if (d.fmt == skan::FMT_I8_R32 || d.fmt == skan::FMT_I8_WIDE) {
+            // fp16 layer GEMM scale: |W| = |g c + b| <= max|g| * 128 + 128 |bias scale|
+            float gmax = 0.f;
+            for (float g : s.lutf) gmax = std::max(gmax, std::fabs(g));
+            const double bound = static_cast<double>(gmax) * 128.0 + 128.0 * std::fabs(d.bs);
+            d.wsc = 0.f;
+            if (std::isfinite(bound) && bound < 1e30) {
+                int ex = 0;
+                std::frexp(bound > 0.0 ? bound : 1.0, &ex);
+                d.wsc = static_cast<float>(std::ldexp(1.0, 15 - ex));
+            }
+        }
         if (d.fmt != skan::FMT_DENSE) {
             d.lutf = static_cast<const float*>(put(s.lutf, sizeof s.lutf));
             d.lutd = static_cast<const double*>(put(s.lutd, sizeof s.lutd));

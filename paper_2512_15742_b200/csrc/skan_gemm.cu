@@ -23,6 +23,63 @@
 namespace skan {
 namespace {
 
+// kind::f16 self-test: one CTA, D[128 x N] = A[128 x K] B[K x N] with A and B
+// rounded to fp16 and staged K-major (element (r, k) at (k / 8) * LBO +
+// (r / 8) * 128 + (r % 8) * 16 + (k % 8) * 2), K <= 64.
+__global__ void __launch_bounds__(128, 1) k_debug_gemm_f16(const float* __restrict__ A, const float* __restrict__ B,
+                                                          float* __restrict__ D, int N, int K) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar;
+    __shared__ uint32_t s_tmem;
+    unsigned char* a_s = smem;
+    unsigned char* b_s = smem + 128 * K * 2;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t lbo_a = (128 / 8) * 128, lbo_b = (N / 8) * 128;
+    for (int q = tid; q < 128 * K; q += 128) {
+        const int r = q / K, k = q % K;
+        *reinterpret_cast<__half*>(a_s + (k >> 3) * lbo_a + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2) = __float2half_rn(A[q]);
+    }
+    for (int q = tid; q < N * K; q += 128) {
+        const int k = q / N, n = q % N;
+        *reinterpret_cast<__half*>(b_s + (k >> 3) * lbo_b + (n >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2) = __float2half_rn(B[q]);
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc::fence_proxy_async();
+    if (warp == 0) tc::tmem_alloc<256>(&s_tmem);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = s_tmem;
+    if (warp == 0) {
+        const uint32_t idesc = tc::idesc_f16(128, N);
+        for (int s = 0; s < K / 16; ++s)
+            tc::mma_f16_ss_warp(tmem, tc::make_desc(tc::smem_addr(a_s) + s * 2 * lbo_a, lbo_a, 128),
+                                tc::make_desc(tc::smem_addr(b_s) + s * 2 * lbo_b, lbo_b, 128), idesc, s > 0);
+        tc::mma_commit_warp(&s_bar);
+    }
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(tc::smem_addr(&s_bar))
+            : "memory");
+    }
+    tc::fence_after_sync();
+    const int row = warp * 32 + lane;
+    for (int c = 0; c < N; c += 8) {
+        float v[8];
+        tc::tmem_ld8(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+        for (int q = 0; q < 8; ++q) D[row * N + c + q] = v[q];
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<256>(tmem);
+}
+
 __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__ A, const float* __restrict__ B,
                                                       float* __restrict__ D, int N, int K, int passes, int M, int ts) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -133,6 +190,17 @@ __global__ void __launch_bounds__(128, 1) k_debug_gemm(const float* __restrict__
 
 extern "C" skan_status skan_debug_gemm_tf32(const float* dA, const float* dB, float* dD, int N, int K, int passes,
                                             void* stream) {
+    if (passes == 1000) {  // kind::f16 (SS) self-test, M = 128
+        if (N < 16 || N > 256 || N % 16 || K < 16 || K > 64 || K % 16)
+            return skan::set_error(SKAN_SHAPE_ERROR, "debug gemm f16: N in [16,256] step 16, K in [16,64] step 16", 0,
+                                   SKAN_FAULT_NONE);
+        const size_t smem = static_cast<size_t>(128 * K + N * K) * 2;
+        cudaFuncSetAttribute(skan::k_debug_gemm_f16, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        skan::k_debug_gemm_f16<<<1, 128, smem, static_cast<cudaStream_t>(stream)>>>(dA, dB, dD, N, K);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return skan::set_error(SKAN_CUDA_ERROR, cudaGetErrorString(e), 0, SKAN_FAULT_NONE);
+        return SKAN_OK;
+    }
     // passes >= 300: A from TMEM, copied there from shared memory by
     // tcgen05.cp; >= 200: A from TMEM written by tcgen05.st (TS form, M =
     // 128); >= 100: M = 64 variant (passes - 100), D receives the raw 128 TMEM lanes
@@ -265,7 +333,7 @@ __device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph
     if (a.dbg && c < 64 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) a.dbg[(role * 64 + c) * 8 + ph] = clock64();
 }
 
-template <int FMT, int IC, bool STACK>
+template <int FMT, int IC, bool STACK, bool F16 = false>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_wfree[4];  // W stage free: the MMAs of its last chunk completed
@@ -282,10 +350,17 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     constexpr uint32_t kLboW = (2 * kGmN / 8) * 128, kLboA = (kGmM / 8) * 128;
     constexpr uint32_t kLoRows = (kGmN / 8) * 128;  // byte offset of the lo rows inside a K group
     constexpr int kAU = IC * kGmM / kGmP;           // A slots (row, input) per thread: 1 or 2
+    // F16 (int8 tables, even G, IC = 8): operands in fp16 split precision
+    // (kind::f16, K = 16 per MMA: half the tensor time of 3xTF32), W scaled
+    // by the layer's power of two DevLayer::wsc (folded into the gain LUT
+    // and the bias scale), hi / lo halves rounded to nearest
+    static_assert(!F16 || (kI8 && IC == 8), "fp16 layer GEMM: int8 tables, IC = 8");
+    constexpr int kEl = F16 ? 2 : 4;                // operand element bytes
     const DevLayer& L = a.L;
     const int G = L.G, KC = IC * G;
-    const uint32_t tile_t = kGmN * KC * 4;          // one 128-output plane (a dense tile)
-    const uint32_t tile_a = kGmM * KC * 4;
+    const uint32_t tile_t = kGmN * KC * kEl;        // one 128-output plane (a dense tile)
+    const uint32_t tile_a = kGmM * KC * kEl;
+    const float wsc = F16 ? L.wsc : 1.f;
     const int wst = a.gemm_wst;
     const int ring = kDense ? a.gemm_ring : 1;
     // smem: two A buffers [A_hi (| A_lo)], `wst` W stages (2 planes each),
@@ -301,7 +376,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     const int nchunks = rend > r0 ? (rend - r0 + IC - 1) / IC : 0;
     pdl_trigger();
     if constexpr (kI8) {
-        if (tid < 256) s_lut[tid] = L.lutf[tid];
+        if (tid < 256) s_lut[tid] = L.lutf[tid] * wsc;
     }
     // the A tiles are sparse: zero them once; each slot owner keeps them clean
     for (uint32_t q = tid * 16; q < 2 * abuf; q += kGmT * 16)
@@ -322,10 +397,12 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     const uint32_t tmem = s_tmem;
 
     // W roles: thread (column rl, lane group eg) owns the edges of inputs
-    // il = eg + kTPC * v, v < kEPT, of its column: every edge record and
-    // codebook row is gathered by exactly one thread (consecutive lanes:
-    // the same column's inputs, then the next column)
+    // il = eg + kTPC * v (F16: il = kEPT * eg + v, adjacent inputs: one
+    // 32-bit store writes a knot of both), v < kEPT, of its column: every edge
+    // record and codebook row is gathered by exactly one thread (consecutive
+    // lanes: the same column's inputs, then the next column)
     const int rl = tid / kTPC, eg = tid % kTPC;
+    auto il_of = [&](int v) { return F16 ? kEPT * eg + v : eg + kTPC * v; };
     const uint32_t rbase = tc::kmajor_off(rl, 0, 2 * kGmN);
     // Producer state, double-buffered: while chunk c is written from set
     // (c & 1), chunk c+1's loads land in the other set (issued at the top of
@@ -355,7 +432,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         bm0[u] = a.bm_in + static_cast<size_t>(r0 + ila) * a.B + s0 + smp;
         bt0[u] = a.bt_in + static_cast<size_t>(r0 + ila) * a.B + s0 + smp;
     }
-    const float bs_f = static_cast<float>(L.bs);
+    const float bs_f = static_cast<float>(L.bs) * wsc;
     const size_t cbase = static_cast<size_t>(r0 / IC);  // DENSE: first chunk of this split in the tiles
     auto issue_tile = [&](int c, int slot) {  // DENSE: TMA of chunk c's pre-tiled W into ring slot `slot`
         if constexpr (kDense) {
@@ -372,7 +449,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             nvalid = 0;
 #pragma unroll
             for (int v = 0; v < kEPT; ++v) {
-                const int i = ib + eg + kTPC * v;
+                const int i = ib + il_of(v);
                 if (rl < nJ && i < rend) {
                     nvalid |= 1u << v;
                     rec_load<FMT>(L, static_cast<size_t>(i) * L.out + j0 + rl, recn[v], kn[v]);
@@ -460,6 +537,33 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                 *reinterpret_cast<float4*>(st + o + kLoRows) =
                     make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
             }
+        } else if constexpr (F16) {
+            // W (fp16): the thread's two edges are adjacent inputs il0 = 2 eg,
+            // il0 + 1 of column rl, so knot m of both is ONE 32-bit store at
+            // k = m * 8 + il0: byte (k / 8) * LBO + row part + (k % 8) * 2;
+            // g and b arrive scaled by wsc (LUT, bias scale), W_hi = fp16(W),
+            // W_lo = fp16(W - W_hi)
+            const uint32_t ob = rbase + (kEPT * eg) * 2;
+            const bool ok0 = cur.valid & 1u, ok1 = cur.valid >> 1 & 1u;
+            const float2 g2 = make_float2(ok0 ? cur.er[0].g : 0.f, ok1 ? cur.er[1].g : 0.f);
+            const float2 b2 = make_float2(ok0 ? cur.er[0].b : 0.f, ok1 ? cur.er[1].b : 0.f);
+            const float2 off = make_float2(-8388736.0f, -8388736.0f), neg = make_float2(-1.f, -1.f);
+            const uint32_t r0w[4] = {cur.er[0].row.x, cur.er[0].row.y, cur.er[0].row.z, cur.er[0].row.w};
+            const uint32_t r1w[4] = {cur.er[1].row.x, cur.er[1].row.y, cur.er[1].row.z, cur.er[1].row.w};
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                if (m >= G) break;
+                const uint32_t sel = static_cast<uint32_t>(m & 3) | 0x7540u;
+                float2 cf = make_float2(__uint_as_float(__byte_perm(r0w[m >> 2], 0x4B000000u, sel)),
+                                        __uint_as_float(__byte_perm(r1w[m >> 2], 0x4B000000u, sel)));
+                cf = __fadd2_rn(cf, off);
+                const float2 w = __ffma2_rn(g2, cf, b2);
+                const __half2 h = __float22half2_rn(w);
+                const __half2 l = __float22half2_rn(__ffma2_rn(__half22float2(h), neg, w));
+                const uint32_t o = ob + m * kLboW;
+                *reinterpret_cast<__half2*>(st + o) = h;
+                *reinterpret_cast<__half2*>(st + o + kLoRows) = l;
+            }
         } else {
             // W: every knot of this thread's edges (hi row rl, lo row 128 + rl);
             // k = m * IC + il sits at byte (k/4) * LBO + row part + (k%4) * 4
@@ -517,6 +621,35 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         for (int u = 0; u < kAU; ++u) {
             const int q = tid + kGmP * u, ra = q / IC, il = q % IC;
             const bool lo_row = STACK && ra >= 64;
+            if constexpr (F16) {
+                // fp16 hat weights: element (r, k) at (k / 8) * LBO + row part + (k % 8) * 2
+                if (cur.aoff[u] != 0xFFFFFFFFu) {
+                    const uint32_t o0 = cur.aoff[u] & 0xFFFFu, o1 = cur.aoff[u] >> 16;
+                    *reinterpret_cast<__half*>(sab + o0) = __float2half_rn(0.f);
+                    *reinterpret_cast<__half*>(sab + o1) = __float2half_rn(0.f);
+                    if constexpr (!STACK) {
+                        *reinterpret_cast<__half*>(sab + tile_a + o0) = __float2half_rn(0.f);
+                        *reinterpret_cast<__half*>(sab + tile_a + o1) = __float2half_rn(0.f);
+                    }
+                    cur.aoff[u] = 0xFFFFFFFFu;
+                }
+                if (cur.bm[u] >= 0) {
+                    const int k0 = cur.bm[u] * IC + il, k1 = k0 + IC;
+                    const uint32_t o0 = (k0 >> 3) * kLboA + (ra >> 3) * 128 + (ra & 7) * 16 + (k0 & 7) * 2;
+                    const uint32_t o1 = (k1 >> 3) * kLboA + (ra >> 3) * 128 + (ra & 7) * 16 + (k1 & 7) * 2;
+                    const float w0 = 1.f - cur.bt[u], w1 = cur.bt[u];
+                    const __half h0 = __float2half_rn(w0), h1 = __float2half_rn(w1);
+                    const __half l0 = __float2half_rn(w0 - __half2float(h0)), l1 = __float2half_rn(w1 - __half2float(h1));
+                    *reinterpret_cast<__half*>(sab + o0) = lo_row ? l0 : h0;
+                    *reinterpret_cast<__half*>(sab + o1) = lo_row ? l1 : h1;
+                    if constexpr (!STACK) {
+                        *reinterpret_cast<__half*>(sab + tile_a + o0) = l0;
+                        *reinterpret_cast<__half*>(sab + tile_a + o1) = l1;
+                    }
+                    cur.aoff[u] = o0 | (o1 << 16);
+                }
+                continue;
+            }
             if (cur.aoff[u] != 0xFFFFFFFFu) {
                 const uint32_t o0 = cur.aoff[u] & 0xFFFFu, o1 = cur.aoff[u] >> 16;
                 *reinterpret_cast<float*>(sab + o0) = 0.f;
@@ -574,13 +707,35 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         // the MMA warp: issues the chunk's tcgen05.mma in order,
         // warp-uniform (one elected lane issues); descriptors advance by
         // immediates from per-chunk bases
-        const int nks = KC / 8;
+        const int nks = KC / (F16 ? 16 : 8);
         const uint64_t da0 = tc::make_desc(tc::smem_addr(s_a), kLboA, 128);
         const uint64_t dw0 = tc::make_desc(tc::smem_addr(s_w), kLboW, 128);
         constexpr uint64_t kStepA = (2 * kLboA) >> 4, kStepW = (2 * kLboW) >> 4;  // descriptor address units
-        const uint32_t idesc2 = tc::idesc_tf32(kGmM, 2 * kGmN), idesc1 = tc::idesc_tf32(kGmM, kGmN);
+        const uint32_t idesc2 = F16 ? tc::idesc_f16(kGmM, 2 * kGmN) : tc::idesc_tf32(kGmM, 2 * kGmN);
+        const uint32_t idesc1 = F16 ? tc::idesc_f16(kGmM, kGmN) : tc::idesc_tf32(kGmM, kGmN);
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
+            if constexpr (F16) {  // K = 16 steps (two core-matrix columns), same descriptor strides
+                const int ab = c & 1;
+                mbar_wait_parity(&s_full[ws], wph);
+                tc::fence_after_sync();
+                const uint64_t da = da0 + ab * (abuf >> 4);
+                const uint64_t dw = dw0 + ws * (wstage >> 4);
+#pragma unroll
+                for (int s = 0; s < 8; ++s) {
+                    if (s >= nks) break;
+                    tc::mma_f16_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
+                    if constexpr (!STACK)
+                        tc::mma_f16_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
+                }
+                tc::mma_commit_warp(&s_afree[ab]);
+                tc::mma_commit_warp(&s_wfree[ws]);
+                if (++ws == wst) {
+                    ws = 0;
+                    wph ^= 1u;
+                }
+                continue;
+            }
             const int ab = c & 1;
             mbar_wait_parity(&s_full[ws], wph);
             if (lane == 0) gstamp(a, 1, c, 0);
@@ -633,8 +788,9 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             if (nchunks > 0) {
                 tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
                 tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
+                const float inv = F16 ? 1.0f / wsc : 1.0f;  // exact: wsc is a power of two
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] += w[u];
+                for (int u = 0; u < 8; ++u) v[u] = (v[u] + w[u]) * inv;
             } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) v[u] = 0.f;
@@ -1464,7 +1620,7 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStre
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kernel, args...);
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, args...), "kernel launch");
 }
 
 }  // namespace
@@ -1544,6 +1700,16 @@ bool dense_persist_ok(const DevLayer& L, int B) {
            dense_persist_smem(L.G) <= kGemmSmemLimit;
 }
 
+// int8 layers in fp16 split precision (k_layer_gemm<..., F16>): even G with
+// a finite scale; IC = 8 keeps K = 8G a multiple of the f16 MMA's 16
+bool gemm_f16_ok(const DevLayer& L) {
+    static const bool off = [] {
+        const char* e = std::getenv("SKAN_GEMM_F16");  // A/B experiment: 0 = 3xTF32
+        return e && e[0] == '0';
+    }();
+    return !off && (L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE) && L.G % 2 == 0 && L.G <= 12 && L.wsc > 0.f;
+}
+
 LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     LaunchCfg c{};
     if (dense_persist_ok(L, B)) {
@@ -1571,6 +1737,10 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
     }
     c.kind = 4;
     c.ic = gemm_ic(L.G);
+    if (gemm_f16_ok(L)) {
+        c.persist = 3;
+        c.ic = 8;  // the same shared-memory bytes per chunk as tf32 at IC = 4
+    }
     c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: 64 = A_hi / A_lo stacked in the 128 rows
     const bool stack = c.spt == 64;
     c.tj = kGmN;
@@ -1605,8 +1775,9 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
 }
 
 template <bool STACK>
-void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
+void (*gemm_kernel(int fmt, int ic, bool f16 = false))(FwdArgs) {
     const bool i4 = ic == 4;
+    if (f16) return fmt == FMT_I8_R32 ? k_layer_gemm<FMT_I8_R32, 8, STACK, true> : k_layer_gemm<FMT_I8_WIDE, 8, STACK, true>;
     switch (fmt) {
         case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, STACK> : k_layer_gemm<FMT_I8_R32, 8, STACK>;
         case FMT_I8_WIDE: return i4 ? k_layer_gemm<FMT_I8_WIDE, 4, STACK> : k_layer_gemm<FMT_I8_WIDE, 8, STACK>;
@@ -1616,7 +1787,7 @@ void (*gemm_kernel(int fmt, int ic))(FwdArgs) {
 }
 
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B) {
-    if (c.persist)  // one M=128 x N=256 x K=8 MMA per K step of every (tile, chunk)
+    if (c.persist == 1 || c.persist == 2)  // one M=128 x N=256 x K=8 MMA per K step of every (tile, chunk)
         return static_cast<double>((L.out + kGmN - 1) / kGmN) * c.dn_nch * (c.ic * L.G / 8) * 2.0 * kGmM * 8 *
                (2 * kGmN);
     // per CTA and K = 8 step: one M=128 x N=256 MMA, plus (not stacked) one N=128
@@ -1639,7 +1810,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         return e ? std::atoi(e) : 0;
     }();
     a.gemm_skip = skip_env;
-    if (c.persist) {
+    if (c.persist == 1 || c.persist == 2) {  // dense persistent (tf32 / fp16)
         static const int dist_env = [] {
             const char* e = std::getenv("SKAN_DENSE_PREFETCH");  // experiment: L2 prefetch distance in chunks
             return e ? std::atoi(e) : 0;
@@ -1663,7 +1834,8 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         return;
     }
     const bool stack = c.spt == 64;
-    void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic) : gemm_kernel<false>(a.L.fmt, c.ic);
+    const bool f16 = c.persist == 3;  // int8 layer GEMM in fp16 split precision
+    void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic, f16) : gemm_kernel<false>(a.L.fmt, c.ic, f16);
     ensure_smem(k, c.smem);
     static const int carve_env = [] {
         const char* e = std::getenv("SKAN_GEMM_CARVEOUT");  // experiment: shared-memory carve-out percent

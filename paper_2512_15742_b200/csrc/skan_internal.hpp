@@ -135,7 +135,8 @@ struct LaunchCfg {
     int rw;      // rows per warp (small kernel); GEMM: dense TMA ring slots
     int ic;      // inputs per staged chunk (large kernel)
     size_t smem; // dynamic shared memory bytes (large kernel)
-    int persist; // GEMM: dense layer on the persistent schedule (k_dense_persist, batch <= 64)
+    int persist; // GEMM: 1 / 2 = dense layer on the persistent schedule (k_dense_persist, tf32 / fp16;
+                 // batch <= 64); 3 = int8 layer GEMM in fp16 split precision
     int dn_nch;  // persistent dense: chunks per output tile
 };
 

@@ -983,7 +983,7 @@ void launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStrea
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kernel, args...);
+    cuda_check(cudaLaunchKernelEx(&cfg, kernel, args...), "kernel launch");
 }
 
 template <int FMT, int VJ, int S>

@@ -33,3 +33,23 @@ def test_tf32x3_gemm_matches_f64(n, k, ts):
         out[passes] = np.max(np.abs(dd.cpu().numpy() - want) / scale)
     assert out[3] < 2e-6, out
     assert out[1] > 1e-5, out  # one tf32 pass really is coarser (the test sees the lo terms)
+
+
+@pytest.mark.parametrize("n,k", [(16, 16), (128, 32), (256, 64), (208, 48)])
+def test_f16_ss_gemm_matches_fp16_rounded_inputs(n, k):
+    """kind::f16 with both operands in shared memory (the layer GEMM's fp16
+    split-precision form): D = fp16(A) fp16(B) accumulated in f32, checked
+    against the f64 product of the fp16-rounded inputs."""
+    import torch
+    rng = np.random.default_rng(7 * n + k)
+    a = rng.standard_normal((128, k)).astype(np.float32)
+    b = rng.standard_normal((k, n)).astype(np.float32)
+    a16, b16 = a.astype(np.float16).astype(np.float64), b.astype(np.float16).astype(np.float64)
+    want = a16 @ b16
+    scale = np.abs(a16) @ np.abs(b16)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    dd = torch.zeros((128, n), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().skan_debug_gemm_tf32(da.data_ptr(), db.data_ptr(), dd.data_ptr(), n, k, 1000,
+                                               torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert np.max(np.abs(dd.cpu().numpy() - want) / scale) < 1e-6

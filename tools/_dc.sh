@@ -1,7 +1,4 @@
-mkdir -p gpurun_out/s4j
-timeout 120 python tools/dense_check.py > gpurun_out/s4j/dc.txt 2>&1; echo "rc $?" >> gpurun_out/s4j/dc.txt
-timeout 60 python tools/dense_timeline.py --chunks 10 > gpurun_out/s4j/tl.txt 2>&1
-for rep in 1 2; do
-echo "== f16"; timeout 60 python tools/diag_configs.py --only-dense 2>&1 | grep cfg4
-echo "== tf32"; SKAN_DENSE_F16=0 timeout 60 python tools/diag_configs.py --only-dense 2>&1 | grep cfg4
-done > gpurun_out/s4j/sweep.txt
+mkdir -p gpurun_out/s4r
+for w in 2 3; do
+echo "== WST=$w"; SKAN_GEMM_WST=$w timeout 60 python tools/diag_latency.py --batches 4,64,256 --reps 100 2>&1 | grep "flush=True"
+done > gpurun_out/s4r/lat.txt
