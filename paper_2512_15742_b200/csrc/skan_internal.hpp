@@ -244,7 +244,8 @@ void launch_unpack_indices(const uint8_t* bytes, uint64_t count, int bits, uint3
 
 // Tensor-core layer GEMM (skan_gemm.cu), kind 4 of LaunchCfg: two launches
 // (the GEMM over input splits, then the fixed-order split reduction).
-constexpr int kB1MaxBatch = 3;     // batches served by per-sample persistent batch-1 launches
+constexpr int kB1MaxBatch = 2;     // batches served by per-sample persistent batch-1 launches (B = 3 is
+                                    // faster on the fp16 layer GEMM: 53 vs 57 us, profiles/r2/latency_by_batch.txt)
 constexpr int kGemmMinBatch = 3;  // smallest batch routed to the tensor-core layer GEMM (default; heads the batch-1 kernel takes use it from 4)
 extern int g_gemm_min_batch;      // current threshold (skan_debug_set_gemm_min_batch)
 bool gemm_supported(const DevLayer& L);
