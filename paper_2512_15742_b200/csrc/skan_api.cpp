@@ -229,6 +229,7 @@ struct skan_head {
     // persisting-L2 fraction requested by skan_head_set_l2_persist (0: off);
     // skan_forward_multi applies it to the side stream that runs this head
     mutable float l2_frac = 0.f;
+    uint64_t gen = 1;  // bumped whenever the resident tables (and so kernel parameters) change
 };
 
 struct skan_workspace {
@@ -254,8 +255,17 @@ struct skan_workspace {
     int last_launches = 0;
     const double* last_x = nullptr;  // device inputs of the last fast forward (profiling hook)
     float* b1_part = nullptr;        // 2 x [grid][max_width] partials of the batch-1 kernel
-    unsigned* b1_done = nullptr;     // its monotonic last-layer arrival counter
-    unsigned b1_epoch = 0;           // value of *b1_done when the next launch starts
+    unsigned* b1_done = nullptr;     // its arrival / grid-barrier counters (0 between launches)
+    // Host-buffer batch-1 forwards replay a CUDA graph [H2D of x from a pinned
+    // staging buffer -> the persistent kernel writing y into mapped pinned
+    // memory]: one launch call instead of a copy plus a cooperative launch
+    // with a 2 KB parameter block.  Rebuilt when the head's tables change.
+    double* pin_in = nullptr;        // page-locked staging of one sample's inputs
+    double* pin_out = nullptr;       // page-locked (mapped) outputs of one sample
+    double* pin_out_d = nullptr;     // its device alias
+    cudaGraphExec_t b1_graph = nullptr;
+    uint64_t b1_graph_gen = 0;       // skan_head::gen the graph was built for
+    bool b1_graph_failed = false;    // capture unsupported: keep the copy + launch path
     unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
     // Fast-path launch plans for every batch 1..max_batch, [B-1][layer],
     // built at creation (forward allocates nothing); rebuilt in place if the
@@ -882,12 +892,10 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
                 a.part[1] = ws->b1_part + n;
                 a.x_tma = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (h->in_dim % 2 == 0);
                 a.done = ws->b1_done;
-                a.epoch = ws->b1_epoch;
+                a.epoch = 0;  // the kernel's last CTA resets the counters
                 a.err = err_flag ? err_flag : d.err;
                 a.timeline = ws->b1_timeline;
                 skan::cuda_check(skan::launch_head_b1(a, h->b1_grid, h->b1_smem, s), "kernel launch");
-                // every CTA arrives once; advanced only for a launch that was accepted
-                ws->b1_epoch += static_cast<unsigned>(h->b1_grid);
             }
             skan::cuda_check(cudaGetLastError(), "kernel launch");
             return B;
@@ -995,6 +1003,7 @@ void swap_staged(skan_head* h, std::vector<Staged>& st, cudaStream_t stream) {
     h->totals = tot;
     upload(h, st, /*swap=*/true, stream);
     if (h->b1_ok) refresh_b1_layers(h, stream);
+    ++h->gen;  // captured launches (workspace graphs) are rebuilt
 }
 
 // Staging of directly loaded layers: headers (already checked by the SKAN
@@ -1156,9 +1165,15 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
         if (h->b1_ok) {
             const size_t n = h->b1_plan.part_floats;
             ws->b1_part = static_cast<float*>(alloc(2 * n * sizeof(float)));
-            // [0] last-layer arrivals, [1] the v2 kernel's grid barrier (both monotonic)
+            // [0] last-layer arrivals, [1] the v2 kernel's grid barrier (0 between launches)
             ws->b1_done = static_cast<unsigned*>(alloc(2 * sizeof(unsigned)));
             skan::cuda_check(cudaMemset(ws->b1_done, 0, 2 * sizeof(unsigned)), "cudaMemset");
+            skan::cuda_check(cudaHostAlloc(&ws->pin_in, static_cast<size_t>(h->in_dim) * 8, cudaHostAllocDefault),
+                             "cudaHostAlloc");
+            skan::cuda_check(cudaHostAlloc(&ws->pin_out, static_cast<size_t>(h->out_dim) * 8, cudaHostAllocMapped),
+                             "cudaHostAlloc");
+            skan::cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->pin_out_d), ws->pin_out, 0),
+                             "cudaHostGetDevicePointer");
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));
@@ -1175,8 +1190,11 @@ skan_status skan_workspace_destroy(skan_workspace* ws) {
     return guarded([&] {
         if (!ws) return;
         DeviceGuard g(ws->device);
+        if (ws->b1_graph) cudaGraphExecDestroy(ws->b1_graph);
         for (void* p : ws->allocs) cudaFree(p);
         if (ws->zc_err_h) cudaFreeHost(ws->zc_err_h);
+        if (ws->pin_in) cudaFreeHost(ws->pin_in);
+        if (ws->pin_out) cudaFreeHost(ws->pin_out);
         delete ws;
     });
 }
@@ -1209,6 +1227,51 @@ const double* mapped_alias(const double* p) {
     return static_cast<const double*>(at.devicePointer);
 }
 
+// The workspace's batch-1 host-path graph: [H2D pin_in -> xin, the
+// persistent kernel (y -> mapped pin_out)], captured on a private stream;
+// null when capture is not possible (the caller falls back).
+cudaGraphExec_t b1_host_graph(const skan_head* h, skan_workspace* ws) {
+    if (ws->b1_graph && ws->b1_graph_gen == h->gen) return ws->b1_graph;
+    if (ws->b1_graph_failed) return nullptr;
+    if (ws->b1_graph) {
+        cudaGraphExecDestroy(ws->b1_graph);
+        ws->b1_graph = nullptr;
+    }
+    cudaStream_t cs = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    bool ok = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+        cudaMemcpyAsync(ws->xin, ws->pin_in, static_cast<size_t>(h->in_dim) * 8, cudaMemcpyHostToDevice, cs);
+        skan::HeadB1Args a = h->b1_plan;
+        const size_t n = h->b1_plan.part_floats;
+        a.x = ws->xin;
+        a.y = ws->pin_out_d;
+        a.part[0] = ws->b1_part;
+        a.part[1] = ws->b1_part + n;
+        a.x_tma = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) && (h->in_dim % 2 == 0);
+        a.done = ws->b1_done;
+        a.epoch = 0;
+        a.err = ws->d.err;
+        a.timeline = nullptr;
+        skan::launch_head_b1(a, h->b1_grid, h->b1_smem, cs);
+        ok = cudaStreamEndCapture(cs, &g) == cudaSuccess && g;
+    }
+    ok = ok && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (cs) cudaStreamDestroy(cs);
+    cudaGetLastError();  // a failed capture leaves no sticky error behind
+    if (!ok) {
+        if (ex) cudaGraphExecDestroy(ex);
+        ws->b1_graph_failed = true;
+        return nullptr;
+    }
+    ws->b1_graph = ex;
+    ws->b1_graph_gen = h->gen;
+    return ex;
+}
+
 skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* inputs,
                          uint64_t n_inputs, int batch, double* outputs, uint64_t n_outputs,
                          int mode, unsigned ptr_flags, void* stream) {
@@ -1235,6 +1298,20 @@ skan_status skan_forward(const skan_head* h, skan_workspace* ws, const double* i
         // kernel writes y straight into host memory and reports a non-finite
         // input in a mapped host flag: copy + launch + sync instead of
         // memset + copy + launch + two D2H copies + sync.
+        // One sample: replay the workspace's graph (x staged through pinned
+        // memory, y read back from mapped pinned memory: any host buffers).
+        if (host && !exact && batch == 1 && h->b1_ok && ws->b1_part && ws->pin_in && !ws->b1_timeline) {
+            if (cudaGraphExec_t ge = b1_host_graph(h, ws)) {
+                std::memcpy(ws->pin_in, inputs, static_cast<size_t>(in) * 8);
+                skan::cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+                skan::cuda_check(cudaStreamSynchronize(s), "forward");
+                ws->last_launches = 1;
+                raise_if_flagged(ws);
+                std::memcpy(outputs, ws->pin_out, static_cast<size_t>(out) * 8);
+                ws->interp_ops += h->edges;  // after success, as lutham.cpp:849
+                return;
+            }
+        }
         if (host && !exact && batch <= skan::kB1MaxBatch && batch <= ws->max_batch && h->b1_ok && ws->b1_part) {
             double* dy = const_cast<double*>(mapped_alias(outputs));
             if (dy) {

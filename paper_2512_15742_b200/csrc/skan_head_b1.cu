@@ -590,6 +590,13 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1(const __grid_constant__ HeadB
     }
     stamp(h, 13);
     stamp_clock(h, 15);
+    // every CTA has arrived: the counters restart at 0 for the next launch
+    // (stream order makes the reset visible to it), so a launch's
+    // parameters never change from call to call (CUDA-graph replay)
+    if (threadIdx.x == 0) {
+        h.done[0] = 0u;
+        h.done[1] = 0u;
+    }
 }
 
 // ===========================================================================
@@ -943,6 +950,10 @@ __global__ void __launch_bounds__(kT, 1) k_head_b1v2(const __grid_constant__ Hea
         }
     }
     stamp(h, 13);
+    if (tid == 0) {  // all CTAs arrived: restart the counters at 0 (see k_head_b1)
+        h.done[0] = 0u;
+        h.done[1] = 0u;
+    }
 }
 
 }  // namespace

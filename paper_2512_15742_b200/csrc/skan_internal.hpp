@@ -182,8 +182,9 @@ struct HeadB1Args {
     const double* x;   // [in]
     double* y;         // [out]
     float* part[2];    // per-CTA partials, [grid][layer width], ping-pong by layer
-    unsigned* done;    // monotonic arrival counter of the last layer (last CTA reduces)
-    unsigned epoch;    // value of *done when this launch starts
+    unsigned* done;    // [0] arrival counter of the last layer (last CTA reduces), [1] v2's grid
+                       // barrier; both 0 at launch, reset to 0 by the last CTA
+    unsigned epoch;    // value of *done when this launch starts (always 0 now)
     int* err;
     unsigned long long* timeline;  // optional: [grid][16] %globaltimer stamps per phase
     int rec_cap;           // layer-0 rows whose records are staged in shared memory

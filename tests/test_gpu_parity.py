@@ -521,8 +521,8 @@ def test_zero_copy_host_forward(torch_cuda):
         yn = np.zeros(batch * 20)  # pageable: copy path, same result
         hq.compressed_forward(model, x, batch, yn, ws, mode="fast")
         assert np.array_equal(_bits(yn), _bits(yp.numpy()))
-    xp[5] = float("nan")
-    rc = L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 3, yp.data_ptr(), yp.numel(),
+    xp[2048 + 5] = float("nan")  # batch 2: per-sample persistent launches
+    rc = L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 2, yp.data_ptr(), yp.numel(),
                         hq.MODE_FAST, _lib.SKAN_PTR_HOST, s)
     assert rc == 2  # SKAN_VALUE_ERROR
     x = synthetic.synthetic_inputs(1, 2048, seed=5)
@@ -530,6 +530,19 @@ def test_zero_copy_host_forward(torch_cuda):
     yp = torch.zeros(20, dtype=torch.float64).pin_memory()
     _lib.check(L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 1, yp.data_ptr(), yp.numel(),
                               hq.MODE_FAST, _lib.SKAN_PTR_HOST, s))  # the flag was reset
+    xp[7] = float("inf")  # batch 1: the workspace's graph replay reports it too
+    rc = L.skan_forward(model.handle, ws.handle, xp.data_ptr(), xp.numel(), 1, yp.data_ptr(), yp.numel(),
+                        hq.MODE_FAST, _lib.SKAN_PTR_HOST, s)
+    assert rc == 2
+    # batch 1 from PAGEABLE buffers also replays the graph (x staged, y copied out): bitwise equal
+    x = synthetic.synthetic_inputs(1, 2048, seed=6)
+    yn = np.zeros(20)
+    _lib.check(L.skan_forward(model.handle, ws.handle, x.ctypes.data, x.size, 1, yn.ctypes.data, yn.size,
+                              hq.MODE_FAST, _lib.SKAN_PTR_HOST, s))
+    dy = torch.zeros(20, dtype=torch.float64, device="cuda")
+    hq.forward_async(model, torch.from_numpy(x).cuda(), 1, dy, ws, stream=s)
+    ws.check()
+    assert np.array_equal(_bits(yn), _bits(dy.cpu().numpy()))
 
 
 def test_hot_swap_refills_a_resident_head(torch_cuda):
