@@ -333,7 +333,7 @@ __device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph
     if (a.dbg && c < 64 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) a.dbg[(role * 64 + c) * 8 + ph] = clock64();
 }
 
-template <int FMT, int IC, bool STACK, bool F16 = false>
+template <int FMT, int IC, bool STACK, bool F16 = false, bool DUAL = false>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_wfree[4];  // W stage free: the MMAs of its last chunk completed
@@ -344,12 +344,17 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     __shared__ float s_lut[256];
     constexpr bool kDense = FMT == FMT_DENSE;
     constexpr bool kI8 = FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE;
-    constexpr int S = STACK ? 64 : kGmM;            // samples per tile
+    // DUAL (fp16 only): 256 samples per CTA as two 128-sample halves, each
+    // with its own A_hi / A_lo tiles and TMEM accumulator, sharing every W
+    // stage: W is decoded once per 256 samples instead of once per 128.  One
+    // A buffer (80 KB), so the A of chunk c+1 waits for chunk c's MMAs.
+    static_assert(!DUAL || (F16 && !STACK), "dual-half tiles: fp16, unstacked");
+    constexpr int S = STACK ? 64 : (DUAL ? 2 * kGmM : kGmM);  // samples per tile
     constexpr int kTPC = kGmP / kGmN;               // W: threads per output column (4)
     constexpr int kEPT = IC / kTPC;                 // W: edges (inputs) per thread and chunk
     constexpr uint32_t kLboW = (2 * kGmN / 8) * 128, kLboA = (kGmM / 8) * 128;
     constexpr uint32_t kLoRows = (kGmN / 8) * 128;  // byte offset of the lo rows inside a K group
-    constexpr int kAU = IC * kGmM / kGmP;           // A slots (row, input) per thread: 1 or 2
+    constexpr int kAU = IC * (DUAL ? 2 * kGmM : kGmM) / kGmP;  // A slots (row, input) per thread: 1, 2 or 4
     // F16 (int8 tables, even G, IC = 8): operands in fp16 split precision
     // (kind::f16, K = 16 per MMA: half the tensor time of 3xTF32), W scaled
     // by the layer's power of two DevLayer::wsc (folded into the gain LUT
@@ -365,9 +370,10 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     const int ring = kDense ? a.gemm_ring : 1;
     // smem: two A buffers [A_hi (| A_lo)], `wst` W stages (2 planes each),
     // then (dense) the ring slots
-    const uint32_t abuf = (STACK ? 1 : 2) * tile_a, wstage = 2 * tile_t;
+    const uint32_t abuf = (STACK ? 1 : (DUAL ? 4 : 2)) * tile_a, wstage = 2 * tile_t;
+    constexpr int kNA = DUAL ? 1 : 2;  // A buffers
     unsigned char* s_a = smem;
-    unsigned char* s_w = smem + 2 * abuf;
+    unsigned char* s_w = smem + kNA * abuf;
     unsigned char* s_ringbuf = s_w + wst * wstage;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int j0 = blockIdx.x * kGmN, s0 = blockIdx.z * S;
@@ -379,7 +385,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         if (tid < 256) s_lut[tid] = L.lutf[tid] * wsc;
     }
     // the A tiles are sparse: zero them once; each slot owner keeps them clean
-    for (uint32_t q = tid * 16; q < 2 * abuf; q += kGmT * 16)
+    for (uint32_t q = tid * 16; q < kNA * abuf; q += kGmT * 16)
         *reinterpret_cast<uint4*>(s_a + q) = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         for (int q = 0; q < 4; ++q) {
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         for (int q = 0; q < 6; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc::smem_addr(&s_ring[q])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tc::tmem_alloc<2 * kGmN>(&s_tmem);
+    if (warp == 0) tc::tmem_alloc<(DUAL ? 4 : 2) * kGmN>(&s_tmem);
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -614,24 +620,34 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         }
         // A: clear this slot's two entries of chunk c-2, write chunk c's
         if (tid == 0) gstamp(a, 0, c, 2);
-        if (c >= 2) mbar_wait_parity(&s_afree[ab], ((c >> 1) - 1) & 1);
+        if constexpr (DUAL) {
+            if (c >= 1) mbar_wait_parity(&s_afree[0], (c - 1) & 1);
+        } else if (c >= 2) {
+            mbar_wait_parity(&s_afree[ab], ((c >> 1) - 1) & 1);
+        }
         if (tid == 0) gstamp(a, 0, c, 3);
-        unsigned char* sab = s_a + ab * abuf;
+        unsigned char* sab = s_a + (DUAL ? 0 : ab) * abuf;
 #pragma unroll
         for (int u = 0; u < kAU; ++u) {
-            const int q = tid + kGmP * u, ra = q / IC, il = q % IC;
+            const int q = tid + kGmP * u, ra_ = q / IC, il = q % IC;
+            // DUAL: half ra_ / 128 has its own [A_hi | A_lo] tile pair
+            unsigned char* sab_u = DUAL ? sab + (ra_ >> 7) * 2 * tile_a : sab;
+            const int ra = DUAL ? (ra_ & 127) : ra_;
             const bool lo_row = STACK && ra >= 64;
             if constexpr (F16) {
-                // fp16 hat weights: element (r, k) at (k / 8) * LBO + row part + (k % 8) * 2
-                if (cur.aoff[u] != 0xFFFFFFFFu) {
-                    const uint32_t o0 = cur.aoff[u] & 0xFFFFu, o1 = cur.aoff[u] >> 16;
-                    *reinterpret_cast<__half*>(sab + o0) = __float2half_rn(0.f);
-                    *reinterpret_cast<__half*>(sab + o1) = __float2half_rn(0.f);
+                // fp16 hat weights: element (r, k) at (k / 8) * LBO + row part + (k % 8) * 2.
+                // DUAL has one A buffer: clear what chunk c-1 wrote (the other
+                // stage's record) instead of chunk c-2's
+                uint32_t& old = DUAL ? nxt.aoff[u] : cur.aoff[u];
+                if (old != 0xFFFFFFFFu) {
+                    const uint32_t o0 = old & 0xFFFFu, o1 = old >> 16;
+                    *reinterpret_cast<__half*>(sab_u + o0) = __float2half_rn(0.f);
+                    *reinterpret_cast<__half*>(sab_u + o1) = __float2half_rn(0.f);
                     if constexpr (!STACK) {
-                        *reinterpret_cast<__half*>(sab + tile_a + o0) = __float2half_rn(0.f);
-                        *reinterpret_cast<__half*>(sab + tile_a + o1) = __float2half_rn(0.f);
+                        *reinterpret_cast<__half*>(sab_u + tile_a + o0) = __float2half_rn(0.f);
+                        *reinterpret_cast<__half*>(sab_u + tile_a + o1) = __float2half_rn(0.f);
                     }
-                    cur.aoff[u] = 0xFFFFFFFFu;
+                    old = 0xFFFFFFFFu;
                 }
                 if (cur.bm[u] >= 0) {
                     const int k0 = cur.bm[u] * IC + il, k1 = k0 + IC;
@@ -640,11 +656,11 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                     const float w0 = 1.f - cur.bt[u], w1 = cur.bt[u];
                     const __half h0 = __float2half_rn(w0), h1 = __float2half_rn(w1);
                     const __half l0 = __float2half_rn(w0 - __half2float(h0)), l1 = __float2half_rn(w1 - __half2float(h1));
-                    *reinterpret_cast<__half*>(sab + o0) = lo_row ? l0 : h0;
-                    *reinterpret_cast<__half*>(sab + o1) = lo_row ? l1 : h1;
+                    *reinterpret_cast<__half*>(sab_u + o0) = lo_row ? l0 : h0;
+                    *reinterpret_cast<__half*>(sab_u + o1) = lo_row ? l1 : h1;
                     if constexpr (!STACK) {
-                        *reinterpret_cast<__half*>(sab + tile_a + o0) = l0;
-                        *reinterpret_cast<__half*>(sab + tile_a + o1) = l1;
+                        *reinterpret_cast<__half*>(sab_u + tile_a + o0) = l0;
+                        *reinterpret_cast<__half*>(sab_u + tile_a + o1) = l1;
                     }
                     cur.aoff[u] = o0 | (o1 << 16);
                 }
@@ -716,7 +732,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll 1
         for (int c = 0; c < nchunks; ++c) {
             if constexpr (F16) {  // K = 16 steps (two core-matrix columns), same descriptor strides
-                const int ab = c & 1;
+                const int ab = DUAL ? 0 : (c & 1);
                 mbar_wait_parity(&s_full[ws], wph);
                 tc::fence_after_sync();
                 const uint64_t da = da0 + ab * (abuf >> 4);
@@ -724,9 +740,14 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
 #pragma unroll
                 for (int s = 0; s < 8; ++s) {
                     if (s >= nks) break;
-                    tc::mma_f16_ss_warp(tmem, da + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
-                    if constexpr (!STACK)
-                        tc::mma_f16_ss_warp(tmem, da + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
+#pragma unroll
+                    for (int hf = 0; hf < (DUAL ? 2 : 1); ++hf) {  // DUAL: half hf's tiles -> accumulator hf
+                        const uint64_t dah = da + hf * ((2 * tile_a) >> 4);
+                        const uint32_t th = tmem + hf * 2 * kGmN;
+                        tc::mma_f16_ss_warp(th, dah + s * kStepA, dw + s * kStepW, idesc2, (c | s) != 0);
+                        if constexpr (!STACK)
+                            tc::mma_f16_ss_warp(th, dah + ((tile_a >> 4) + s * kStepA), dw + s * kStepW, idesc1, 1u);
+                    }
                 }
                 tc::mma_commit_warp(&s_afree[ab]);
                 tc::mma_commit_warp(&s_wfree[ws]);
@@ -777,17 +798,19 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     // STACK: lanes 64-127 (A_lo rows) go to their own partial plane, summed
     // with the A_hi plane by the split reduction.
     if (warp < kGmP / 32) {
+      for (int hf = 0; hf < (DUAL ? 2 : 1); ++hf) {  // DUAL: accumulator hf holds samples 128 hf ..
         const int q4 = warp & 3, cq = warp >> 2;
-        const int as = STACK ? (q4 & 1) * 32 + lane : q4 * 32 + lane;
+        const int as = STACK ? (q4 & 1) * 32 + lane : hf * kGmM + q4 * 32 + lane;
         const size_t plane = static_cast<size_t>(a.B) * L.out;
         const int pz = STACK ? 2 * blockIdx.y + (q4 >> 1) : blockIdx.y;
         float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
+        const uint32_t tacc = tmem + hf * 2 * kGmN;
 #pragma unroll 1
         for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
             float v[8], w[8];
             if (nchunks > 0) {
-                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
-                tc::tmem_ld8(tmem + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
+                tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+                tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
                 const float inv = F16 ? 1.0f / wsc : 1.0f;  // exact: wsc is a power of two
 #pragma unroll
                 for (int u = 0; u < 8; ++u) v[u] = (v[u] + w[u]) * inv;
@@ -806,10 +829,11 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
                 }
             }
         }
+      }
     }
     tc::fence_before_sync();
     __syncthreads();
-    if (warp == 0) tc::tmem_free<2 * kGmN>(tmem);
+    if (warp == 0) tc::tmem_free<(DUAL ? 4 : 2) * kGmN>(tmem);
 }
 
 // Pre-tiled dense grid for the layer GEMM (built at upload; the only
@@ -1742,10 +1766,21 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
         c.ic = 8;  // the same shared-memory bytes per chunk as tf32 at IC = 4
     }
     c.spt = B <= 64 ? 64 : kGmM;  // samples per tile: 64 = A_hi / A_lo stacked in the 128 rows
+    static const bool dual_off = [] {
+        const char* e = std::getenv("SKAN_GEMM_DUAL");  // A/B experiment: 0 = one CTA per 128 samples
+        return e && e[0] == '0';
+    }();
+    if (c.persist == 3 && B > kGmM && !dual_off) c.spt = 2 * kGmM;  // 256 samples per CTA, W decoded once
     const bool stack = c.spt == 64;
     c.tj = kGmN;
     GemmPlan gp{};
     gemm_plan(L.G, L.fmt, stack, &gp);
+    if (c.spt == 2 * kGmM) {  // one A buffer of two [A_hi | A_lo] pairs + two W stages
+        const size_t kc = static_cast<size_t>(gemm_ic(L.G)) * L.G;  // fp16 at IC = 8: the bytes of f32 at IC = 4
+        gp.wst = 2;
+        gp.ring = 0;
+        gp.smem = 4 * kGmM * kc * 4 + 2 * 2 * kGmN * kc * 4;
+    }
     c.vj = gp.wst;
     c.rw = gp.ring;
     c.jt = (L.out + c.tj - 1) / c.tj;
@@ -1775,8 +1810,13 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
 }
 
 template <bool STACK>
-void (*gemm_kernel(int fmt, int ic, bool f16 = false))(FwdArgs) {
+void (*gemm_kernel(int fmt, int ic, bool f16 = false, bool dual = false))(FwdArgs) {
     const bool i4 = ic == 4;
+    if constexpr (!STACK) {
+        if (f16 && dual)
+            return fmt == FMT_I8_R32 ? k_layer_gemm<FMT_I8_R32, 8, false, true, true>
+                                     : k_layer_gemm<FMT_I8_WIDE, 8, false, true, true>;
+    }
     if (f16) return fmt == FMT_I8_R32 ? k_layer_gemm<FMT_I8_R32, 8, STACK, true> : k_layer_gemm<FMT_I8_WIDE, 8, STACK, true>;
     switch (fmt) {
         case FMT_I8_R32: return i4 ? k_layer_gemm<FMT_I8_R32, 4, STACK> : k_layer_gemm<FMT_I8_R32, 8, STACK>;
@@ -1835,7 +1875,9 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     }
     const bool stack = c.spt == 64;
     const bool f16 = c.persist == 3;  // int8 layer GEMM in fp16 split precision
-    void (*k)(FwdArgs) = stack ? gemm_kernel<true>(a.L.fmt, c.ic, f16) : gemm_kernel<false>(a.L.fmt, c.ic, f16);
+    const bool dual = c.spt == 2 * kGmM;  // 256 samples per CTA (two halves share W)
+    void (*k)(FwdArgs) =
+        stack ? gemm_kernel<true>(a.L.fmt, c.ic, f16) : gemm_kernel<false>(a.L.fmt, c.ic, f16, dual);
     ensure_smem(k, c.smem);
     static const int carve_env = [] {
         const char* e = std::getenv("SKAN_GEMM_CARVEOUT");  // experiment: shared-memory carve-out percent
