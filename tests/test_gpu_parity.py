@@ -557,7 +557,12 @@ def test_hot_swap_refills_a_resident_head(torch_cuda):
     ws = hq.make_workspace(model, max_batch=8)
     x = synthetic.synthetic_inputs(3, 512, seed=4)
     want, _ = oracle.port_forward(tb, x, 3)
-    hq.swap_model(model, b)
+    ta = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(a)]
+    y1 = np.zeros(8)  # batch 1 from host buffers: builds the workspace's captured graph for head a
+    hq.compressed_forward(model, x[:512], 1, y1, ws, mode="fast")
+    wa, _ = oracle.port_forward(ta, x[:512], 1)
+    assert_close(y1, wa, l1_scale(ta, x[:512], 1))
+    hq.swap_model(model, b)  # ... which must be rebuilt for the new tables
     y = np.zeros(3 * 8)
     hq.compressed_forward(model, x, 3, y, ws, mode="exact")
     assert np.array_equal(_bits(y), _bits(want))

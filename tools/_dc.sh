@@ -1,3 +1,3 @@
-mkdir -p gpurun_out/s4x
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/s4x/pytest.log 2>&1; echo "rc $?" >> gpurun_out/s4x/pytest.log
-timeout 120 python tools/diag_configs.py > gpurun_out/s4x/configs.txt 2>&1
+mkdir -p gpurun_out/s5a
+timeout 120 python tools/gemm_check.py > gpurun_out/s5a/gc.txt 2>&1
+for rep in 1 2; do timeout 60 python tools/diag_latency.py --batches 4,64,256 --reps 100 2>&1 | grep "flush=True"; done > gpurun_out/s5a/lat.txt
