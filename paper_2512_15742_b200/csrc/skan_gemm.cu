@@ -1341,6 +1341,11 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
     };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     pdl_trigger();
+    // the ring starts zeroed: the conversion loop is branch-free and a pair's
+    // missing second tile must not hold non-finite bit patterns
+    for (uint32_t q = tid * 16; q < kD16Ring * 2 * tile_t; q += kD16T * 16)
+        *reinterpret_cast<uint4*>(s_ring + q) = make_uint4(0, 0, 0, 0);
+    tc::fence_proxy_async();  // ordered before the TMA writes into the same ring
     if (tid == 0) {
         for (int q = 0; q < kD16Ring; ++q) mbar_init(&s_tfull[q], 1);
         for (int q = 0; q < kDnQ; ++q) {
@@ -1565,20 +1570,22 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
                 const int g = q >> 7, rr = q & 127;
                 const int k = KC * hsel + 4 * g;
                 const uint32_t o = (k >> 3) * kLbo + (rr >> 3) * 128 + (rr & 7) * 16 + (k & 7) * 2;
-                uint2 hi = make_uint2(0, 0), lo = make_uint2(0, 0);
-                if (hsel < nt) {
-                    // packed: f32x2 scale, two-at-a-time fp16 rounding, f32x2 remainder
-                    const float4 w = src[qq];
-                    const float2 sc = make_float2(wsc, wsc), neg = make_float2(-1.f, -1.f);
-                    const float2 a2 = __fmul2_rn(make_float2(w.x, w.y), sc), b2 = __fmul2_rn(make_float2(w.z, w.w), sc);
-                    const __half2 ha = __float22half2_rn(a2), hb = __float22half2_rn(b2);
-                    const __half2 la = __float22half2_rn(__ffma2_rn(__half22float2(ha), neg, a2));
-                    const __half2 lb = __float22half2_rn(__ffma2_rn(__half22float2(hb), neg, b2));
-                    hi = make_uint2(*reinterpret_cast<const uint32_t*>(&ha), *reinterpret_cast<const uint32_t*>(&hb));
-                    lo = make_uint2(*reinterpret_cast<const uint32_t*>(&la), *reinterpret_cast<const uint32_t*>(&lb));
-                }
-                *reinterpret_cast<uint2*>(stg + o) = hi;
-                *reinterpret_cast<uint2*>(stg + half_t + o) = lo;
+                // branch-free (the ring was zeroed at kernel start, so a pair's
+                // missing second tile converts finite stale data or zeros, and
+                // its A columns are zero): the unrolled iterations' independent
+                // chains overlap.  Packed: f32x2 scale, two-at-a-time fp16
+                // rounding, f32x2 remainder.
+                (void)nt;
+                const float4 w = src[qq];
+                const float2 sc = make_float2(wsc, wsc), neg = make_float2(-1.f, -1.f);
+                const float2 a2 = __fmul2_rn(make_float2(w.x, w.y), sc), b2 = __fmul2_rn(make_float2(w.z, w.w), sc);
+                const __half2 ha = __float22half2_rn(a2), hb = __float22half2_rn(b2);
+                const __half2 la = __float22half2_rn(__ffma2_rn(__half22float2(ha), neg, a2));
+                const __half2 lb = __float22half2_rn(__ffma2_rn(__half22float2(hb), neg, b2));
+                *reinterpret_cast<uint2*>(stg + o) =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&ha), *reinterpret_cast<const uint32_t*>(&hb));
+                *reinterpret_cast<uint2*>(stg + half_t + o) =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&la), *reinterpret_cast<const uint32_t*>(&lb));
             }
             tc::fence_proxy_async();
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
