@@ -850,8 +850,7 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
         a.bt_out = bt[(l + 1) & 1];
     }
     a.err = d.err;
-    skan::launch_fwd_fast(a, c, chained, s);
-    return launches + (c.kind == 4 ? 2 : 1);  // the tensor-core GEMM is followed by its split reduction
+    return launches + skan::launch_fwd_fast(a, c, chained, s);  // the GEMM's split reduction counted inside
 }
 
 // Enqueue one chunk (B <= ws->max_batch) on `s`; x/y are device pointers.

@@ -906,6 +906,20 @@ __host__ __device__ __forceinline__ long long dn_start(int c, long long T, int P
 __host__ __device__ __forceinline__ int dn_owner(long long x, long long T, int P) {
     return static_cast<int>(((x + 1) * P - 1) / T);
 }
+// With fewer units than CTAs some ranges are empty: a tile's segments are
+// numbered densely over the NON-empty CTAs.  dn_rank = how many non-empty
+// CTAs lie in [f, c) (c - f when every CTA has work).
+__host__ __device__ __forceinline__ int dn_rank(long long T, int P, int f, int c) {
+    if (T >= P) return c - f;
+    int r = 0;
+    for (int q = f; q < c; ++q) r += dn_start(q + 1, T, P) > dn_start(q, T, P);
+    return r;
+}
+// segments of tile jt (units per tile u)
+__host__ __device__ __forceinline__ int dn_nseg(int jt, int u, long long T, int P) {
+    const int f = dn_owner(static_cast<long long>(jt) * u, T, P);
+    return dn_rank(T, P, f, dn_owner(static_cast<long long>(jt + 1) * u - 1, T, P) + 1);
+}
 
 // debug stamps (skan_debug_gemm_timeline): CTA 0 of a wide layer, 4 roles
 // x chunk u < 64 x phase < 8
@@ -1168,7 +1182,7 @@ __global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
             // seg' = this CTA's index among the tile's CTAs
             mbar_wait_parity(&s_accfull[seg % kDnSeg], (seg / kDnSeg) & 1);
             tc::fence_after_sync();
-            const int segi = c - dn_owner(static_cast<long long>(jt_u) * nch, T, P);
+            const int segi = dn_rank(T, P, dn_owner(static_cast<long long>(jt_u) * nch, T, P), c);
             const int as = (q4 & 1) * 32 + lane;
             const int j0 = jt_u * kGmN, nJ = min(kGmN, L.out - j0);
             const size_t plane = static_cast<size_t>(a.B) * L.out;
@@ -1516,7 +1530,7 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
             if (!last) continue;
             mbar_wait_parity(&s_accfull[seg % kDnSeg], (seg / kDnSeg) & 1);
             tc::fence_after_sync();
-            const int segi = c - dn_owner(static_cast<long long>(jt_u) * nch2, T, P);
+            const int segi = dn_rank(T, P, dn_owner(static_cast<long long>(jt_u) * nch2, T, P), c);
             const int as = (q4 & 1) * 32 + lane;
             const int j0 = jt_u * kGmN, nJ = min(kGmN, L.out - j0);
             const size_t plane = static_cast<size_t>(a.B) * L.out;
@@ -1598,6 +1612,10 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+void (*k_dense_persist16_ptr(int G))(FwdArgs, int) {
+    return G == 10 ? k_dense_persist16<40> : (G == 8 ? k_dense_persist16<32> : k_dense_persist16<24>);
+}
+
 // Persistent dense layer: output j of tile jt has 2 * (CTAs holding part of
 // the tile) planes, summed in ascending order in f64.
 __global__ void k_dense_reduce(FwdArgs a, int nch, int P) {
@@ -1609,8 +1627,7 @@ __global__ void k_dense_reduce(FwdArgs a, int nch, int P) {
     for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int jt = static_cast<int>(p % a.L.out) / kGmN;
-        const int nz = 2 * (dn_owner(static_cast<long long>(jt + 1) * nch - 1, T, P) -
-                            dn_owner(static_cast<long long>(jt) * nch, T, P) + 1);
+        const int nz = 2 * dn_nseg(jt, nch, T, P);
         double v = 0.0;
         for (int z = 0; z < nz; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
         reduce_finish(a, p, v, 0);
@@ -1629,8 +1646,7 @@ __global__ void k_dense_reduce_warp(FwdArgs a, int nch, int P) {
     for (size_t p = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / 32; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
         const int jt = static_cast<int>(p % a.L.out) / kGmN;
-        const int nz = 2 * (dn_owner(static_cast<long long>(jt + 1) * nch - 1, T, P) -
-                            dn_owner(static_cast<long long>(jt) * nch, T, P) + 1);
+        const int nz = 2 * dn_nseg(jt, nch, T, P);
         double v = 0.0;
         for (int z = lane; z < nz; z += 32) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
 #pragma unroll
@@ -1756,11 +1772,10 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
         const int units = c.persist == 2 ? d16_nch2(c.dn_nch) : c.dn_nch;  // schedule units per tile
         const long long T = static_cast<long long>(ntile) * units;
         c.jt = sms;  // grid
-        c.st = 1;
+        c.st = (ntile + sms - 1) / sms;  // so that jt * st >= ntile: the per-tile arrival counters fit
         int maxseg = 1;
         for (int jt = 0; jt < ntile; ++jt)
-            maxseg = std::max(maxseg, dn_owner(static_cast<long long>(jt + 1) * units - 1, T, sms) -
-                                          dn_owner(static_cast<long long>(jt) * units, T, sms) + 1);
+            maxseg = std::max(maxseg, dn_nseg(jt, units, T, sms));
         c.nsplit = 2 * maxseg;
         c.ichunk = L.in;
         c.smem = c.persist == 2 ? dense_f16_smem(L.G) : dense_persist_smem(L.G);
@@ -1847,7 +1862,7 @@ double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B) {
 unsigned long long* g_gemm_dbg = nullptr;
 int g_gemm_min_batch = kGemmMinBatch;
 
-void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce) {
+int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce) {
     FwdArgs a = a0;
     a.dbg = g_gemm_dbg;
     a.gemm_wst = c.vj;
@@ -1864,11 +1879,18 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         }();
         a.gemm_ring = dist_env;
         void (*kp)(FwdArgs, int) = c.ic == 4 ? k_dense_persist<4> : k_dense_persist<8>;
-        if (c.persist == 2)
-            kp = a.L.G == 10 ? k_dense_persist16<40> : (a.L.G == 8 ? k_dense_persist16<32> : k_dense_persist16<24>);
-        ensure_smem(kp, c.smem);
-        launch_pdl(kp, dim3(c.jt), dim3(c.persist == 2 ? kD16T : kDnT), c.smem, pdl, s, a, c.dn_nch);
-        if (!with_reduce) return;
+        if (c.persist == 2) ensure_smem(k_dense_persist16_ptr(a.L.G), c.smem);
+        else ensure_smem(kp, c.smem);
+        // (fusing the reduction into the kernel — the CTA that drains a
+        // tile's last segment reduces it — measured slower: 311 -> 421 us at
+        // cfg4, the reducing CTA's stream stalls behind ~8k outputs)
+        if (c.persist == 2) {
+            launch_pdl(k_dense_persist16_ptr(a.L.G), dim3(c.jt), dim3(kD16T), c.smem, pdl, s, a, c.dn_nch);
+            if (!with_reduce) return 1;
+        } else {
+            launch_pdl(kp, dim3(c.jt), dim3(kDnT), c.smem, pdl, s, a, c.dn_nch);
+            if (!with_reduce) return 1;
+        }
         const int units = c.persist == 2 ? d16_nch2(c.dn_nch) : c.dn_nch;  // the reduction's schedule unit
         const long long n = static_cast<long long>(a.B) * a.L.out;
         if (c.nsplit >= 32) {
@@ -1878,7 +1900,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
             const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
             launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         }
-        return;
+        return 2;
     }
     const bool stack = c.spt == 64;
     const bool f16 = c.persist == 3;  // int8 layer GEMM in fp16 split precision
@@ -1893,7 +1915,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
     if (carve_env >= 0) cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve_env);
     const int splits = (a.L.in + c.ichunk - 1) / c.ichunk;
     launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
-    if (!with_reduce) return;
+    if (!with_reduce) return 1;
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
@@ -1903,6 +1925,7 @@ void launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStre
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
         launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
     }
+    return 2;
 }
 
 // Dense layers the GEMM takes keep their grid ONLY in its pre-tiled layout

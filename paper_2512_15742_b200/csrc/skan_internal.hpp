@@ -232,7 +232,7 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
 // Fused fast-path layer (gather + split reduction + next-layer locate).
 // pdl: launch with programmatic stream serialization (overlaps the
 // prologue with the previous kernel's tail).
-void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);
+int launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);  // returns the launches made
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
                          const double* btd, double* y, cudaStream_t s);
 void launch_locate_raw(const double* x, int n, double lo, double hi, int G, int* idx,
@@ -255,7 +255,7 @@ int gemm_ic(int G);
 uint64_t dense_tile_floats(int in, int out, int G);
 void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s);
 float dense_fp16_scale(const float* wt, uint64_t n, cudaStream_t s);
-void launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce = true);
+int launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce = true);
 // MMA work one k_layer_gemm launch issues (flops, as 2*M*N*K per tcgen05.mma)
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B);
 

@@ -1135,11 +1135,8 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
     k_locate_input<<<grid_for(n, 256), 256, 0, s>>>(x, n, L, bm, btf, btd, err, width, input_major ? n_rows : 0);
 }
 
-void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
-    if (c.kind == 4) {
-        launch_layer_gemm(a, c, pdl, s);
-        return;
-    }
+int launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    if (c.kind == 4) return launch_layer_gemm(a, c, pdl, s);
     if (c.kind == 2) {
         void (*k)(FwdArgs);
         switch (c.vj) {
@@ -1150,14 +1147,14 @@ void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_
         }
         ensure_smem(k, c.smem);
         launch_ex(k, dim3(c.nsplit), dim3(256), c.smem, pdl, s, a);
-        return;
+        return 1;
     }
     if (c.kind == 1) {
         void (*k)(FwdArgs) = a.L.fmt == FMT_I8_R32 ? large_kernel<FMT_I8_R32>(a.L.G, c.vj, c.spt)
                                                     : large_kernel<FMT_I8_WIDE>(a.L.G, c.vj, c.spt);
         ensure_smem(k, c.smem);
         launch_ex(k, dim3(c.jt, c.nsplit, c.st), dim3(256), c.smem, pdl, s, a);
-        return;
+        return 1;
     }
     switch (a.L.fmt) {
         case FMT_I8_R32:
@@ -1168,6 +1165,7 @@ void launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_
         case FMT_F32: dispatch_small_s<FMT_F32, 1>(a, c, pdl, s); break;
         default: dispatch_small_s<FMT_DENSE, 1>(a, c, pdl, s); break;
     }
+    return 1;
 }
 
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
