@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "skan_device.cuh"
 #include "skan_internal.hpp"
@@ -1077,7 +1078,11 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         c.ichunk = L.in;
         return c;
     }
-    if (B >= g_gemm_min_batch && L.out >= 16 && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
+    static const int gemm_min_out = [] {
+        const char* e = std::getenv("SKAN_GEMM_MIN_OUT");  // experiment: narrowest layer routed to the GEMM
+        return e ? std::atoi(e) : 16;
+    }();
+    if (B >= g_gemm_min_batch && L.out >= gemm_min_out && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {
         // samples in lanes: tile 128 samples x (32 or 64) outputs x split of the rows
