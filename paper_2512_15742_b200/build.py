@@ -60,7 +60,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         list(ex.map(compile_one, SOURCES))
-    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp", *[_obj(s) for s in SOURCES]]
+    cmd = [NVCC, *ARCH, "-shared", "-Xlinker", "--no-undefined", "-o", OUT + ".tmp", *[_obj(s) for s in SOURCES]]
     subprocess.run(cmd, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT

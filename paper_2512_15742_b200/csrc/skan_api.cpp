@@ -267,6 +267,9 @@ struct skan_workspace {
     uint64_t b1_graph_gen = 0;       // skan_head::gen the graph was built for
     bool b1_graph_failed = false;    // capture unsupported: keep the copy + launch path
     unsigned long long* b1_timeline = nullptr;  // optional phase stamps (profiling hook)
+    double* ex_terms = nullptr;      // exact mode, batch <= kExactSplitMaxBatch: the per-edge terms
+    size_t ex_doubles = 0;           // ... its size (>= one input's terms for the workspace's batch)
+    double* ex_acc = nullptr;        // ... and the running in-order sums [kExactSplitMaxBatch * width]
     // Fast-path launch plans for every batch 1..max_batch, [B-1][layer],
     // built at creation (forward allocates nothing); rebuilt in place if the
     // GEMM routing threshold changes (skan_debug_set_gemm_min_batch).
@@ -852,6 +855,16 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
     a.err = d.err;
     return launches + skan::launch_fwd_fast(a, c, chained, s);  // the GEMM's split reduction counted inside
 }
+// batches at or below this take the two-pass exact path (SKAN_EXACT_SPLIT_MAX
+// overrides it, for measurement; 0 = always the one-pass kernel)
+static int exact_split_max() {
+    static const int v = [] {
+        const char* e = std::getenv("SKAN_EXACT_SPLIT_MAX");
+        return e ? std::atoi(e) : skan::kExactSplitMaxBatch;
+    }();
+    return std::min(v, skan::kExactSplitMaxBatch);
+}
+
 
 // Enqueue one chunk (B <= ws->max_batch) on `s`; x/y are device pointers.
 //   fast:  [locate] -> fused layer 0 -> fused layer 1 -> ...  (PDL-chained;
@@ -869,9 +882,14 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
             const DevLayer& L = h->dl[l];
             const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
             double* out = next ? d.act[l & 1] : y;
-            const skan::LaunchCfg c = skan::choose_cfg(L, B, true, h->num_sms);
-            skan::launch_gather_exact(L, c, B, d.bm, d.btd, out, s);
-            ++launches;
+            if (B <= exact_split_max() && ws->ex_terms) {
+                launches += skan::launch_exact_split(L, B, d.bm, d.btd, out, ws->ex_terms, ws->ex_doubles,
+                                                     ws->ex_acc, s);
+            } else {
+                const skan::LaunchCfg c = skan::choose_cfg(L, B, true, h->num_sms);
+                skan::launch_gather_exact(L, c, B, d.bm, d.btd, out, s);
+                ++launches;
+            }
             if (next) {
                 skan::launch_locate_input(out, B, L.out, *next, d.bm, d.btf, d.btd, d.err, s);
                 ++launches;
@@ -1173,6 +1191,14 @@ skan_status skan_workspace_create(const skan_head* h, int max_batch, skan_worksp
                              "cudaHostAlloc");
             skan::cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->pin_out_d), ws->pin_out, 0),
                              "cudaHostGetDevicePointer");
+        }
+        {  // exact-mode scratch: the largest layer's terms at this workspace's batch, capped
+            const size_t bx = static_cast<size_t>(std::min<uint32_t>(max_batch, skan::kExactSplitMaxBatch));
+            size_t need = 0;
+            for (const auto& L : h->dl) need = std::max(need, bx * ((L.out + 31) / 32 * 32) * L.in);
+            ws->ex_doubles = std::min(need, skan::kExactTermBytes / sizeof(double));
+            ws->ex_terms = static_cast<double*>(alloc(ws->ex_doubles * sizeof(double)));
+            ws->ex_acc = static_cast<double*>(alloc(bx * ws->width * 8));
         }
         ws->xin = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->in_dim * 8));
         ws->yout = static_cast<double*>(alloc(static_cast<size_t>(max_batch) * h->out_dim * 8));

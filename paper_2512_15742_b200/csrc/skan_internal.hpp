@@ -235,6 +235,14 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
 int launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);  // returns the launches made
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
                          const double* btd, double* y, cudaStream_t s);
+// Exact mode at small batch: terms in parallel into `terms` (term_doubles of
+// scratch; blocks of inputs when it does not hold a whole layer), then the
+// in-order sums per (sample, output), carried in `acc` [B * out].  Returns the
+// launches made.
+constexpr int kExactSplitMaxBatch = 128;
+constexpr size_t kExactTermBytes = 256ull << 20;
+int launch_exact_split(const DevLayer& L, int B, const int* bm, const double* btd, double* y, double* terms,
+                       size_t term_doubles, double* acc, cudaStream_t s);
 void launch_locate_raw(const double* x, int n, double lo, double hi, int G, int* idx,
                        double* t, uint8_t* clamped, int* err, cudaStream_t s);
 void launch_pli_lookup(const double* cb, int k, int G, const int* rows, const double* g,

@@ -898,6 +898,159 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// Exact mode at small batch, in two passes.  k_gather_exact gives each
+// (sample, output) one thread that walks the inputs in order: at batch 1 that
+// is ~1.4k threads chasing dependent record -> codebook loads, far below the
+// machine.  Bitwise equality only needs each output's SUM in input order, so:
+//   k_exact_terms: every (input, output, sample) term in parallel, with
+//     exactly k_gather_exact's operations (lutham.cpp:810, no contraction),
+//     for a block of inputs, into a scratch buffer;
+//   k_exact_sum:   per (sample, output), acc = acc + term in input order over
+//     the block (coalesced across outputs), acc carried across blocks.
+template <int FMT>
+__global__ void __launch_bounds__(256) k_exact_terms(DevLayer L, int B, const int* __restrict__ bm,
+                                                     const double* __restrict__ btd, int i0, int ni,
+                                                     double* __restrict__ terms) {
+    // one thread per (sample group of kExS, input, output): the record is
+    // loaded once per group, the groups re-read it from L2
+    constexpr int kExS = 4;
+    const int ng = (B + kExS - 1) / kExS, njb = (L.out + 31) >> 5;
+    const size_t n = static_cast<size_t>(ni) * L.out, nt = n * ng;
+    for (size_t qq = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; qq < nt;
+         qq += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int sg = static_cast<int>(qq / n);
+        const size_t q = qq - static_cast<size_t>(sg) * n;
+        const int il = static_cast<int>(q / L.out), j = static_cast<int>(q - static_cast<size_t>(il) * L.out);
+        const int i = i0 + il;
+        Edge<FMT> ed;
+        ed.load(L, static_cast<size_t>(i) * L.out + j);
+        double g = 0.0, b = 0.0;
+        if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
+            g = __ldg(L.lutd + ed.gcode());
+            b = __dmul_rn(static_cast<double>(ed.bcode()), L.bs);
+        }
+        if constexpr (FMT == FMT_F32) {
+            g = static_cast<double>(ed.g);
+            b = static_cast<double>(ed.b);
+        }
+        const int s1 = min(B, (sg + 1) * kExS);
+        for (int sm = sg * kExS; sm < s1; ++sm) {
+            const int m = __ldg(bm + static_cast<size_t>(sm) * L.in + i);
+            const double t = __ldg(btd + static_cast<size_t>(sm) * L.in + i);
+            const double w0 = __dsub_rn(1.0, t);
+            double c0, c1, term;
+            if constexpr (FMT == FMT_I8_R32 || FMT == FMT_I8_WIDE) {
+                c0 = __dmul_rn(static_cast<double>(__ldg(ed.row + m)), L.cs);
+                c1 = __dmul_rn(static_cast<double>(__ldg(ed.row + m + 1)), L.cs);
+            } else if constexpr (FMT == FMT_DENSE) {
+                c0 = static_cast<double>(dense_at(L, ed.i, ed.j, m));
+                c1 = static_cast<double>(dense_at(L, ed.i, ed.j, m + 1));
+            } else {
+                c0 = static_cast<double>(__ldg(ed.row + m));
+                c1 = static_cast<double>(__ldg(ed.row + m + 1));
+            }
+            if constexpr (FMT == FMT_DENSE) {
+                term = __dadd_rn(__dmul_rn(c0, w0), __dmul_rn(c1, t));
+            } else {
+                term = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(g, c0), b), w0),
+                                 __dmul_rn(__dadd_rn(__dmul_rn(g, c1), b), t));
+            }
+            // [sample][output block of 32][input][32]: a sum block's chunk of
+            // inputs is one contiguous run for a bulk copy
+            terms[((static_cast<size_t>(sm) * njb + (j >> 5)) * ni + il) * 32 + (j & 31)] = term;
+        }
+    }
+}
+
+// Each (sample, output) chain is a strictly ordered run of dependent adds (a
+// dependent DADD is ~8 clocks, tools/micro/dadd_lat.cu), and at small batch
+// there are few chains, so the terms must stream in far ahead of the adds.
+// One warp per (sample, block of 32 outputs); its chunks of kExKc inputs x 32
+// outputs are contiguous 8 KB runs, so lane 0 keeps kExSt of them in flight
+// with TMA bulk copies on per-stage mbarriers, and each lane adds its column
+// from shared memory.  With 16 stages one warp has ~128 KB in flight.
+constexpr int kExKc = 32;
+
+template <int kExSt>
+__global__ void __launch_bounds__(32) k_exact_sum(int out, int ni, const double* __restrict__ terms,
+                                                  double* __restrict__ acc, double* __restrict__ y, int first,
+                                                  int last) {
+    extern __shared__ __align__(128) double sbuf[];  // [kExSt][kExKc][32]
+    __shared__ __align__(8) uint64_t bar[kExSt];
+    const int lane = threadIdx.x;
+    const int njb = (out + 31) >> 5;
+    const int sm = blockIdx.x / njb, j = (blockIdx.x - sm * njb) * 32 + lane;
+    const bool act = j < out;
+    const double* tb = terms + static_cast<size_t>(blockIdx.x) * ni * 32;
+    const int nch = (ni + kExKc - 1) / kExKc;
+    auto issue = [&](int c) {
+        if (lane == 0 && c < nch) {
+            const int st = c % kExSt;
+            const uint32_t bytes = static_cast<uint32_t>(min(kExKc, ni - c * kExKc)) * 32u * 8u;
+            dev::mbar_expect_tx(&bar[st], bytes);
+            dev::bulk_g2s(sbuf + static_cast<size_t>(st) * kExKc * 32, tb + static_cast<size_t>(c) * kExKc * 32,
+                          bytes, &bar[st]);
+        }
+    };
+    if (lane == 0) {
+#pragma unroll
+        for (int st = 0; st < kExSt; ++st) dev::mbar_init(&bar[st], 1);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < kExSt; ++c) issue(c);
+    const size_t q = static_cast<size_t>(sm) * out + j;
+    double a = (act && !first) ? acc[q] : 0.0;  // the reference's y starts at 0.0 (0.0 + -0.0 = +0.0 matters)
+    for (int c = 0; c < nch; ++c) {
+        const int st = c % kExSt;
+        dev::mbar_wait(&bar[st], static_cast<unsigned>(c / kExSt) & 1u);
+        const double* src = sbuf + static_cast<size_t>(st) * kExKc * 32 + lane;
+        const int rn = min(kExKc, ni - c * kExKc);
+        if (rn == kExKc) {
+#pragma unroll
+            for (int r = 0; r < kExKc; ++r) a = __dadd_rn(a, src[r * 32]);
+        } else {
+            for (int r = 0; r < rn; ++r) a = __dadd_rn(a, src[r * 32]);
+        }
+        __syncwarp();      // every lane is done with this stage ...
+        issue(c + kExSt);  // ... before it is refilled
+    }
+    if (!act) return;
+    if (last) y[q] = a;
+    else acc[q] = a;
+}
+
+template <int FMT>
+int dispatch_exact_split(const DevLayer& L, int B, const int* bm, const double* btd, double* y, double* terms,
+                         size_t term_doubles, double* acc, cudaStream_t s) {
+    const size_t outp = static_cast<size_t>((L.out + 31) / 32) * 32;  // the blocked term layout pads outputs
+    const int per = static_cast<int>(std::max<size_t>(1, term_doubles / (static_cast<size_t>(B) * outp)));
+    int launches = 0;
+    for (int i0 = 0; i0 < L.in; i0 += per) {
+        const int ni = std::min(per, L.in - i0);
+        const size_t n = static_cast<size_t>(ni) * L.out * ((B + 3) / 4);
+        const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 16));
+        k_exact_terms<FMT><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L, B, bm, btd, i0, ni, terms);
+        const int nb = B * ((L.out + 31) / 32), f = i0 == 0 ? 1 : 0, la = i0 + ni >= L.in ? 1 : 0;
+        static const bool attr = [] {  // 128 KB of dynamic shared memory (opt-in above 48 KB)
+            return cudaFuncSetAttribute(k_exact_sum<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        16 * kExKc * 32 * 8) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        4 * kExKc * 32 * 8) == cudaSuccess;
+        }();
+        (void)attr;
+        if (nb <= 2 * 148) {
+            k_exact_sum<16><<<nb, 32, 16 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
+        } else {
+            k_exact_sum<4><<<nb, 32, 4 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
+        }
+        launches += 2;
+    }
+    return launches;
+}
+
+
+// ---------------------------------------------------------------------------
 
 __global__ void k_locate_raw(const double* __restrict__ x, int n, double lo, double hi, int G,
                              double dx, int* __restrict__ idx, double* __restrict__ t,
@@ -1171,6 +1324,16 @@ int launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t
         default: dispatch_small_s<FMT_DENSE, 1>(a, c, pdl, s); break;
     }
     return 1;
+}
+
+int launch_exact_split(const DevLayer& L, int B, const int* bm, const double* btd, double* y, double* terms,
+                       size_t term_doubles, double* acc, cudaStream_t s) {
+    switch (L.fmt) {
+        case FMT_I8_R32: return dispatch_exact_split<FMT_I8_R32>(L, B, bm, btd, y, terms, term_doubles, acc, s);
+        case FMT_I8_WIDE: return dispatch_exact_split<FMT_I8_WIDE>(L, B, bm, btd, y, terms, term_doubles, acc, s);
+        case FMT_F32: return dispatch_exact_split<FMT_F32>(L, B, bm, btd, y, terms, term_doubles, acc, s);
+        default: return dispatch_exact_split<FMT_DENSE>(L, B, bm, btd, y, terms, term_doubles, acc, s);
+    }
 }
 
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,

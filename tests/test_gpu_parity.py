@@ -142,6 +142,20 @@ def test_exact_mode_headline_head_bitwise(torch_cuda):
     assert ws.interp_ops == ops == 2 * 2_911_744
 
 
+@pytest.mark.parametrize("batch", [12, 130])
+def test_exact_mode_headline_head_split_and_one_pass(torch_cuda, batch):
+    """Exact mode's two kernels: batch 12 takes the two-pass split (terms, then
+    in-order sums) with layer 0 in two input blocks (12 * 1408 * 2048 doubles
+    exceed the 256 MB term buffer), batch 130 the one-pass kernel
+    (> kExactSplitMaxBatch).  Both bitwise equal to the reference."""
+    cn = synthetic.synthetic_head()
+    tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
+    x = synthetic.synthetic_inputs(batch, 2048, seed=batch)
+    want, _ = oracle.port_forward(tables, x, batch)
+    got, _ = _gpu_forward(hq.build_model(cn), x, batch, "exact")
+    assert np.array_equal(_bits(got), _bits(want))
+
+
 # ---------------------------------------------------------------------------
 # forward, fast mode within tolerance
 
