@@ -109,7 +109,9 @@ int device_format(const skan_layer_header& h) {
 // grid pre-tiled in its shared-memory layout (DevLayer::wt): the GEMM then
 // streams each chunk with one TMA bulk copy.  Built on the device at upload.
 bool dense_tiled(const skan_layer_header& h) {
-    return h.k == 0 && h.out_dim >= 16 && h.grid_size >= 2 && h.grid_size <= 16 &&
+    // (out <= 32: a 128-output tile would be mostly padding; those layers keep
+    // the natural layout for the CUDA-core narrow kernel, LaunchCfg kind 5)
+    return h.k == 0 && h.out_dim > 32 && h.grid_size >= 2 && h.grid_size <= 16 &&
            skan::gemm_ic(static_cast<int>(h.grid_size)) * static_cast<int>(h.grid_size) <= 88;
 }
 

@@ -896,6 +896,7 @@ constexpr int kDnRing = 7;
 constexpr int kDnLo = 3;
 constexpr int kDnA = 4;    // TMEM A buffers (columns kDnAcol + 64 * b)
 constexpr int kDnQ = 8;    // full / done barrier slots (> kDnRing: the TMA warp runs kDnRing chunks ahead)
+constexpr int kDnTileTab = 512;  // k_dense_reduce: output tiles whose segment counts are tabulated
 constexpr int kDnSeg = 8;  // accumulator-complete barriers (> segments an A set can run ahead: kDnA + 1)
 constexpr int kDnBr = 8;   // bracket slots (>= kDnRing + 1)
 constexpr int kDnT = kGmP + 64;       // A + lo warps, MMA warp, TMA warp
@@ -1243,6 +1244,24 @@ __global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
+// sum of partial planes z = z0, z0 + dz, ... < nz in that order (f64), up to
+// eight loads in flight (guarded, so short sums get them too): the adds are
+// ordered, the loads need not be
+__device__ __forceinline__ double ordered_plane_sum(const float* __restrict__ base, size_t plane, int z0, int dz,
+                                                    int nz) {
+    double v = 0.0;
+    for (int z = z0; z < nz; z += 8 * dz) {
+        float f[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            f[u] = z + u * dz < nz ? __ldcg(base + static_cast<size_t>(z + u * dz) * plane) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (z + u * dz < nz) v += static_cast<double>(f[u]);
+    }
+    return v;
+}
+
 __device__ __forceinline__ void reduce_finish(const FwdArgs& a, size_t p, double v, int add_bias) {
     const DevLayer& L = a.L;
     const int j = static_cast<int>(p % L.out);
@@ -1267,17 +1286,7 @@ __global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
     const size_t plane = static_cast<size_t>(a.B) * a.L.out;
     for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        double v = 0.0;
-        int z = 0;
-        for (; z + 4 <= nsplit; z += 4) {  // four loads in flight, summed in split order
-            float f[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) f[u] = __ldcg(a.partial + (z + u) * plane + p);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
-        }
-        for (; z < nsplit; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
-        reduce_finish(a, p, v, add_bias);
+        reduce_finish(a, p, ordered_plane_sum(a.partial + p, plane, 0, 1, nsplit), add_bias);
     }
 }
 
@@ -1290,8 +1299,7 @@ __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
     const int lane = threadIdx.x & 31;
     for (size_t p = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / 32; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
-        double v = 0.0;
-        for (int z = lane; z < nsplit; z += 32) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+        double v = ordered_plane_sum(a.partial + p, plane, lane, 32, nsplit);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) reduce_finish(a, p, v, add_bias);
@@ -1619,18 +1627,19 @@ void (*k_dense_persist16_ptr(int G))(FwdArgs, int) {
 // Persistent dense layer: output j of tile jt has 2 * (CTAs holding part of
 // the tile) planes, summed in ascending order in f64.
 __global__ void k_dense_reduce(FwdArgs a, int nch, int P) {
+    __shared__ int s_nz[kDnTileTab];  // planes per output tile (two per segment)
+    const int ntile = (a.L.out + kGmN - 1) / kGmN;
+    const long long T = static_cast<long long>(ntile) * nch;
+    for (int jt = threadIdx.x; jt < min(ntile, kDnTileTab); jt += blockDim.x) s_nz[jt] = 2 * dn_nseg(jt, nch, T, P);
+    __syncthreads();
     pdl_trigger();
     pdl_wait();
     const size_t plane = static_cast<size_t>(a.B) * a.L.out;
-    const int ntile = (a.L.out + kGmN - 1) / kGmN;
-    const long long T = static_cast<long long>(ntile) * nch;
     for (size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; p < plane;
          p += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int jt = static_cast<int>(p % a.L.out) / kGmN;
-        const int nz = 2 * dn_nseg(jt, nch, T, P);
-        double v = 0.0;
-        for (int z = 0; z < nz; ++z) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
-        reduce_finish(a, p, v, 0);
+        const int nz = jt < kDnTileTab ? s_nz[jt] : 2 * dn_nseg(jt, nch, T, P);
+        reduce_finish(a, p, ordered_plane_sum(a.partial + p, plane, 0, 1, nz), 0);
     }
 }
 
@@ -1647,11 +1656,93 @@ __global__ void k_dense_reduce_warp(FwdArgs a, int nch, int P) {
          p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
         const int jt = static_cast<int>(p % a.L.out) / kGmN;
         const int nz = 2 * dn_nseg(jt, nch, T, P);
-        double v = 0.0;
-        for (int z = lane; z < nz; z += 32) v += static_cast<double>(__ldcg(a.partial + z * plane + p));
+        double v = ordered_plane_sum(a.partial + p, plane, lane, 32, nz);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         if (lane == 0) reduce_finish(a, p, v, 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Narrow dense layers (out <= 32, e.g. cfg4's 13664 -> 20 tail) at batch >= 3.
+// A 128-output tensor-core tile would be 84% padding here (6.4x the grid's
+// bytes streamed for a 20-wide layer), so the layer keeps its natural
+// [in][out][G] grid and runs on the CUDA cores: CTA z owns a contiguous block
+// of rows, stages their grid slice (one contiguous run: issued BEFORE the
+// programmatic wait, so it streams while the previous kernel drains) and
+// their brackets in shared memory, and each thread accumulates (sample,
+// output) pairs over the rows in ascending order into split partials
+// [z][B][out]; k_split_reduce(_warp) sums the splits in order in f64.
+constexpr int kNarrowT = 256;
+
+// n 4-byte words global -> shared by all threads, eight loads in flight each
+__device__ __forceinline__ void stage_words(uint32_t* dst, const uint32_t* __restrict__ src, size_t n, int tid) {
+    size_t e = tid;
+    for (; e + 7 * kNarrowT < n; e += 8 * kNarrowT) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + e + u * kNarrowT);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dst[e + u * kNarrowT] = v[u];
+    }
+    for (; e < n; e += kNarrowT) dst[e] = __ldcg(src + e);
+}
+__device__ __forceinline__ bool bulk_ok(const void* p, size_t bytes) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (bytes & 15) == 0 && bytes > 0 && bytes < (1u << 20);
+}
+
+__global__ void __launch_bounds__(kNarrowT) k_dense_narrow(FwdArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar[2];  // [0] grid slice, [1] brackets
+    const DevLayer& L = a.L;
+    const int B = a.B, out = L.out, G = L.G;
+    const int i0 = blockIdx.x * a.rows_per_cta, nr = min(a.rows_per_cta, L.in - i0);
+    const int tid = threadIdx.x;
+    float* s_grid = reinterpret_cast<float*>(smem);  // [nr][out][G]
+    const size_t gfl = static_cast<size_t>(nr) * out * G;
+    int* s_bm = reinterpret_cast<int*>(smem + ((gfl * 4 + 15) & ~static_cast<size_t>(15)));  // [nr][B]
+    const size_t nb = static_cast<size_t>(nr) * B, boff = static_cast<size_t>(i0) * B;
+    float* s_bt = reinterpret_cast<float*>(s_bm + ((nb + 3) & ~static_cast<size_t>(3)));
+    const float* gsrc = L.cb32 + static_cast<size_t>(i0) * out * G;
+    const bool gbulk = bulk_ok(gsrc, gfl * 4);
+    const bool bbulk = bulk_ok(a.bm_in + boff, nb * 4) && bulk_ok(a.bt_in + boff, nb * 4);
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        if (gbulk) {  // the grid slice does not depend on the previous kernel
+            mbar_expect_tx(&s_bar[0], static_cast<uint32_t>(gfl * 4));
+            bulk_g2s(s_grid, gsrc, static_cast<uint32_t>(gfl * 4), &s_bar[0]);
+        }
+    }
+    if (!gbulk) stage_words(reinterpret_cast<uint32_t*>(s_grid), reinterpret_cast<const uint32_t*>(gsrc), gfl, tid);
+    pdl_trigger();
+    pdl_wait();  // the brackets come from the previous kernel
+    if (bbulk) {
+        if (tid == 0) {
+            mbar_expect_tx(&s_bar[1], static_cast<uint32_t>(nb * 8));
+            bulk_g2s(s_bm, a.bm_in + boff, static_cast<uint32_t>(nb * 4), &s_bar[1]);
+            bulk_g2s(s_bt, a.bt_in + boff, static_cast<uint32_t>(nb * 4), &s_bar[1]);
+        }
+    } else {
+        stage_words(reinterpret_cast<uint32_t*>(s_bm), reinterpret_cast<const uint32_t*>(a.bm_in + boff), nb, tid);
+        stage_words(reinterpret_cast<uint32_t*>(s_bt), reinterpret_cast<const uint32_t*>(a.bt_in + boff), nb, tid);
+    }
+    __syncthreads();  // the barrier inits and any word-staged data
+    if (gbulk) mbar_wait(&s_bar[0], 0);
+    if (bbulk) mbar_wait(&s_bar[1], 0);
+    float* part = a.partial + static_cast<size_t>(blockIdx.x) * B * out;
+    for (int p = tid; p < B * out; p += kNarrowT) {
+        const int sm = p / out, j = p - sm * out;
+        const float* g = s_grid + j * G;
+        float acc = 0.f;
+#pragma unroll 4
+        for (int r = 0; r < nr; ++r) {
+            const int m = s_bm[r * B + sm];
+            const float t = s_bt[r * B + sm];
+            const float c0 = g[r * out * G + m], c1 = g[r * out * G + m + 1];
+            acc += fmaf(t, c1 - c0, c0);
+        }
+        part[p] = acc;
     }
 }
 
@@ -1897,7 +1988,11 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
             const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
             launch_pdl(k_dense_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         } else {
-            const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+            static const long long cap = [] {
+                const char* e = std::getenv("SKAN_DENSE_REDUCE_BLOCKS");  // experiment: grid cap per SM
+                return e ? std::max(1, std::atoi(e)) : 64;  // one output per thread at cfg4
+            }();
+            const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * cap));
             launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         }
         return 2;
@@ -1917,6 +2012,49 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
     launch_pdl(k, dim3(c.jt, splits, c.st), dim3(kGmT), c.smem, pdl, s, a);
     if (!with_reduce) return 1;
     // bias: folded into W for compressed layers; dense layers have none
+    const long long n = static_cast<long long>(a.B) * a.L.out;
+    if (c.nsplit >= 16 && n < 148LL * 256) {
+        const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
+        launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+    } else {
+        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+        launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+    }
+    return 2;
+}
+
+bool dense_narrow_ok(const DevLayer& L) { return L.fmt == FMT_DENSE && !L.wt && L.out <= 32 && L.G >= 2; }
+
+size_t dense_narrow_smem(const DevLayer& L, int B, int rows) {
+    const size_t nb = (static_cast<size_t>(rows) * B + 3) & ~static_cast<size_t>(3);
+    return ((static_cast<size_t>(rows) * L.out * L.G * 4 + 15) & ~static_cast<size_t>(15)) + nb * 8;
+}
+
+LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms) {
+    LaunchCfg c{};
+    const int sms = num_sms > 0 ? num_sms : 148;
+    c.kind = 5;
+    // about two CTAs per SM, fewer rows per CTA while the staging exceeds ~100 KB
+    static const int per_sm = [] {
+        const char* e = std::getenv("SKAN_NARROW_PER_SM");  // experiment: CTAs per SM
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    int splits = std::min(L.in, per_sm * sms);
+    int rows = (L.in + splits - 1) / splits;
+    while (rows > 1 && dense_narrow_smem(L, B, rows) > 100 * 1024) rows = (rows + 1) / 2;
+    c.ichunk = rows;
+    c.nsplit = (L.in + rows - 1) / rows;
+    c.jt = 1;
+    c.st = 1;
+    c.smem = dense_narrow_smem(L, B, rows);
+    return c;
+}
+
+int launch_dense_narrow(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
+    FwdArgs a = a0;
+    a.rows_per_cta = c.ichunk;
+    ensure_smem(k_dense_narrow, c.smem);
+    launch_pdl(k_dense_narrow, dim3(c.nsplit), dim3(kNarrowT), c.smem, pdl, s, a);
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
         const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));

@@ -130,7 +130,8 @@ struct LaunchCfg {
     int ichunk;  // inputs per split
     int kind;    // fast path kernel: 0 = rows-in-warps (small batch), 1 = samples-in-lanes
                  // (large batch), 2 = pair planes in shared memory (batch 1), 4 = tensor-core
-                 // GEMM over the knot basis (large batch, wide layers; skan_gemm.cu)
+                 // GEMM over the knot basis (large batch, wide layers; skan_gemm.cu),
+                 // 5 = narrow dense layer on the CUDA cores (skan_gemm.cu)
     int vj;      // outputs per lane (small kernel); GEMM: W stages
     int rw;      // rows per warp (small kernel); GEMM: dense TMA ring slots
     int ic;      // inputs per staged chunk (large kernel)
@@ -264,6 +265,11 @@ uint64_t dense_tile_floats(int in, int out, int G);
 void build_dense_tiles(const DevLayer& L, float* wt, const float* src, int ch0, int ch1, cudaStream_t s);
 float dense_fp16_scale(const float* wt, uint64_t n, cudaStream_t s);
 int launch_layer_gemm(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s, bool with_reduce = true);
+// Narrow dense layers (out <= 32, natural grid layout) at batch >= 3: CUDA-core
+// split kernel + fixed-order reduction (skan_gemm.cu).  LaunchCfg::kind 5.
+bool dense_narrow_ok(const DevLayer& L);
+LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms);
+int launch_dense_narrow(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s);
 // MMA work one k_layer_gemm launch issues (flops, as 2*M*N*K per tcgen05.mma)
 double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B);
 

@@ -1235,6 +1235,7 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         const char* e = std::getenv("SKAN_GEMM_MIN_OUT");  // experiment: narrowest layer routed to the GEMM
         return e ? std::atoi(e) : 16;
     }();
+    if (B >= g_gemm_min_batch && dense_narrow_ok(L)) return dense_narrow_cfg(L, B, sms);
     if (B >= g_gemm_min_batch && L.out >= gemm_min_out && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {
@@ -1295,6 +1296,7 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
 
 int launch_fwd_fast(const FwdArgs& a, const LaunchCfg& c, bool pdl, cudaStream_t s) {
     if (c.kind == 4) return launch_layer_gemm(a, c, pdl, s);
+    if (c.kind == 5) return launch_dense_narrow(a, c, pdl, s);
     if (c.kind == 2) {
         void (*k)(FwdArgs);
         switch (c.vj) {
