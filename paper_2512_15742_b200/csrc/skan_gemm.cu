@@ -1321,9 +1321,8 @@ __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
 // the same K order into TMEM as fp16 pairs.  The f32 tiles land by TMA in a
 // ring (reading them from L2 in the conversion warps instead was measured
 // latency-bound).
-constexpr int kD16Ring = 3;   // pair slots of the f32 ring (two IC = 4 tiles each)
-constexpr int kD16Stg = 2;    // fp16 [W_hi | W_lo] operand stages
-constexpr int kD16Br = 4;     // bracket slots (8 inputs x B each)
+constexpr int kD16Ring = 5;   // pair slots (two f32 IC = 4 tiles each, converted in place to [W_hi | W_lo])
+constexpr int kD16Br = kD16Ring + 1;  // bracket slots (8 inputs x B each): > the ring, see the TMA warp
 constexpr int kD16Cv = 2;     // conversion warp sets (of four), taking pairs in turn
 constexpr int kD16T = kGmP / 2 + kD16Cv * 128 + 64;  // A sets + conversion sets + MMA warp + TMA warp
 constexpr int kD16Mma = kD16T / 32 - 2, kD16Tma = kD16T / 32 - 1;
@@ -1353,9 +1352,8 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
     const uint32_t tile_t = kGmN * KC * 4;         // one f32 IC = 4 tile
     const uint32_t half_t = kGmN * KC2 * 2;        // one fp16 operand (W_hi or W_lo) of a pair
     unsigned char* s_ring = smem;                                  // kD16Ring x 2 f32 tiles
-    unsigned char* s_stg = smem + kD16Ring * 2 * tile_t;           // kD16Stg x [W_hi | W_lo]
     const uint32_t br_bytes = static_cast<uint32_t>(2 * IC) * a.B * 4;
-    unsigned char* s_br = s_stg + kD16Stg * 2 * half_t;            // kD16Br x [int m | float t] x 8 x B
+    unsigned char* s_br = smem + kD16Ring * 2 * tile_t;            // kD16Br x [int m | float t] x 8 x B
     const float wsc = L.wsc, wsc_inv = 1.0f / L.wsc;
     // pair x = (tile jt = x / nch2, pair q = x % nch2): IC = 4 tiles 2q, 2q + 1 of block jt
     auto tile_src = [&](int jt, int ch) {
@@ -1363,15 +1361,12 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
     };
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     pdl_trigger();
-    // the ring starts zeroed: the conversion loop is branch-free and a pair's
-    // missing second tile must not hold non-finite bit patterns
-    for (uint32_t q = tid * 16; q < kD16Ring * 2 * tile_t; q += kD16T * 16)
-        *reinterpret_cast<uint4*>(s_ring + q) = make_uint4(0, 0, 0, 0);
-    tc::fence_proxy_async();  // ordered before the TMA writes into the same ring
     if (tid == 0) {
-        for (int q = 0; q < kD16Ring; ++q) mbar_init(&s_tfull[q], 1);
+        for (int q = 0; q < kD16Ring; ++q) {
+            mbar_init(&s_tfull[q], 1);
+        }
         for (int q = 0; q < kDnQ; ++q) {
-            mbar_init(&s_full[q], kGmP / 2);
+            mbar_init(&s_full[q], kGmP / 4 + kD16Cv * 128);  // one A set + every conversion thread
             mbar_init(&s_done[q], 1);
         }
         for (int q = 0; q < kDnSeg; ++q) mbar_init(&s_accfull[q], 1);
@@ -1405,12 +1400,36 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
                     }
                 }
             }
+            // optional HBM -> L2 prefetch running `dist` pairs past the ring
+            // (a.gemm_ring = SKAN_DENSE_PREFETCH; 0 = off)
+            const int dist = a.gemm_ring;
+            int pu = kD16Ring, jp = jt, qp = q2;
+            for (int r = 0; r < kD16Ring; ++r)
+                if (++qp == nch2) {
+                    qp = 0;
+                    ++jp;
+                }
+            auto prefetch_to = [&](int lim) {
+                for (; pu < lim && pu < n; ++pu) {
+                    const int nt = min(2, nch - 2 * qp);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tile_src(jp, 2 * qp)),
+                                 "r"(nt * tile_t)
+                                 : "memory");
+                    if (++qp == nch2) {
+                        qp = 0;
+                        ++jp;
+                    }
+                }
+            };
+            if (dist > 0) prefetch_to(kD16Ring + dist);
             pdl_wait();  // brackets come from the previous kernel
             int jr = jt, qr = q2;  // ring refill position: pair u
 #pragma unroll 1
             for (int u = 0; u < n; ++u) {
+                if (dist > 0) prefetch_to(u + kD16Ring + dist);
                 if (u >= kD16Ring) {
-                    // ring slot u % kD16Ring held pair u - kD16Ring: converted before its MMAs
+                    // ring slot u % kD16Ring held pair u - kD16Ring (converted in place,
+                    // then the MMAs' operand): free once those MMAs completed
                     qwait(s_done, u - kD16Ring);
                     dstamp(a, 2, u, 0);
                     issue(u, jr, qr);
@@ -1436,7 +1455,7 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
         }
     } else if (warp == kD16Mma) {
         // MMA warp: per K = 16 step, A x W_hi and A x W_lo (M = 128, N = 128, kind::f16)
-        const uint64_t dg0 = tc::make_desc(tc::smem_addr(s_stg), kLbo, 128);
+        const uint64_t dg0 = tc::make_desc(tc::smem_addr(s_ring), kLbo, 128);
         constexpr uint64_t kStep = (2 * kLbo) >> 4;
         const uint32_t idesc = tc::idesc_f16(kGmM, kGmN);
         int seg = 0;
@@ -1450,7 +1469,7 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
             tc::fence_after_sync();
             if (lane == 0) dstamp(a, 1, u, 0);
             const uint32_t ta = tmem + kDnAcol + (u % kDnA) * 64;
-            const uint64_t dh = dg0 + (u % kD16Stg) * ((2 * half_t) >> 4), dl = dh + (half_t >> 4);
+            const uint64_t dh = dg0 + (u % kD16Ring) * ((2 * half_t) >> 4), dl = dh + (half_t >> 4);
             mma_chunk_ts<true>(tmem, ta, dh, dl, idesc, first ? 0u : 1u, nstep, kStep);
             tc::mma_commit_warp(&s_done[u % kDnQ]);
             if (lane == 0) dstamp(a, 1, u, 1);
@@ -1565,54 +1584,60 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
             ++seg;
         }
     } else {
-        // conversion warps, kD16Cv sets of four taking pairs in turn: the f32
-        // tiles of the pair (ring) -> fp16 W_hi and W_lo (scaled) in a stage
-        const int set = (warp - kGmP / 64) >> 2;
-        const int lt = tid - kGmP / 2 - set * 128;
+        // conversion warps (kD16Cv sets of four), all on every pair, each
+        // thread a share of it: the pair's f32 tiles -> fp16 W_hi and W_lo
+        // (scaled), IN PLACE: every thread loads its share, the conversion
+        // threads meet at a named barrier, then write the two fp16 operands
+        // over the same 40 KB.  No separate operand stages, so the ring is
+        // five pairs deep: the slots' TMA land latency (~5k cycles with all
+        // SMs streaming) is what bounds this kernel.
+        constexpr int kCvT = kD16Cv * 128;
+        constexpr int kPer = (2 * 32 * KC + kCvT - 1) / kCvT;  // float4 per thread and pair (2 * nq / kCvT)
+        const int lt = tid - kGmP / 2;
         const int nq = static_cast<int>(tile_t / 16);  // float4 per tile
+        static_assert(32 * KC == kGmN * KC * 4 / 16, "nq");
         int q2 = static_cast<int>(x0 % nch2);
-        auto advance = [&]() { q2 = q2 + 1 == nch2 ? 0 : q2 + 1; };
-        for (int r = 0; r < set; ++r) advance();
 #pragma unroll 1
-        for (int u = set; u < n; u += kD16Cv) {
+        for (int u = 0; u < n; ++u) {
             const int nt = min(2, nch - 2 * q2);
-            // stage u % kD16Stg held pair u - kD16Stg; done(u - kD16Stg) also
-            // completes the ring slot's phase of pair u - kD16Ring
-            if (lt == 0 && set == 0) dstamp(a, 2, u, 2);
-            if (u >= kD16Stg) qwait(s_done, u - kD16Stg);
+            if (lt == 0) dstamp(a, 2, u, 2);
             mbar_wait_parity(&s_tfull[u % kD16Ring], (u / kD16Ring) & 1);
-            if (lt == 0 && set == 0) dstamp(a, 2, u, 3);
-            unsigned char* stg = s_stg + (u % kD16Stg) * 2 * half_t;
-            const float4* src = reinterpret_cast<const float4*>(s_ring + (u % kD16Ring) * 2 * tile_t);
-#pragma unroll 4
-            for (int qq = lt; qq < 2 * nq; qq += 128) {
+            if (lt == 0) dstamp(a, 2, u, 3);
+            unsigned char* slot = s_ring + (u % kD16Ring) * 2 * tile_t;
+            const float4* src = reinterpret_cast<const float4*>(slot);
+            float4 w[kPer];
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int qq = lt + r * kCvT;
+                // a pair's missing second tile (odd chunk count) converts as zeros
+                w[r] = qq < 2 * nq && (qq < nq || nt == 2) ? src[qq] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kCvT) : "memory");  // every share read before any write
+#pragma unroll
+            for (int r = 0; r < kPer; ++r) {
+                const int qq = lt + r * kCvT;
+                if (qq >= 2 * nq) break;
                 const int hsel = qq >= nq ? 1 : 0, q = qq - hsel * nq;
                 // float4 q of an f32 tile: core-matrix column g = q / 128 (K
                 // 4g..4g+3), row (q % 128): fp16 K index k = KC * h + 4g ..
                 const int g = q >> 7, rr = q & 127;
                 const int k = KC * hsel + 4 * g;
                 const uint32_t o = (k >> 3) * kLbo + (rr >> 3) * 128 + (rr & 7) * 16 + (k & 7) * 2;
-                // branch-free (the ring was zeroed at kernel start, so a pair's
-                // missing second tile converts finite stale data or zeros, and
-                // its A columns are zero): the unrolled iterations' independent
-                // chains overlap.  Packed: f32x2 scale, two-at-a-time fp16
-                // rounding, f32x2 remainder.
-                (void)nt;
-                const float4 w = src[qq];
+                // packed: f32x2 scale, two-at-a-time fp16 rounding, f32x2 remainder
                 const float2 sc = make_float2(wsc, wsc), neg = make_float2(-1.f, -1.f);
-                const float2 a2 = __fmul2_rn(make_float2(w.x, w.y), sc), b2 = __fmul2_rn(make_float2(w.z, w.w), sc);
+                const float2 a2 = __fmul2_rn(make_float2(w[r].x, w[r].y), sc), b2 = __fmul2_rn(make_float2(w[r].z, w[r].w), sc);
                 const __half2 ha = __float22half2_rn(a2), hb = __float22half2_rn(b2);
                 const __half2 la = __float22half2_rn(__ffma2_rn(__half22float2(ha), neg, a2));
                 const __half2 lb = __float22half2_rn(__ffma2_rn(__half22float2(hb), neg, b2));
-                *reinterpret_cast<uint2*>(stg + o) =
+                *reinterpret_cast<uint2*>(slot + o) =
                     make_uint2(*reinterpret_cast<const uint32_t*>(&ha), *reinterpret_cast<const uint32_t*>(&hb));
-                *reinterpret_cast<uint2*>(stg + half_t + o) =
+                *reinterpret_cast<uint2*>(slot + half_t + o) =
                     make_uint2(*reinterpret_cast<const uint32_t*>(&la), *reinterpret_cast<const uint32_t*>(&lb));
             }
             tc::fence_proxy_async();
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_addr(&s_full[u % kDnQ])) : "memory");
-            if (lt == 0 && set == 0) dstamp(a, 2, u, 4);
-            for (int r = 0; r < kD16Cv; ++r) advance();
+            if (lt == 0) dstamp(a, 2, u, 4);
+            q2 = q2 + 1 == nch2 ? 0 : q2 + 1;
         }
     }
     tc::fence_before_sync();
@@ -1826,7 +1851,7 @@ bool dense_f16_ok(const DevLayer& L) {
 }
 size_t dense_f16_smem(int G) {
     const size_t kc = 4 * static_cast<size_t>(G);
-    return kD16Ring * 2 * kGmN * kc * 4 + kD16Stg * 2 * kGmN * (2 * kc) * 2 + kD16Br * 2 * 8 * 64 * 4;
+    return kD16Ring * 2 * kGmN * kc * 4 + kD16Br * 2 * 8 * 64 * 4;
 }
 
 bool dense_persist_ok(const DevLayer& L, int B) {
