@@ -1324,7 +1324,8 @@ __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
 constexpr int kD16Ring = 5;   // pair slots (two f32 IC = 4 tiles each, converted in place to [W_hi | W_lo])
 constexpr int kD16Br = kD16Ring + 1;  // bracket slots (8 inputs x B each): > the ring, see the TMA warp
 constexpr int kD16Cv = 2;     // conversion warp sets (of four), taking pairs in turn
-constexpr int kD16T = kGmP / 2 + kD16Cv * 128 + 64;  // A sets + conversion sets + MMA warp + TMA warp
+constexpr int kD16As = 3;     // A warp sets (of four), taking pairs in turn
+constexpr int kD16T = kD16As * 128 + kD16Cv * 128 + 64;  // A sets + conversion sets + MMA warp + TMA warp
 constexpr int kD16Mma = kD16T / 32 - 2, kD16Tma = kD16T / 32 - 1;
 
 __host__ __device__ __forceinline__ int d16_nch2(int nch) { return (nch + 1) / 2; }
@@ -1478,8 +1479,8 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
                 ++seg;
             }
         }
-    } else if (warp < kGmP / 64) {
-        // A warps, two sets of four taking alternate pairs: lane row r (sample
+    } else if (warp < kD16As * 4) {
+        // A warps, kD16As sets of four taking pairs in turn: lane row r (sample
         // r & 63, t_lo for r >= 64), every column k of the pair (k < KC: tile
         // a, knot k / 4, input k % 4; k >= KC: tile b), fp16 pairs in TMEM
         const int q4 = warp & 3, set = warp >> 2;
@@ -1498,7 +1499,7 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
                 q2 = 0;
                 ++jt;
             }
-            if ((u & 1) != set) {
+            if (u % kD16As != set) {
                 seg += last;
                 continue;
             }
@@ -1593,9 +1594,9 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
         // SMs streaming) is what bounds this kernel.
         constexpr int kCvT = kD16Cv * 128;
         constexpr int kPer = (2 * 32 * KC + kCvT - 1) / kCvT;  // float4 per thread and pair (2 * nq / kCvT)
-        const int lt = tid - kGmP / 2;
+        const int lt = tid - kD16As * 128;
         const int nq = static_cast<int>(tile_t / 16);  // float4 per tile
-        static_assert(32 * KC == kGmN * KC * 4 / 16, "nq");
+        static_assert(32 * KC == kGmN * KC * 4 / 16 && (KC / 4) % 2 == 0, "nq; K groups come in pairs");
         int q2 = static_cast<int>(x0 % nch2);
 #pragma unroll 1
         for (int u = 0; u < n; ++u) {
@@ -1605,22 +1606,34 @@ __global__ void __launch_bounds__(kD16T, 1) k_dense_persist16(FwdArgs a, int nch
             if (lt == 0) dstamp(a, 2, u, 3);
             unsigned char* slot = s_ring + (u % kD16Ring) * 2 * tile_t;
             const float4* src = reinterpret_cast<const float4*>(slot);
+            // share element e -> (tile h, K group g, row rr) so that a warp's 32
+            // lanes are 16 rows x the two K groups of one 16-byte fp16 row
+            // chunk: its fp16 stores are 256 contiguous bytes (no bank
+            // conflicts) and its f32 loads two contiguous 256-byte runs.
+            // float4 (g, rr) of an f32 tile = K 4g..4g+3 of row rr; fp16 K
+            // index k = KC * h + 4g.
+            auto share = [&](int e, int& h, int& g, int& rr) {
+                h = e >= nq ? 1 : 0;
+                const int i = e - h * nq, rem = i & 255;
+                g = 2 * (i >> 8) + ((rem >> 4) & 1);
+                rr = (rem >> 5) * 16 + (rem & 15);
+            };
             float4 w[kPer];
 #pragma unroll
             for (int r = 0; r < kPer; ++r) {
                 const int qq = lt + r * kCvT;
+                int h, g, rr;
+                share(qq, h, g, rr);
                 // a pair's missing second tile (odd chunk count) converts as zeros
-                w[r] = qq < 2 * nq && (qq < nq || nt == 2) ? src[qq] : make_float4(0.f, 0.f, 0.f, 0.f);
+                w[r] = qq < 2 * nq && (h == 0 || nt == 2) ? src[h * nq + g * 128 + rr] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             asm volatile("bar.sync 1, %0;" ::"n"(kCvT) : "memory");  // every share read before any write
 #pragma unroll
             for (int r = 0; r < kPer; ++r) {
                 const int qq = lt + r * kCvT;
                 if (qq >= 2 * nq) break;
-                const int hsel = qq >= nq ? 1 : 0, q = qq - hsel * nq;
-                // float4 q of an f32 tile: core-matrix column g = q / 128 (K
-                // 4g..4g+3), row (q % 128): fp16 K index k = KC * h + 4g ..
-                const int g = q >> 7, rr = q & 127;
+                int hsel, g, rr;
+                share(qq, hsel, g, rr);
                 const int k = KC * hsel + 4 * g;
                 const uint32_t o = (k >> 3) * kLbo + (rr >> 3) * 128 + (rr & 7) * 16 + (k & 7) * 2;
                 // packed: f32x2 scale, two-at-a-time fp16 rounding, f32x2 remainder
