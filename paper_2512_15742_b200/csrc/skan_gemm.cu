@@ -1244,21 +1244,20 @@ __global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
     if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
-// sum of partial planes z = z0, z0 + dz, ... < nz in that order (f64), up to
-// eight loads in flight (guarded, so short sums get them too): the adds are
-// ordered, the loads need not be
+// sum of partial planes z = z0, z0 + dz, ... < nz in that order (f64), four
+// loads in flight: the adds are ordered, the loads need not be
 __device__ __forceinline__ double ordered_plane_sum(const float* __restrict__ base, size_t plane, int z0, int dz,
                                                     int nz) {
     double v = 0.0;
-    for (int z = z0; z < nz; z += 8 * dz) {
-        float f[8];
+    int z = z0;
+    for (; z + 3 * dz < nz; z += 4 * dz) {
+        float f[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            f[u] = z + u * dz < nz ? __ldcg(base + static_cast<size_t>(z + u * dz) * plane) : 0.f;
+        for (int u = 0; u < 4; ++u) f[u] = __ldcg(base + static_cast<size_t>(z + u * dz) * plane);
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (z + u * dz < nz) v += static_cast<double>(f[u]);
+        for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
     }
+    for (; z < nz; z += dz) v += static_cast<double>(__ldcg(base + static_cast<size_t>(z) * plane));
     return v;
 }
 
