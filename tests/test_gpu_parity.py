@@ -652,6 +652,29 @@ def test_swap_from_bytes_refills_in_place(torch_cuda):
         hq.swap_model_bytes(model, other.serialize())
 
 
+@pytest.mark.parametrize("dims,grid", [((300, 20), 10), ((97, 3), 5), ((64, 33, 32), 3), ((1000, 1), 16)])
+@pytest.mark.parametrize("batch", [3, 17, 64, 200])
+def test_dense_narrow_layer_against_oracle(torch_cuda, dims, grid, batch):
+    """Dense layers with <= 32 outputs keep the natural [in][out][G] grid and
+    run k_dense_narrow at batch >= 3: row blocks staged by bulk copies when
+    16-byte aligned (3 x 5 x 4 = 60-byte rows are not: the word-staging
+    path), brackets likewise (batch 17: most blocks unaligned), split partials
+    summed in order.  Fast mode within the bound, exact mode bitwise (the
+    exact kernels read the same natural grid)."""
+    rls = synthetic.dense_runtime_head(dims=dims, grid=grid, seed=11)
+    tables = [oracle.Tables.from_runtime(rl) for rl in rls]
+    model = hq.upload(rls, device=0)
+    x = synthetic.synthetic_inputs(batch, dims[0], seed=5, grid=grid)
+    ws = hq.make_workspace(model, max_batch=batch)
+    got = np.zeros(batch * dims[-1])
+    want, scale = oracle.port_forward_l1(tables, x, batch, threads=16)
+    hq.compressed_forward(model, x, batch, got, ws, mode="fast")
+    assert_close(got, want, scale)
+    want_e, _ = oracle.port_forward(tables, x, batch)
+    hq.compressed_forward(model, x, batch, got, ws, mode="exact")
+    assert np.array_equal(_bits(got), _bits(want_e))
+
+
 @pytest.mark.parametrize("dims,batch", [((256, 1024), 64), ((256, 1024, 20), 64), ((300, 700, 20), 17),
                                         ((1024, 4096), 32), ((2048, 1408), 64)])
 def test_dense_persistent_schedule_against_oracle(torch_cuda, dims, batch):
