@@ -794,42 +794,96 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     if (nchunks > 0) mbar_wait_parity(&s_wfree[(nchunks - 1) % wst], ((nchunks - 1) / wst) & 1);
     tc::fence_after_sync();
     // epilogue: producer warp w reads TMEM lanes (w%4)*32.. and columns
-    // (w/4)*32..+32 of both halves (W_hi and W_lo products) and adds them.
-    // STACK: lanes 64-127 (A_lo rows) go to their own partial plane, summed
-    // with the A_hi plane by the split reduction.
-    if (warp < kGmP / 32) {
-      for (int hf = 0; hf < (DUAL ? 2 : 1); ++hf) {  // DUAL: accumulator hf holds samples 128 hf ..
-        const int q4 = warp & 3, cq = warp >> 2;
-        const int as = STACK ? (q4 & 1) * 32 + lane : hf * kGmM + q4 * 32 + lane;
-        const size_t plane = static_cast<size_t>(a.B) * L.out;
-        const int pz = STACK ? 2 * blockIdx.y + (q4 >> 1) : blockIdx.y;
-        float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
-        const uint32_t tacc = tmem + hf * 2 * kGmN;
+    // (w/4)*32..+32 of both halves (W_hi and W_lo products), adds them and
+    // stages the CTA's output tile in shared memory (the operand buffers are
+    // free: every MMA completed); then each warp writes whole sample rows,
+    // 512 contiguous bytes per instruction.  (Written straight from the
+    // TMEM lanes each store was 32 scattered 16-byte pieces: ~15k cycles of
+    // a ~120k-cycle CTA at bs256.)  Virtual row vr = hf * 128 + lane row:
+    // STACK rows 64-127 (A_lo) go to their own partial plane, summed with
+    // the A_hi plane by the split reduction.
+    // Small tiles (few samples; every stacked 64-sample tile) keep the direct
+    // stores: staging all rows costs more than their few scattered writes
+    // (measured: +4 us at batch 3-16).
+    constexpr bool kStaged = !STACK;
+    if (warp < kGmP / 32 && (!kStaged || nS < 64)) {
+        for (int hf = 0; hf < (DUAL ? 2 : 1); ++hf) {
+            const int q4 = warp & 3, cq = warp >> 2;
+            const int as = STACK ? (q4 & 1) * 32 + lane : hf * kGmM + q4 * 32 + lane;
+            const size_t plane = static_cast<size_t>(a.B) * L.out;
+            const int pz = STACK ? 2 * blockIdx.y + (q4 >> 1) : blockIdx.y;
+            float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
+            const uint32_t tacc = tmem + hf * 2 * kGmN;
 #pragma unroll 1
-        for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
-            float v[8], w[8];
-            if (nchunks > 0) {
-                tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
-                tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
-                const float inv = F16 ? 1.0f / wsc : 1.0f;  // exact: wsc is a power of two
+            for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+                float v[8], w[8];
+                if (nchunks > 0) {
+                    tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+                    tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
+                    const float inv = F16 ? 1.0f / wsc : 1.0f;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = (v[u] + w[u]) * inv;
-            } else {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = 0.f;
-            }
-            if (as < nS) {
-                if (c8 + 8 <= nJ && (L.out & 3) == 0) {
-                    *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
-                    *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                    for (int u = 0; u < 8; ++u) v[u] = (v[u] + w[u]) * inv;
                 } else {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (c8 + u < nJ) dst[c8 + u] = v[u];
+                    for (int u = 0; u < 8; ++u) v[u] = 0.f;
+                }
+                if (as < nS) {
+                    if (c8 + 8 <= nJ && (L.out & 3) == 0) {
+                        *reinterpret_cast<float4*>(dst + c8) = make_float4(v[0], v[1], v[2], v[3]);
+                        *reinterpret_cast<float4*>(dst + c8 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u)
+                            if (c8 + u < nJ) dst[c8 + u] = v[u];
+                    }
                 }
             }
         }
-      }
+    } else if (kStaged && warp < kGmP / 32) {
+        constexpr int kOS = kGmN + 4;  // padded row: conflict-free float4 staging stores
+        float* s_out = reinterpret_cast<float*>(smem);
+        const float inv = F16 ? 1.0f / wsc : 1.0f;  // exact: wsc is a power of two
+        for (int hf = 0; hf < (DUAL ? 2 : 1); ++hf) {  // DUAL: accumulator hf holds samples 128 hf ..
+            const int q4 = warp & 3, cq = warp >> 2;
+            const int vr = hf * kGmM + q4 * 32 + lane;
+            const uint32_t tacc = tmem + hf * 2 * kGmN;
+#pragma unroll 1
+            for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+                float v[8], w[8];
+                if (nchunks > 0) {
+                    tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
+                    tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + kGmN + c8, w);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = (v[u] + w[u]) * inv;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = 0.f;
+                }
+                float4* o = reinterpret_cast<float4*>(s_out + vr * kOS + c8);
+                o[0] = make_float4(v[0], v[1], v[2], v[3]);
+                o[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kGmP) : "memory");  // the producer warps only
+        const size_t plane = static_cast<size_t>(a.B) * L.out;
+        const bool vec = (L.out & 3) == 0;
+        const int col = 4 * lane;
+#pragma unroll 1
+        for (int vr = warp; vr < (DUAL ? 2 * kGmM : kGmM); vr += kGmP / 32) {
+            const int smp = STACK ? (vr & 63) : vr;
+            const int pz = STACK ? 2 * blockIdx.y + (vr >> 6) : blockIdx.y;
+            if (smp >= nS) continue;
+            float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + smp) * L.out + j0;
+            const float4 v = *reinterpret_cast<const float4*>(s_out + vr * kOS + col);
+            if (vec && col + 4 <= nJ) {
+                *reinterpret_cast<float4*>(dst + col) = v;
+            } else {
+                const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (col + u < nJ) dst[col + u] = e[u];
+            }
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -1931,6 +1985,8 @@ LaunchCfg gemm_cfg(const DevLayer& L, int B, int num_sms) {
         gp.ring = 0;
         gp.smem = 4 * kGmM * kc * 4 + 2 * 2 * kGmN * kc * 4;
     }
+    // the epilogue stages the output tile in shared memory: [rows][128 + 4] f32
+    if (!stack) gp.smem = std::max(gp.smem, static_cast<size_t>(c.spt == 2 * kGmM ? 2 * kGmM : kGmM) * (kGmN + 4) * 4);
     c.vj = gp.wst;
     c.rw = gp.ring;
     c.jt = (L.out + c.tj - 1) / c.tj;

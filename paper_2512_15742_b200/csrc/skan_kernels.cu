@@ -1029,7 +1029,7 @@ int dispatch_exact_split(const DevLayer& L, int B, const int* bm, const double* 
     for (int i0 = 0; i0 < L.in; i0 += per) {
         const int ni = std::min(per, L.in - i0);
         const size_t n = static_cast<size_t>(ni) * L.out * ((B + 3) / 4);
-        const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 16));
+        const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 64));
         k_exact_terms<FMT><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L, B, bm, btd, i0, ni, terms);
         const int nb = B * ((L.out + 31) / 32), f = i0 == 0 ? 1 : 0, la = i0 + ni >= L.in ? 1 : 0;
         static const bool attr = [] {  // 128 KB of dynamic shared memory (opt-in above 48 KB)
