@@ -701,19 +701,21 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             wph ^= 1u;
         }
     };
+    // the layer's own data does not depend on the previous kernel: the first
+    // records (and dense W tiles) are in flight while it drains
+    if (tid < kGmP) {
+        if constexpr (kDense) {
+            if (tid == 0)
+                for (int c = 0; c < ring; ++c) issue_tile(c, c);
+        }
+        if (nchunks > 0) load_recs(0);
+    }
     pdl_wait();  // brackets come from the previous kernel
     __syncthreads();  // s_lut visible
     if (tid < kGmP) {
         // producers: W of chunk c into stage c % wst once the MMAs of chunk
         // c - wst released it; A into buffer c & 1 once chunk c-2's did
-        if constexpr (kDense) {
-            if (tid == 0)
-                for (int c = 0; c < ring; ++c) issue_tile(c, c);
-        }
-        if (nchunks > 0) {
-            load_recs(0);
-            load_chunk(sa, 0);
-        }
+        if (nchunks > 0) load_chunk(sa, 0);
 #pragma unroll 1
         for (int c = 0; c < nchunks; c += 2) {
             produce(sa, sb, c);
