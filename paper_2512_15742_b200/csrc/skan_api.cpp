@@ -824,6 +824,20 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
     const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
     const skan::LaunchCfg& c = cfg[l];
     const bool prev_planes = l > 0 && cfg[l - 1].kind == 2;
+    // at small batch a layer GEMM followed by a one-tile-wide layer GEMM
+    // leaves its split partials to that GEMM, which reduces and brackets them
+    // in its prologue (measured: batch 16 59.4 -> 55.3 us; from batch 64 the
+    // separate 1184-block reduction is faster than ~90 CTAs doing it)
+    static const bool fuse_off = [] {
+        const char* e = std::getenv("SKAN_GEMM_FUSE_REDUCE");  // A/B experiment: 0 = separate reduction
+        return e && e[0] == '0';
+    }();
+    auto fuses = [&](const skan::LaunchCfg& p, const skan::LaunchCfg& n) {
+        return !fuse_off && B <= 32 && p.kind == 4 && (p.persist == 0 || p.persist == 3) && n.kind == 4 &&
+               (n.persist == 0 || n.persist == 3) && n.jt == 1;
+    };
+    const bool prev_fused = l > 0 && fuses(cfg[l - 1], c);
+    const bool next_fused = next != nullptr && fuses(c, cfg[l + 1]);
     int launches = 0;
     skan::FwdArgs a{};
     a.L = L;
@@ -845,6 +859,10 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
         a.prev_nsplit = cfg[l - 1].nsplit;
         a.prev_bias_sum = h->dl[l - 1].bias_sum;
     }
+    if (prev_fused) {  // bias folded into the previous GEMM's W: partials only
+        a.prev_partial = part[(l - 1) & 1];
+        a.prev_nsplit = cfg[l - 1].nsplit;
+    }
     a.partial = part[l & 1];
     a.counters = d.counters + static_cast<size_t>(l) * d.counter_stride;
     a.y = out;
@@ -855,6 +873,7 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
         a.bt_out = bt[(l + 1) & 1];
     }
     a.err = d.err;
+    if (next_fused) return launches + skan::launch_layer_gemm(a, c, chained, s, /*with_reduce=*/false);
     return launches + skan::launch_fwd_fast(a, c, chained, s);  // the GEMM's split reduction counted inside
 }
 // batches at or below this take the two-pass exact path (SKAN_EXACT_SPLIT_MAX

@@ -333,6 +333,23 @@ __device__ __forceinline__ void gstamp(const FwdArgs& a, int role, int c, int ph
     if (a.dbg && c < 64 && (blockIdx.x | blockIdx.y | blockIdx.z) == 0) a.dbg[(role * 64 + c) * 8 + ph] = clock64();
 }
 
+// sum of partial planes z = z0, z0 + dz, ... < nz in that order (f64), four
+// loads in flight: the adds are ordered, the loads need not be
+__device__ __forceinline__ double ordered_plane_sum(const float* __restrict__ base, size_t plane, int z0, int dz,
+                                                    int nz) {
+    double v = 0.0;
+    int z = z0;
+    for (; z + 3 * dz < nz; z += 4 * dz) {
+        float f[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) f[u] = __ldcg(base + static_cast<size_t>(z + u * dz) * plane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
+    }
+    for (; z < nz; z += dz) v += static_cast<double>(__ldcg(base + static_cast<size_t>(z) * plane));
+    return v;
+}
+
 template <int FMT, int IC, bool STACK, bool F16 = false, bool DUAL = false>
 __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -711,7 +728,28 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
         if (nchunks > 0) load_recs(0);
     }
     pdl_wait();  // brackets come from the previous kernel
-    __syncthreads();  // s_lut visible
+    if (a.prev_partial) {
+        // the previous GEMM layer left its split partials: this CTA reduces
+        // the entries its rows and samples consume (ascending split order in
+        // f64, exactly k_split_reduce's sums) and brackets them for this
+        // layer, in place of a separate reduction launch (one CTA per row
+        // range: the next layer is one output tile wide)
+        const size_t pplane = static_cast<size_t>(a.B) * L.in;
+        const int nrow = rend - r0;
+        int* bm_w = const_cast<int*>(a.bm_in);
+        float* bt_w = const_cast<float*>(a.bt_in);
+        for (int e = tid; e < nrow * nS; e += kGmT) {
+            const int sm = e / nrow, i = r0 + (e - sm * nrow), smp = s0 + sm;
+            const double v = ordered_plane_sum(a.prev_partial + static_cast<size_t>(smp) * L.in + i, pplane, 0, 1,
+                                               a.prev_nsplit);
+            int m;
+            float t;
+            fast_locate(L, v, a.err, m, t);
+            bm_w[static_cast<size_t>(i) * a.B + smp] = m;
+            bt_w[static_cast<size_t>(i) * a.B + smp] = t;
+        }
+    }
+    __syncthreads();  // s_lut visible (and the fused brackets)
     if (tid < kGmP) {
         // producers: W of chunk c into stage c % wst once the MMAs of chunk
         // c - wst released it; A into buffer c & 1 once chunk c-2's did
@@ -1298,23 +1336,6 @@ __global__ void __launch_bounds__(kDnT, 1) k_dense_persist(FwdArgs a, int nch) {
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_free<512>(tmem);
-}
-
-// sum of partial planes z = z0, z0 + dz, ... < nz in that order (f64), four
-// loads in flight: the adds are ordered, the loads need not be
-__device__ __forceinline__ double ordered_plane_sum(const float* __restrict__ base, size_t plane, int z0, int dz,
-                                                    int nz) {
-    double v = 0.0;
-    int z = z0;
-    for (; z + 3 * dz < nz; z += 4 * dz) {
-        float f[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) f[u] = __ldcg(base + static_cast<size_t>(z + u * dz) * plane);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v += static_cast<double>(f[u]);
-    }
-    for (; z < nz; z += dz) v += static_cast<double>(__ldcg(base + static_cast<size_t>(z) * plane));
-    return v;
 }
 
 __device__ __forceinline__ void reduce_finish(const FwdArgs& a, size_t p, double v, int add_bias) {
