@@ -1235,7 +1235,9 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
         const char* e = std::getenv("SKAN_GEMM_MIN_OUT");  // experiment: narrowest layer routed to the GEMM
         return e ? std::atoi(e) : 16;
     }();
-    if (B >= g_gemm_min_batch && dense_narrow_ok(L)) return dense_narrow_cfg(L, B, sms);
+    // (up to batch 512: above it the staged brackets leave few rows per CTA and
+    // the split partials grow with the batch; the generic kernels take over)
+    if (B >= g_gemm_min_batch && B <= 512 && dense_narrow_ok(L)) return dense_narrow_cfg(L, B, sms);
     if (B >= g_gemm_min_batch && L.out >= gemm_min_out && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {

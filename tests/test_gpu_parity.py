@@ -653,7 +653,7 @@ def test_swap_from_bytes_refills_in_place(torch_cuda):
 
 
 @pytest.mark.parametrize("dims,grid", [((300, 20), 10), ((97, 3), 5), ((64, 33, 32), 3), ((1000, 1), 16)])
-@pytest.mark.parametrize("batch", [3, 17, 64, 200])
+@pytest.mark.parametrize("batch", [3, 17, 64, 200, 600])
 def test_dense_narrow_layer_against_oracle(torch_cuda, dims, grid, batch):
     """Dense layers with <= 32 outputs keep the natural [in][out][G] grid and
     run k_dense_narrow at batch >= 3: row blocks staged by bulk copies when
