@@ -2139,7 +2139,11 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
     return 2;
 }
 
-bool dense_narrow_ok(const DevLayer& L) { return L.fmt == FMT_DENSE && !L.wt && L.out <= 32 && L.G >= 2; }
+bool dense_narrow_ok(const DevLayer& L) {
+    // one input row of the grid plus the brackets of 512 samples must fit the staging
+    return L.fmt == FMT_DENSE && !L.wt && L.out <= 32 && L.G >= 2 &&
+           static_cast<size_t>(L.out) * L.G * 4 + 16 + 512 * 8 <= 100 * 1024;
+}
 
 size_t dense_narrow_smem(const DevLayer& L, int B, int rows) {
     const size_t nb = (static_cast<size_t>(rows) * B + 3) & ~static_cast<size_t>(3);
