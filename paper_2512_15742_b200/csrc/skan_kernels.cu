@@ -966,10 +966,12 @@ __global__ void __launch_bounds__(256) k_exact_terms(DevLayer L, int B, const in
 // dependent DADD is ~8 clocks, tools/micro/dadd_lat.cu), and at small batch
 // there are few chains, so the terms must stream in far ahead of the adds.
 // One warp per (sample, block of 32 outputs); its chunks of kExKc inputs x 32
-// outputs are contiguous 8 KB runs, so lane 0 keeps kExSt of them in flight
+// outputs are contiguous 32 KB runs, so lane 0 keeps kExSt of them in flight
 // with TMA bulk copies on per-stage mbarriers, and each lane adds its column
-// from shared memory.  With 16 stages one warp has ~128 KB in flight.
-constexpr int kExKc = 32;
+// from shared memory.  With 4 stages one warp has ~128 KB in flight; long
+// chunks keep the per-chunk wait/refill overhead off the add chain (8 KB
+// chunks: 89 us at batch 1, 16 KB: 79, 32 KB: 75).
+constexpr int kExKc = 128;
 
 template <int kExSt>
 __global__ void __launch_bounds__(32) k_exact_sum(int out, int ni, const double* __restrict__ terms,
@@ -1033,16 +1035,16 @@ int dispatch_exact_split(const DevLayer& L, int B, const int* bm, const double* 
         k_exact_terms<FMT><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L, B, bm, btd, i0, ni, terms);
         const int nb = B * ((L.out + 31) / 32), f = i0 == 0 ? 1 : 0, la = i0 + ni >= L.in ? 1 : 0;
         static const bool attr = [] {  // 128 KB of dynamic shared memory (opt-in above 48 KB)
-            return cudaFuncSetAttribute(k_exact_sum<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        16 * kExKc * 32 * 8) == cudaSuccess &&
-                   cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        4 * kExKc * 32 * 8) == cudaSuccess;
+            return cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        4 * kExKc * 32 * 8) == cudaSuccess &&
+                   cudaFuncSetAttribute(k_exact_sum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        2 * kExKc * 32 * 8) == cudaSuccess;
         }();
         (void)attr;
         if (nb <= 2 * 148) {
-            k_exact_sum<16><<<nb, 32, 16 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
-        } else {
             k_exact_sum<4><<<nb, 32, 4 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
+        } else {
+            k_exact_sum<2><<<nb, 32, 2 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
         }
         launches += 2;
     }
