@@ -142,9 +142,10 @@ def test_exact_mode_headline_head_bitwise(torch_cuda):
     assert ws.interp_ops == ops == 2 * 2_911_744
 
 
-@pytest.mark.parametrize("batch", [12, 130])
+@pytest.mark.parametrize("batch", [1, 12, 130])
 def test_exact_mode_headline_head_split_and_one_pass(torch_cuda, batch):
-    """Exact mode's two kernels: batch 12 takes the two-pass split (terms, then
+    """Exact mode's kernels: batch 1 the bracket-ordered terms read from the
+    pair planes (k_exact_terms_planes), batch 12 the two-pass split (terms, then
     in-order sums) with layer 0 in two input blocks (12 * 1408 * 2048 doubles
     exceed the 256 MB term buffer), batch 130 the one-pass kernel
     (> kExactSplitMaxBatch).  Both bitwise equal to the reference."""
