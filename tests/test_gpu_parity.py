@@ -175,7 +175,9 @@ def test_fast_mode_headline_head(torch_cuda):
     cn = synthetic.synthetic_head()
     tables = [oracle.Tables.from_runtime(rl) for rl in synthetic.runtime_layers(cn)]
     model = hq.build_model(cn)
-    for batch in (1, 2, 3, 4):  # 1-2: per-sample persistent launches; 3-4: tensor-core GEMM
+    # 1-2: per-sample persistent launches; 3-32: tensor-core GEMMs, layer 1
+    # reducing layer 0's split partials in its prologue; 33+: separate reduction
+    for batch in (1, 2, 3, 4, 17, 32, 33, 64):
         x = synthetic.synthetic_inputs(batch, 2048, seed=30 + batch)
         want, _ = oracle.port_forward(tables, x, batch)
         got, ws = _gpu_forward(model, x, batch, "fast")
