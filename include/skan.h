@@ -307,6 +307,14 @@ skan_status skan_debug_gemm_timeline(unsigned long long* d_stamps);
  * in force then); not thread-safe against concurrent forwards. */
 int skan_debug_set_gemm_min_batch(int batch);
 
+/* Whether a layer GEMM at batch <= 32 leaves its split partials to a
+ * following one-tile-wide layer GEMM, which reduces them in its prologue
+ * (default on; SKAN_GEMM_FUSE_REDUCE=0 turns it off).  Both routes sum the
+ * same partials in the same f64 order, so outputs are bitwise equal.
+ * Returns the previous setting.  A test knob; not thread-safe against
+ * concurrent forwards. */
+int skan_debug_set_fuse_reduce(int on);
+
 /* ---- single-edge primitive (lutham.cpp:730-755) ----------------------- */
 
 /* Batched pli_lookup over n independent (row, g, b, x) tuples on the GPU:

@@ -102,6 +102,7 @@ _SIGS = {
     "skan_debug_gemm_tf32": (C.c_int, [_p, _p, _p, C.c_int, C.c_int, C.c_int, _p]),
     "skan_debug_gemm_timeline": (C.c_int, [_p]),
     "skan_debug_set_gemm_min_batch": (C.c_int, [C.c_int]),
+    "skan_debug_set_fuse_reduce": (C.c_int, [C.c_int]),
     "skan_profile_gemm": (C.c_int, [_p, _p, C.c_int, C.c_int, _p, C.POINTER(C.c_double)]),
     "skan_assign_indices": (C.c_int, [_p, C.c_uint64, C.c_int, _p, C.c_int, _p, C.c_uint, _p]),
 }

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -812,6 +813,13 @@ const skan::LaunchCfg* ws_plan(const skan_head* h, skan_workspace* ws, int B) {
 // bm[l&1] and its finisher writes layer l+1's into bm[(l+1)&1]; split
 // partials ping-pong between two buffers so a layer can reduce its
 // predecessor's partials while writing its own.
+// Small-batch fused split reduction (below): on unless SKAN_GEMM_FUSE_REDUCE=0
+// or skan_debug_set_fuse_reduce(0).
+std::atomic<bool> g_fuse_reduce{[] {
+    const char* e = std::getenv("SKAN_GEMM_FUSE_REDUCE");
+    return !(e && e[0] == '0');
+}()};
+
 int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::LaunchCfg* cfg, int l,
                       const double* x, int B, double* out, bool chained, cudaStream_t s) {
     auto& d = ws->d;
@@ -828,12 +836,8 @@ int launch_layer_fast(const skan_head* h, skan_workspace* ws, const skan::Launch
     // leaves its split partials to that GEMM, which reduces and brackets them
     // in its prologue (measured: batch 16 59.4 -> 55.3 us; from batch 64 the
     // separate 1184-block reduction is faster than ~90 CTAs doing it)
-    static const bool fuse_off = [] {
-        const char* e = std::getenv("SKAN_GEMM_FUSE_REDUCE");  // A/B experiment: 0 = separate reduction
-        return e && e[0] == '0';
-    }();
     auto fuses = [&](const skan::LaunchCfg& p, const skan::LaunchCfg& n) {
-        return !fuse_off && B <= 32 && p.kind == 4 && (p.persist == 0 || p.persist == 3) && n.kind == 4 &&
+        return g_fuse_reduce.load(std::memory_order_relaxed) && B <= 32 && p.kind == 4 && (p.persist == 0 || p.persist == 3) && n.kind == 4 &&
                (n.persist == 0 || n.persist == 3) && n.jt == 1;
     };
     const bool prev_fused = l > 0 && fuses(cfg[l - 1], c);
@@ -1615,3 +1619,7 @@ void swap_head_from_sections(skan_head* h, const SectionLayer* layers, int n, cu
 }
 
 }  // namespace skan
+
+extern "C" int skan_debug_set_fuse_reduce(int on) {
+    return g_fuse_reduce.exchange(on != 0) ? 1 : 0;
+}

@@ -186,6 +186,28 @@ def test_fast_mode_headline_head(torch_cuda):
             assert ws.last_launches() == batch
 
 
+def test_fused_small_batch_reduction_is_bitwise_the_separate_one(torch_cuda):
+    """At batch <= 32 layer 1's GEMM reduces layer 0's split partials in its
+    prologue; the separate k_split_reduce launch sums the same partials in
+    the same f64 order, so both routes give bitwise-equal outputs."""
+    from paper_2512_15742_b200 import _lib
+    cn = synthetic.synthetic_head()
+    model = hq.build_model(cn)
+    for batch in (3, 17, 32):
+        x = synthetic.synthetic_inputs(batch, 2048, seed=40 + batch)
+        prev = _lib.lib().skan_debug_set_fuse_reduce(1)
+        try:
+            fused, ws = _gpu_forward(model, x, batch, "fast")
+            n_fused = ws.last_launches()
+            _lib.lib().skan_debug_set_fuse_reduce(0)
+            sep, ws = _gpu_forward(model, x, batch, "fast")
+            n_sep = ws.last_launches()
+        finally:
+            _lib.lib().skan_debug_set_fuse_reduce(prev)
+        assert n_sep == n_fused + 1
+        assert np.array_equal(_bits(fused), _bits(sep))
+
+
 def test_fast_mode_bitwise_reproducible(torch_cuda):
     cn = synthetic.synthetic_head(dims=(512, 300, 20), k=4096, grid=10, int8=True, seed=5)
     model = hq.build_model(cn)
