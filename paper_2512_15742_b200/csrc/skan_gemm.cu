@@ -1366,6 +1366,41 @@ __global__ void k_split_reduce(FwdArgs a, int nsplit, int add_bias) {
     }
 }
 
+// The same reduction when a next layer needs brackets, through a 32 x 32
+// (sample x output) tile: the partial loads and y stores run along the
+// outputs, the input-major bracket stores ([j][B]) along the samples, both
+// coalesced (one thread per entry wrote the brackets 4 bytes at a B-sample
+// stride: ~12 us at bs256 for 360k entries).  One entry per thread, 1024
+// threads per tile.  Same sums, same order as k_split_reduce.
+__global__ void __launch_bounds__(1024) k_split_reduce_t(FwdArgs a, int nsplit, int add_bias) {
+    __shared__ int s_m[32][33];
+    __shared__ float s_t[32][33];
+    pdl_trigger();
+    pdl_wait();
+    const DevLayer& L = a.L;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 32: one entry per thread
+    const int j0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+    const size_t plane = static_cast<size_t>(a.B) * L.out;
+    const int j = j0 + tx, sm = s0 + ty;
+    int m = 0;
+    float t = 0.f;
+    if (sm < a.B && j < L.out) {
+        const size_t p = static_cast<size_t>(sm) * L.out + j;
+        double w = ordered_plane_sum(a.partial + p, plane, 0, 1, nsplit);
+        if (add_bias && L.bias_sum) w += L.bias_sum[j];
+        a.y[p] = w;
+        fast_locate(a.N, w, a.err, m, t);
+    }
+    s_m[ty][tx] = m;
+    s_t[ty][tx] = t;
+    __syncthreads();
+    const int jj = j0 + ty, s2 = s0 + tx;
+    if (jj < L.out && s2 < a.B) {
+        a.bm_out[static_cast<size_t>(jj) * a.B + s2] = s_m[tx][ty];
+        a.bt_out[static_cast<size_t>(jj) * a.B + s2] = s_t[tx][ty];
+    }
+}
+
 // Many splits, few entries (narrow layers): one warp per entry, lane l sums
 // splits l, l+32, ... in order, then a fixed butterfly.
 __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
@@ -1875,6 +1910,23 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStre
     cuda_check(cudaLaunchKernelEx(&cfg, kernel, args...), "kernel launch");
 }
 
+// k_split_reduce(_t) launch: the tiled form when a next layer takes brackets
+// (SKAN_SPLIT_REDUCE_T=0: the one-thread-per-entry form, for A/B)
+void launch_split_reduce(const FwdArgs& a, int nsplit, int add_bias, cudaStream_t s) {
+    static const bool t_off = [] {
+        const char* e = std::getenv("SKAN_SPLIT_REDUCE_T");
+        return e && e[0] == '0';
+    }();
+    if (a.has_next && !t_off) {
+        launch_pdl(k_split_reduce_t, dim3((a.L.out + 31) / 32, (a.B + 31) / 32), dim3(1024), 0, true, s, a, nsplit,
+                   add_bias);
+        return;
+    }
+    const long long n = static_cast<long long>(a.B) * a.L.out;
+    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
+    launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, nsplit, add_bias);
+}
+
 }  // namespace
 
 // Inputs per chunk: IC*G must be a multiple of the tf32 MMA K (8), and IC
@@ -2108,6 +2160,8 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
                 const char* e = std::getenv("SKAN_DENSE_REDUCE_BLOCKS");  // experiment: grid cap per SM
                 return e ? std::max(1, std::atoi(e)) : 64;  // one output per thread at cfg4
             }();
+            // (a tiled form with coalesced bracket stores, as k_split_reduce_t,
+            // measured no faster here: cfg4's reduction overlaps the narrow tail)
             const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * cap));
             launch_pdl(k_dense_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, units, c.jt);
         }
@@ -2133,8 +2187,7 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
         const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
         launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
     } else {
-        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
-        launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+        launch_split_reduce(a, c.nsplit, 0, s);
     }
     return 2;
 }
@@ -2180,8 +2233,7 @@ int launch_dense_narrow(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStr
         const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
         launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
     } else {
-        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 8));
-        launch_pdl(k_split_reduce, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+        launch_split_reduce(a, c.nsplit, 0, s);
     }
     return 2;
 }
