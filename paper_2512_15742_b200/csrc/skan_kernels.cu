@@ -64,32 +64,28 @@ __global__ void k_locate_input(const double* __restrict__ x, long long n, DevLay
 // Fast-path brackets of x [rows][width] written input-major ([width][rows])
 // through a 32 x 32 shared-memory tile: both the read of x and the write of
 // the brackets are coalesced.
-__global__ void __launch_bounds__(256) k_locate_transpose(const double* __restrict__ x, int rows, int width,
-                                                         DevLayer L, int* __restrict__ bm, float* __restrict__ bt,
-                                                         int* __restrict__ err) {
+__global__ void __launch_bounds__(1024) k_locate_transpose(const double* __restrict__ x, int rows, int width,
+                                                          DevLayer L, int* __restrict__ bm, float* __restrict__ bt,
+                                                          int* __restrict__ err) {
     __shared__ int s_m[32][33];
     __shared__ float s_t[32][33];
     pdl_trigger();
     pdl_wait();
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 32: one entry per thread
     const int i0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int r = r0 + ty + 8 * k, i = i0 + tx;
+    {
+        const int r = r0 + ty, i = i0 + tx;
         int m = 0;
         float t = 0.f;
         if (r < rows && i < width) fast_locate(L, x[static_cast<size_t>(r) * width + i], err, m, t);
-        s_m[ty + 8 * k][tx] = m;
-        s_t[ty + 8 * k][tx] = t;
+        s_m[ty][tx] = m;
+        s_t[ty][tx] = t;
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = i0 + ty + 8 * k, r = r0 + tx;
-        if (r < rows && i < width) {
-            bm[static_cast<size_t>(i) * rows + r] = s_m[tx][ty + 8 * k];
-            bt[static_cast<size_t>(i) * rows + r] = s_t[tx][ty + 8 * k];
-        }
+    const int i = i0 + ty, r = r0 + tx;
+    if (r < rows && i < width) {
+        bm[static_cast<size_t>(i) * rows + r] = s_m[tx][ty];
+        bt[static_cast<size_t>(i) * rows + r] = s_t[tx][ty];
     }
 }
 
@@ -1374,7 +1370,7 @@ void launch_locate_input(const double* x, int n_rows, int width, const DevLayer&
     const long long n = static_cast<long long>(n_rows) * width;
     if (n == 0) return;
     if (input_major && !btd) {
-        k_locate_transpose<<<dim3((width + 31) / 32, (n_rows + 31) / 32), 256, 0, s>>>(x, n_rows, width, L, bm, btf,
+        k_locate_transpose<<<dim3((width + 31) / 32, (n_rows + 31) / 32), 1024, 0, s>>>(x, n_rows, width, L, bm, btf,
                                                                                       err);
         return;
     }
