@@ -1403,19 +1403,29 @@ __global__ void __launch_bounds__(1024) k_split_reduce_t(FwdArgs a, int nsplit, 
 
 // Many splits, few entries (narrow layers): one warp per entry, lane l sums
 // splits l, l+32, ... in order, then a fixed butterfly.
+// LP lanes per entry (32 / LP consecutive entries per warp): with fewer
+// splits, 8 or 16 lanes each keep more loads in flight and a warp's loads
+// cover LP planes x 32 / LP adjacent entries instead of 32 planes x 1.
+template <int LP>
 __global__ void k_split_reduce_warp(FwdArgs a, int nsplit, int add_bias) {
     pdl_trigger();
     pdl_wait();
     const size_t plane = static_cast<size_t>(a.B) * a.L.out;
-    const int lane = threadIdx.x & 31;
-    for (size_t p = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / 32; p < plane;
-         p += static_cast<size_t>(gridDim.x) * blockDim.x / 32) {
-        double v = ordered_plane_sum(a.partial + p, plane, lane, 32, nsplit);
+    const int lane = threadIdx.x & (LP - 1);
+    const size_t g = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) / LP;
+    const size_t gstep = static_cast<size_t>(gridDim.x) * blockDim.x / LP;
+    // every lane of a warp runs the same number of iterations (the shuffles)
+    const size_t iters = (plane + gstep - 1) / gstep;
+    for (size_t it = 0; it < iters; ++it) {
+        const size_t p = g + it * gstep;
+        double v = p < plane ? ordered_plane_sum(a.partial + p, plane, lane, LP, nsplit) : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-        if (lane == 0) reduce_finish(a, p, v, add_bias);
+        for (int o = LP >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        if (lane == 0 && p < plane) reduce_finish(a, p, v, add_bias);
     }
 }
+
+void launch_split_reduce_warp(const FwdArgs& a, int nsplit, int add_bias, bool pdl, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // The same persistent dense schedule in fp16 split precision (kind::f16: K =
@@ -1910,6 +1920,21 @@ void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStre
     cuda_check(cudaLaunchKernelEx(&cfg, kernel, args...), "kernel launch");
 }
 
+// k_split_reduce_warp launch: lanes per entry from the split count
+void launch_split_reduce_warp(const FwdArgs& a, int nsplit, int add_bias, bool pdl, cudaStream_t s) {
+    static const int lp_env = [] {
+        const char* e = std::getenv("SKAN_REDUCE_LANES");  // A/B experiment: force 8, 16 or 32
+        return e ? std::atoi(e) : 0;
+    }();
+    const int lp = lp_env == 8 || lp_env == 16 || lp_env == 32 ? lp_env : (nsplit <= 96 ? 8 : (nsplit <= 192 ? 16 : 32));
+    const long long n = static_cast<long long>(a.B) * a.L.out;
+    const int blocks = static_cast<int>(std::min<long long>((n * lp + 255) / 256, 148LL * 16));
+    const dim3 g(blocks > 0 ? blocks : 1);
+    if (lp == 8) launch_pdl(k_split_reduce_warp<8>, g, dim3(256), 0, pdl, s, a, nsplit, add_bias);
+    else if (lp == 16) launch_pdl(k_split_reduce_warp<16>, g, dim3(256), 0, pdl, s, a, nsplit, add_bias);
+    else launch_pdl(k_split_reduce_warp<32>, g, dim3(256), 0, pdl, s, a, nsplit, add_bias);
+}
+
 // k_split_reduce(_t) launch: the tiled form when a next layer takes brackets
 // (SKAN_SPLIT_REDUCE_T=0: the one-thread-per-entry form, for A/B)
 void launch_split_reduce(const FwdArgs& a, int nsplit, int add_bias, cudaStream_t s) {
@@ -2184,8 +2209,7 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
     // bias: folded into W for compressed layers; dense layers have none
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
-        const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
-        launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+        launch_split_reduce_warp(a, c.nsplit, 0, true, s);
     } else {
         launch_split_reduce(a, c.nsplit, 0, s);
     }
@@ -2230,8 +2254,7 @@ int launch_dense_narrow(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStr
     launch_pdl(k_dense_narrow, dim3(c.nsplit), dim3(kNarrowT), c.smem, pdl, s, a);
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
-        const int blocks = static_cast<int>(std::min<long long>((n * 32 + 255) / 256, 148LL * 16));
-        launch_pdl(k_split_reduce_warp, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, true, s, a, c.nsplit, 0);
+        launch_split_reduce_warp(a, c.nsplit, 0, true, s);
     } else {
         launch_split_reduce(a, c.nsplit, 0, s);
     }
