@@ -2136,11 +2136,13 @@ double gemm_issued_flops(const DevLayer& L, const LaunchCfg& c, int B) {
     if (c.persist == 1 || c.persist == 2)  // one M=128 x N=256 x K=8 MMA per K step of every (tile, chunk)
         return static_cast<double>((L.out + kGmN - 1) / kGmN) * c.dn_nch * (c.ic * L.G / 8) * 2.0 * kGmM * 8 *
                (2 * kGmN);
-    // per CTA and K = 8 step: one M=128 x N=256 MMA, plus (not stacked) one N=128
+    // per 128-sample half and K = 8 step: one M=128 x N=256 MMA, plus (not
+    // stacked) one N=128; dual-half tiles run two halves per CTA
     const double ksteps = static_cast<double>((L.in + c.ic - 1) / c.ic) * c.ic * L.G / 8.0;
     const double per_step = 2.0 * kGmM * 8 * (2 * kGmN + (c.spt == 64 ? 0 : kGmN));
+    const double halves = c.spt == 2 * kGmM ? 2.0 : 1.0;
     (void)B;
-    return ksteps * per_step * c.jt * c.st;
+    return ksteps * per_step * halves * c.jt * c.st;
 }
 
 unsigned long long* g_gemm_dbg = nullptr;
