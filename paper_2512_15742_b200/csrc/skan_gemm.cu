@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             float* dst = a.partial + pz * plane + static_cast<size_t>(s0 + min(as, nS > 0 ? nS - 1 : 0)) * L.out + j0;
             const uint32_t tacc = tmem + hf * 2 * kGmN;
 #pragma unroll 1
-            for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+            for (int c8 = cq * 32; c8 < cq * 32 + 32 && c8 < nJ; c8 += 8) {  // (warp-uniform: narrow tiles skip)
                 float v[8], w[8];
                 if (nchunks > 0) {
                     tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(kGmT, 1) k_layer_gemm(FwdArgs a) {
             const int vr = hf * kGmM + q4 * 32 + lane;
             const uint32_t tacc = tmem + hf * 2 * kGmN;
 #pragma unroll 1
-            for (int c8 = cq * 32; c8 < cq * 32 + 32; c8 += 8) {
+            for (int c8 = cq * 32; c8 < cq * 32 + 32 && c8 < nJ; c8 += 8) {  // (warp-uniform: narrow tiles skip)
                 float v[8], w[8];
                 if (nchunks > 0) {
                     tc::tmem_ld8(tacc + (static_cast<uint32_t>(q4 * 32) << 16) + c8, v);
