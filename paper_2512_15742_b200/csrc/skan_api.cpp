@@ -901,22 +901,29 @@ int enqueue_chunk(const skan_head* h, skan_workspace* ws, const double* x, int B
     auto& d = ws->d;
     int launches = 0;
     if (exact) {
-        skan::launch_locate_input(x, B, h->dl[0].in, h->dl[0], d.bm, d.btf, d.btd, d.err, s);
-        ++launches;
+        // each layer brackets its own input (layer l: x or layer l-1's output)
+        const double* xin = x;
         for (int l = 0; l < nl; ++l) {
             const DevLayer& L = h->dl[l];
             const DevLayer* next = l + 1 < nl ? &h->dl[l + 1] : nullptr;
             double* out = next ? d.act[l & 1] : y;
+            const int b1 = B == 1 && exact_split_max() >= 1 && ws->ex_terms
+                               ? skan::launch_exact_b1(L, xin, d.bm, d.btf, d.btd, d.err, out, ws->ex_terms,
+                                                       ws->ex_doubles, ws->ex_acc, s)
+                               : 0;
+            xin = out;
+            if (b1) {
+                launches += b1;
+                continue;
+            }
+            skan::launch_locate_input(l == 0 ? x : d.act[(l - 1) & 1], B, L.in, L, d.bm, d.btf, d.btd, d.err, s);
+            ++launches;
             if (B <= exact_split_max() && ws->ex_terms) {
                 launches += skan::launch_exact_split(L, B, d.bm, d.btd, out, ws->ex_terms, ws->ex_doubles,
                                                      ws->ex_acc, s);
             } else {
                 const skan::LaunchCfg c = skan::choose_cfg(L, B, true, h->num_sms);
                 skan::launch_gather_exact(L, c, B, d.bm, d.btd, out, s);
-                ++launches;
-            }
-            if (next) {
-                skan::launch_locate_input(out, B, L.out, *next, d.bm, d.btf, d.btd, d.err, s);
                 ++launches;
             }
         }

@@ -242,6 +242,11 @@ void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int
 // launches made.
 constexpr int kExactSplitMaxBatch = 128;
 constexpr size_t kExactTermBytes = 256ull << 20;
+// Exact mode, batch 1, int8 layer with pair planes: brackets + their order in
+// one launch, the plane-ordered terms, the in-order sums (3 launches); 0 when
+// the layer does not qualify (the caller takes the general path).
+int launch_exact_b1(const DevLayer& L, const double* xin, int* bm, float* btf, double* btd, int* err, double* y,
+                    double* terms, size_t term_doubles, double* acc, cudaStream_t s);
 int launch_exact_split(const DevLayer& L, int B, const int* bm, const double* btd, double* y, double* terms,
                        size_t term_doubles, double* acc, cudaStream_t s);
 void launch_locate_raw(const double* x, int n, double lo, double hi, int G, int* idx,

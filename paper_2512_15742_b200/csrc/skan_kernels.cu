@@ -964,16 +964,29 @@ __global__ void __launch_bounds__(256) k_exact_terms(DevLayer L, int B, const in
 // m (c[k][m] | c[k][m+1] << 8, the same int8 codes as the codebook row), so a
 // CTA working through inputs of one bracket keeps that 128 KB plane in L1
 // instead of pulling a 32-byte sector of a random codebook row per edge from
-// L2.  k_exact_order sorts each sample's inputs by bracket (a counting sort;
-// the order within a bracket is irrelevant: terms land at their input's slot).
-__global__ void __launch_bounds__(256) k_exact_order(const int* __restrict__ bm, int in, int nb,
-                                                      int* __restrict__ order) {
+// L2.  k_exact_locate_order brackets the inputs and sorts them by bracket (a
+// counting sort; the order within a bracket is irrelevant: terms land at
+// their input's slot).  Batch 1 only: from batch 2 the sample-grouped
+// kernel, which decodes each record once for up to 16 samples, is faster.
+// Batch 1: the layer's exact brackets (k_locate_input's bracket_of) and
+// their counting sort in one block, one launch instead of two.
+__global__ void __launch_bounds__(1024) k_exact_locate_order(const double* __restrict__ x, DevLayer L,
+                                                             int* __restrict__ bm, float* __restrict__ btf,
+                                                             double* __restrict__ btd, int* __restrict__ err,
+                                                             int* __restrict__ order) {
     __shared__ int cnt[64], off[64];
-    const int sm = blockIdx.x;
+    const int nb = L.G - 1, in = L.in;
     if (threadIdx.x < 64) cnt[threadIdx.x] = 0;
     __syncthreads();
-    const int* b = bm + static_cast<size_t>(sm) * in;
-    for (int i = threadIdx.x; i < in; i += blockDim.x) atomicAdd(&cnt[min(max(b[i], 0), nb - 1)], 1);
+    for (int i = threadIdx.x; i < in; i += blockDim.x) {
+        int m;
+        double t;
+        bracket_of(L.lo, L.hi, L.G, L.dx, x[i], err, m, t);
+        btf[i] = static_cast<float>(t);
+        btd[i] = t;
+        bm[i] = m;
+        atomicAdd(&cnt[min(max(m, 0), nb - 1)], 1);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         int a = 0;
@@ -984,8 +997,8 @@ __global__ void __launch_bounds__(256) k_exact_order(const int* __restrict__ bm,
     }
     __syncthreads();
     for (int i = threadIdx.x; i < in; i += blockDim.x) {
-        const int pos = atomicAdd(&off[min(max(b[i], 0), nb - 1)], 1);
-        order[static_cast<size_t>(sm) * in + pos] = i;
+        const int pos = atomicAdd(&off[min(max(bm[i], 0), nb - 1)], 1);
+        order[pos] = i;
     }
 }
 
@@ -1077,55 +1090,33 @@ __global__ void __launch_bounds__(32) k_exact_sum(int out, int ni, const double*
     else acc[q] = a;
 }
 
+// the in-order sums of one term block (first: acc starts at 0, last: write y)
+void launch_exact_sum(int out, int B, int ni, const double* terms, double* acc, double* y, cudaStream_t s,
+                      int first = 1, int last = 1) {
+    static const bool attr = [] {  // 64 KB of dynamic shared memory and more (opt-in above 48 KB)
+        return cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    4 * kExKc * 32 * 8) == cudaSuccess &&
+               cudaFuncSetAttribute(k_exact_sum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * kExKc * 32 * 8) == cudaSuccess;
+    }();
+    (void)attr;
+    const int nb = B * ((out + 31) / 32);
+    if (nb <= 2 * 148) k_exact_sum<4><<<nb, 32, 4 * kExKc * 32 * 8, s>>>(out, ni, terms, acc, y, first, last);
+    else k_exact_sum<2><<<nb, 32, 2 * kExKc * 32 * 8, s>>>(out, ni, terms, acc, y, first, last);
+}
+
 template <int FMT>
 int dispatch_exact_split(const DevLayer& L, int B, const int* bm, const double* btd, double* y, double* terms,
                          size_t term_doubles, double* acc, cudaStream_t s) {
     const size_t outp = static_cast<size_t>((L.out + 31) / 32) * 32;  // the blocked term layout pads outputs
     const int per = static_cast<int>(std::max<size_t>(1, term_doubles / (static_cast<size_t>(B) * outp)));
     int launches = 0;
-    if constexpr (FMT == FMT_I8_R32) {
-        // batch 1 (one term block, room for the bracket order after it): the
-        // plane-ordered terms.  Measured 74.7 -> 70.8 us at batch 1; from batch
-        // 2 the sample-grouped kernel, which decodes each record once for up
-        // to four samples, is faster (85 vs 87 us at 2, 171 vs 200 at 8)
-        const size_t need = static_cast<size_t>(B) * outp * L.in, order_d = (static_cast<size_t>(B) * L.in + 1) / 2;
-        if (B == 1 && per >= L.in && L.pair8 && L.K > 0 && need + order_d <= term_doubles && L.G - 1 <= 64) {
-            int* order = reinterpret_cast<int*>(terms + need);
-            k_exact_order<<<B, 256, 0, s>>>(bm, L.in, L.G - 1, order);
-            const size_t n = static_cast<size_t>(L.in) * L.out * B;
-            const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 64));
-            k_exact_terms_planes<<<blocks, 256, 0, s>>>(L, B, bm, btd, order, terms);
-            const int nb = B * ((L.out + 31) / 32);
-            static const bool attr = [] {
-                return cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            4 * kExKc * 32 * 8) == cudaSuccess &&
-                       cudaFuncSetAttribute(k_exact_sum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            2 * kExKc * 32 * 8) == cudaSuccess;
-            }();
-            (void)attr;
-            if (nb <= 2 * 148) k_exact_sum<4><<<nb, 32, 4 * kExKc * 32 * 8, s>>>(L.out, L.in, terms, acc, y, 1, 1);
-            else k_exact_sum<2><<<nb, 32, 2 * kExKc * 32 * 8, s>>>(L.out, L.in, terms, acc, y, 1, 1);
-            return 3;
-        }
-    }
     for (int i0 = 0; i0 < L.in; i0 += per) {
         const int ni = std::min(per, L.in - i0);
         const size_t n = static_cast<size_t>(ni) * L.out * ((B + 15) / 16);
         const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 64));
         k_exact_terms<FMT><<<blocks > 0 ? blocks : 1, 256, 0, s>>>(L, B, bm, btd, i0, ni, terms);
-        const int nb = B * ((L.out + 31) / 32), f = i0 == 0 ? 1 : 0, la = i0 + ni >= L.in ? 1 : 0;
-        static const bool attr = [] {  // 128 KB of dynamic shared memory (opt-in above 48 KB)
-            return cudaFuncSetAttribute(k_exact_sum<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        4 * kExKc * 32 * 8) == cudaSuccess &&
-                   cudaFuncSetAttribute(k_exact_sum<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        2 * kExKc * 32 * 8) == cudaSuccess;
-        }();
-        (void)attr;
-        if (nb <= 2 * 148) {
-            k_exact_sum<4><<<nb, 32, 4 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
-        } else {
-            k_exact_sum<2><<<nb, 32, 2 * kExKc * 32 * 8, s>>>(L.out, ni, terms, acc, y, f, la);
-        }
+        launch_exact_sum(L.out, B, ni, terms, acc, y, s, i0 == 0 ? 1 : 0, i0 + ni >= L.in ? 1 : 0);
         launches += 2;
     }
     return launches;
@@ -1420,6 +1411,21 @@ int launch_exact_split(const DevLayer& L, int B, const int* bm, const double* bt
         case FMT_F32: return dispatch_exact_split<FMT_F32>(L, B, bm, btd, y, terms, term_doubles, acc, s);
         default: return dispatch_exact_split<FMT_DENSE>(L, B, bm, btd, y, terms, term_doubles, acc, s);
     }
+}
+
+int launch_exact_b1(const DevLayer& L, const double* xin, int* bm, float* btf, double* btd, int* err, double* y,
+                    double* terms, size_t term_doubles, double* acc, cudaStream_t s) {
+    if (L.fmt != FMT_I8_R32 || !L.pair8 || L.K <= 0 || L.G - 1 > 64) return 0;
+    const size_t outp = static_cast<size_t>((L.out + 31) / 32) * 32;
+    const size_t need = outp * L.in, order_d = (static_cast<size_t>(L.in) + 1) / 2;
+    if (need + order_d > term_doubles) return 0;
+    int* order = reinterpret_cast<int*>(terms + need);
+    k_exact_locate_order<<<1, 1024, 0, s>>>(xin, L, bm, btf, btd, err, order);
+    const size_t n = static_cast<size_t>(L.in) * L.out;
+    const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, 148ull * 64));
+    k_exact_terms_planes<<<blocks, 256, 0, s>>>(L, 1, bm, btd, order, terms);
+    launch_exact_sum(L.out, 1, L.in, terms, acc, y, s);
+    return 3;
 }
 
 void launch_gather_exact(const DevLayer& L, const LaunchCfg& c, int B, const int* bm,
