@@ -1850,6 +1850,7 @@ __device__ __forceinline__ bool bulk_ok(const void* p, size_t bytes) {
     return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (bytes & 15) == 0 && bytes > 0 && bytes < (1u << 20);
 }
 
+template <int FMT>
 __global__ void __launch_bounds__(kNarrowT) k_dense_narrow(FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t s_bar[2];  // [0] grid slice, [1] brackets
@@ -1862,8 +1863,8 @@ __global__ void __launch_bounds__(kNarrowT) k_dense_narrow(FwdArgs a) {
     int* s_bm = reinterpret_cast<int*>(smem + ((gfl * 4 + 15) & ~static_cast<size_t>(15)));  // [nr][B]
     const size_t nb = static_cast<size_t>(nr) * B, boff = static_cast<size_t>(i0) * B;
     float* s_bt = reinterpret_cast<float*>(s_bm + ((nb + 3) & ~static_cast<size_t>(3)));
-    const float* gsrc = L.cb32 + static_cast<size_t>(i0) * out * G;
-    const bool gbulk = bulk_ok(gsrc, gfl * 4);
+    const float* gsrc = FMT == FMT_DENSE ? L.cb32 + static_cast<size_t>(i0) * out * G : nullptr;
+    const bool gbulk = FMT == FMT_DENSE && bulk_ok(gsrc, gfl * 4);
     const bool bbulk = bulk_ok(a.bm_in + boff, nb * 4) && bulk_ok(a.bt_in + boff, nb * 4);
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
@@ -1873,7 +1874,22 @@ __global__ void __launch_bounds__(kNarrowT) k_dense_narrow(FwdArgs a) {
             bulk_g2s(s_grid, gsrc, static_cast<uint32_t>(gfl * 4), &s_bar[0]);
         }
     }
-    if (!gbulk) stage_words(reinterpret_cast<uint32_t*>(s_grid), reinterpret_cast<const uint32_t*>(gsrc), gfl, tid);
+    if constexpr (FMT == FMT_I8_R32) {
+        // the rows' per-edge grids decoded from the records (g c[m]; the bias
+        // sums are added by the reduction), before the programmatic wait
+        const size_t ne = static_cast<size_t>(nr) * out;
+        for (size_t e = tid; e < ne; e += kNarrowT) {
+            const uint32_t r = __ldg(L.rec + static_cast<size_t>(i0) * out + e);
+            const float g = __ldg(L.lutf + ((r >> 16) & 0xFFu));
+            const uint4 row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(r & 0xFFFFu) * L.rs));
+            const uint32_t w[4] = {row.x, row.y, row.z, row.w};
+#pragma unroll
+            for (int m = 0; m < 16; ++m)
+                if (m < G) s_grid[e * G + m] = g * static_cast<float>(static_cast<int8_t>((w[m >> 2] >> (8 * (m & 3))) & 0xFFu));
+        }
+    } else if (!gbulk) {
+        stage_words(reinterpret_cast<uint32_t*>(s_grid), reinterpret_cast<const uint32_t*>(gsrc), gfl, tid);
+    }
     pdl_trigger();
     pdl_wait();  // the brackets come from the previous kernel
     if (bbulk) {
@@ -2218,10 +2234,19 @@ int launch_layer_gemm(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStrea
     return 2;
 }
 
+static bool narrow_i8_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("SKAN_NARROW_I8");  // A/B experiment: 0 = narrow int8 layers on the GEMM
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool dense_narrow_ok(const DevLayer& L) {
-    // one input row of the grid plus the brackets of 512 samples must fit the staging
-    return L.fmt == FMT_DENSE && !L.wt && L.out <= 32 && L.G >= 2 &&
-           static_cast<size_t>(L.out) * L.G * 4 + 16 + 512 * 8 <= 100 * 1024;
+    // one input row of the grid plus the brackets of 512 samples must fit the
+    // staging; int8 layers (records decoded in the kernel) with 16-byte rows
+    const bool fmt_ok = (L.fmt == FMT_DENSE && !L.wt) || (L.fmt == FMT_I8_R32 && L.G <= 16 && narrow_i8_on());
+    return fmt_ok && L.out <= 32 && L.G >= 2 && static_cast<size_t>(L.out) * L.G * 4 + 16 + 512 * 8 <= 100 * 1024;
 }
 
 size_t dense_narrow_smem(const DevLayer& L, int B, int rows) {
@@ -2238,7 +2263,8 @@ LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms) {
         const char* e = std::getenv("SKAN_NARROW_PER_SM");  // experiment: CTAs per SM
         return e ? std::max(1, std::atoi(e)) : 2;
     }();
-    int splits = std::min(L.in, per_sm * sms);
+    // (int8: one CTA per SM, fewer partial planes; its staging is small)
+    int splits = std::min(L.in, (L.fmt == FMT_DENSE ? per_sm : 1) * sms);
     int rows = (L.in + splits - 1) / splits;
     while (rows > 1 && dense_narrow_smem(L, B, rows) > 100 * 1024) rows = (rows + 1) / 2;
     c.ichunk = rows;
@@ -2252,13 +2278,17 @@ LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms) {
 int launch_dense_narrow(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
     FwdArgs a = a0;
     a.rows_per_cta = c.ichunk;
-    ensure_smem(k_dense_narrow, c.smem);
-    launch_pdl(k_dense_narrow, dim3(c.nsplit), dim3(kNarrowT), c.smem, pdl, s, a);
+    void (*k)(FwdArgs) = a.L.fmt == FMT_DENSE ? k_dense_narrow<FMT_DENSE> : k_dense_narrow<FMT_I8_R32>;
+    ensure_smem(k, c.smem);
+    launch_pdl(k, dim3(c.nsplit), dim3(kNarrowT), c.smem, pdl, s, a);
+    // int8 partials exclude the edges' biases: their per-output sums are added
+    // here (dense layers have none)
+    const int add_bias = a.L.fmt == FMT_DENSE ? 0 : 1;
     const long long n = static_cast<long long>(a.B) * a.L.out;
     if (c.nsplit >= 16 && n < 148LL * 256) {
-        launch_split_reduce_warp(a, c.nsplit, 0, true, s);
+        launch_split_reduce_warp(a, c.nsplit, add_bias, true, s);
     } else {
-        launch_split_reduce(a, c.nsplit, 0, s);
+        launch_split_reduce(a, c.nsplit, add_bias, s);
     }
     return 2;
 }

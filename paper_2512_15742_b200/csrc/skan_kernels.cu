@@ -1310,7 +1310,10 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
     }();
     // (up to batch 512: above it the staged brackets leave few rows per CTA and
     // the split partials grow with the batch; the generic kernels take over)
-    if (B >= g_gemm_min_batch && B <= 512 && dense_narrow_ok(L)) return dense_narrow_cfg(L, B, sms);
+    // (int8 layers only up to batch 16: from there the one-tile GEMM and its
+    // 88-plane reduction beat the narrow kernel's 148 planes; batch 256 98 vs 107 us)
+    if (B >= g_gemm_min_batch && B <= (L.fmt == FMT_DENSE ? 512 : 16) && dense_narrow_ok(L))
+        return dense_narrow_cfg(L, B, sms);
     if (B >= g_gemm_min_batch && L.out >= gemm_min_out && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
     if (i8 && L.G <= 16 && B >= 64) {

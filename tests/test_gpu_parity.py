@@ -189,12 +189,13 @@ def test_fast_mode_headline_head(torch_cuda):
 def test_fused_small_batch_reduction_is_bitwise_the_separate_one(torch_cuda):
     """At batch <= 32 layer 1's GEMM reduces layer 0's split partials in its
     prologue; the separate k_split_reduce launch sums the same partials in
-    the same f64 order, so both routes give bitwise-equal outputs."""
+    the same f64 order, so both routes give bitwise-equal outputs.  (A last
+    layer of 33-128 outputs: narrower int8 layers take k_dense_narrow.)"""
     from paper_2512_15742_b200 import _lib
-    cn = synthetic.synthetic_head()
+    cn = synthetic.synthetic_head(dims=(1024, 512, 64), k=4096, seed=9)
     model = hq.build_model(cn)
     for batch in (3, 17, 32):
-        x = synthetic.synthetic_inputs(batch, 2048, seed=40 + batch)
+        x = synthetic.synthetic_inputs(batch, 1024, seed=40 + batch)
         prev = _lib.lib().skan_debug_set_fuse_reduce(1)
         try:
             fused, ws = _gpu_forward(model, x, batch, "fast")
