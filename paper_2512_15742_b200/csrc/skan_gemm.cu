@@ -1921,6 +1921,107 @@ __global__ void __launch_bounds__(kNarrowT) k_dense_narrow(FwdArgs a) {
     }
 }
 
+// int8 narrow layers: the rows' per-edge grids decoded knot-major (see below)
+template <int FMT>
+__global__ void __launch_bounds__(kNarrowT) k_narrow_knot(FwdArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t s_bar;  // brackets
+    const DevLayer& L = a.L;
+    const int B = a.B, out = L.out, G = L.G, outp = (out + 3) & ~3;
+    const int i0 = blockIdx.x * a.rows_per_cta, nr = min(a.rows_per_cta, L.in - i0);
+    const int tid = threadIdx.x;
+    // the rows' grid slice knot-major, [nr][G][outp]: a knot's outputs are
+    // contiguous, so one 16-byte load serves four outputs of a sample
+    float* s_grid = reinterpret_cast<float*>(smem);
+    const size_t gfl = static_cast<size_t>(nr) * G * outp;
+    int* s_bm = reinterpret_cast<int*>(smem + ((gfl * 4 + 15) & ~static_cast<size_t>(15)));  // [nr][B]
+    const size_t nb = static_cast<size_t>(nr) * B, boff = static_cast<size_t>(i0) * B;
+    float* s_bt = reinterpret_cast<float*>(s_bm + ((nb + 3) & ~static_cast<size_t>(3)));
+    const bool bbulk = bulk_ok(a.bm_in + boff, nb * 4) && bulk_ok(a.bt_in + boff, nb * 4);
+    if (tid == 0) mbar_init(&s_bar, 1);
+    // the slice does not depend on the previous kernel: before the programmatic wait
+    const size_t ne = static_cast<size_t>(nr) * out;
+    if constexpr (FMT == FMT_I8_R32) {
+        // per-edge grids decoded from the records (g c[m]; the bias sums are
+        // added by the reduction)
+        for (size_t e = tid; e < ne; e += kNarrowT) {
+            const int r = static_cast<int>(e / out), j = static_cast<int>(e - static_cast<size_t>(r) * out);
+            const uint32_t rec = __ldg(L.rec + static_cast<size_t>(i0) * out + e);
+            const float g = __ldg(L.lutf + ((rec >> 16) & 0xFFu));
+            const uint4 row = __ldg(reinterpret_cast<const uint4*>(L.cb8 + static_cast<size_t>(rec & 0xFFFFu) * L.rs));
+            const uint32_t w[4] = {row.x, row.y, row.z, row.w};
+#pragma unroll
+            for (int m = 0; m < 16; ++m)
+                if (m < G)
+                    s_grid[(static_cast<size_t>(r) * G + m) * outp + j] =
+                        g * static_cast<float>(static_cast<int8_t>((w[m >> 2] >> (8 * (m & 3))) & 0xFFu));
+        }
+    } else {
+        // natural [i][out][G] rows, read coalesced and stored knot-major
+        const float* src = L.cb32 + static_cast<size_t>(i0) * out * G;
+        const size_t n = ne * G;
+        size_t e = tid;
+        for (; e + 7 * kNarrowT < n; e += 8 * kNarrowT) {
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(src + e + u * kNarrowT);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const size_t q = e + u * kNarrowT, rj = q / G;
+                const int m = static_cast<int>(q - rj * G), r = static_cast<int>(rj / out), j = static_cast<int>(rj - static_cast<size_t>(r) * out);
+                s_grid[(static_cast<size_t>(r) * G + m) * outp + j] = v[u];
+            }
+        }
+        for (; e < n; e += kNarrowT) {
+            const size_t rj = e / G;
+            const int m = static_cast<int>(e - rj * G), r = static_cast<int>(rj / out), j = static_cast<int>(rj - static_cast<size_t>(r) * out);
+            s_grid[(static_cast<size_t>(r) * G + m) * outp + j] = __ldg(src + e);
+        }
+    }
+    if (outp != out) {  // padding outputs read as zeros
+        for (size_t e = tid; e < static_cast<size_t>(nr) * G * (outp - out); e += kNarrowT) {
+            const size_t rm = e / (outp - out);
+            s_grid[rm * outp + out + (e - rm * (outp - out))] = 0.f;
+        }
+    }
+    pdl_trigger();
+    pdl_wait();  // the brackets come from the previous kernel
+    __syncthreads();  // the barrier init
+    if (bbulk) {
+        if (tid == 0) {
+            mbar_expect_tx(&s_bar, static_cast<uint32_t>(nb * 8));
+            bulk_g2s(s_bm, a.bm_in + boff, static_cast<uint32_t>(nb * 4), &s_bar);
+            bulk_g2s(s_bt, a.bt_in + boff, static_cast<uint32_t>(nb * 4), &s_bar);
+        }
+    } else {
+        stage_words(reinterpret_cast<uint32_t*>(s_bm), reinterpret_cast<const uint32_t*>(a.bm_in + boff), nb, tid);
+        stage_words(reinterpret_cast<uint32_t*>(s_bt), reinterpret_cast<const uint32_t*>(a.bt_in + boff), nb, tid);
+    }
+    __syncthreads();  // the grid slice and any word-staged brackets
+    if (bbulk) mbar_wait(&s_bar, 0);
+    // work item: (sample, four consecutive outputs), rows in ascending order
+    const int ng = outp >> 2;
+    float* part = a.partial + static_cast<size_t>(blockIdx.x) * B * out;
+    for (int q = tid; q < B * ng; q += kNarrowT) {
+        const int sm = q / ng, j4 = (q - sm * ng) * 4;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int r = 0; r < nr; ++r) {
+            const int m = s_bm[r * B + sm];
+            const float t = s_bt[r * B + sm];
+            const float4 c0 = *reinterpret_cast<const float4*>(s_grid + (static_cast<size_t>(r) * G + m) * outp + j4);
+            const float4 c1 = *reinterpret_cast<const float4*>(s_grid + (static_cast<size_t>(r) * G + m + 1) * outp + j4);
+            acc[0] += fmaf(t, c1.x - c0.x, c0.x);
+            acc[1] += fmaf(t, c1.y - c0.y, c0.y);
+            acc[2] += fmaf(t, c1.z - c0.z, c0.z);
+            acc[3] += fmaf(t, c1.w - c0.w, c0.w);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (j4 + u < out) part[static_cast<size_t>(sm) * out + j4 + u] = acc[u];
+    }
+}
+
 template <typename K, typename... Args>
 void launch_pdl(K kernel, dim3 grid, dim3 block, size_t smem, bool pdl, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -2246,12 +2347,14 @@ bool dense_narrow_ok(const DevLayer& L) {
     // one input row of the grid plus the brackets of 512 samples must fit the
     // staging; int8 layers (records decoded in the kernel) with 16-byte rows
     const bool fmt_ok = (L.fmt == FMT_DENSE && !L.wt) || (L.fmt == FMT_I8_R32 && L.G <= 16 && narrow_i8_on());
-    return fmt_ok && L.out <= 32 && L.G >= 2 && static_cast<size_t>(L.out) * L.G * 4 + 16 + 512 * 8 <= 100 * 1024;
+    return fmt_ok && L.out <= 32 && L.G >= 2 && static_cast<size_t>(L.out + 3) * L.G * 4 + 16 + 512 * 8 <= 100 * 1024;
 }
 
 size_t dense_narrow_smem(const DevLayer& L, int B, int rows) {
     const size_t nb = (static_cast<size_t>(rows) * B + 3) & ~static_cast<size_t>(3);
-    return ((static_cast<size_t>(rows) * L.out * L.G * 4 + 15) & ~static_cast<size_t>(15)) + nb * 8;
+    const size_t outp = L.fmt == FMT_DENSE ? static_cast<size_t>(L.out)
+                                           : (static_cast<size_t>(L.out) + 3) & ~static_cast<size_t>(3);
+    return ((static_cast<size_t>(rows) * outp * L.G * 4 + 15) & ~static_cast<size_t>(15)) + nb * 8;
 }
 
 LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms) {
@@ -2278,7 +2381,9 @@ LaunchCfg dense_narrow_cfg(const DevLayer& L, int B, int num_sms) {
 int launch_dense_narrow(const FwdArgs& a0, const LaunchCfg& c, bool pdl, cudaStream_t s) {
     FwdArgs a = a0;
     a.rows_per_cta = c.ichunk;
-    void (*k)(FwdArgs) = a.L.fmt == FMT_DENSE ? k_dense_narrow<FMT_DENSE> : k_dense_narrow<FMT_I8_R32>;
+    // dense: natural [i][out][G] slice bulk-copied (cfg4's tail measured faster
+    // that way); int8: knot-major decoded slice, four outputs per 16-byte load
+    void (*k)(FwdArgs) = a.L.fmt == FMT_DENSE ? k_dense_narrow<FMT_DENSE> : k_narrow_knot<FMT_I8_R32>;
     ensure_smem(k, c.smem);
     launch_pdl(k, dim3(c.nsplit), dim3(kNarrowT), c.smem, pdl, s, a);
     // int8 partials exclude the edges' biases: their per-output sums are added

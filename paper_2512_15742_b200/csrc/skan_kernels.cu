@@ -1310,9 +1310,13 @@ LaunchCfg choose_cfg(const DevLayer& L, int B, bool exact, int num_sms, bool all
     }();
     // (up to batch 512: above it the staged brackets leave few rows per CTA and
     // the split partials grow with the batch; the generic kernels take over)
-    // (int8 layers only up to batch 16: from there the one-tile GEMM and its
-    // 88-plane reduction beat the narrow kernel's 148 planes; batch 256 98 vs 107 us)
-    if (B >= g_gemm_min_batch && B <= (L.fmt == FMT_DENSE ? 512 : 16) && dense_narrow_ok(L))
+    // (int8 layers up to batch 128: at 256 the one-tile GEMM and its 88-plane
+    // reduction beat the narrow kernel's 148 planes, 98 vs 101 us)
+    static const int i8_maxb = [] {
+        const char* e = std::getenv("SKAN_NARROW_I8_MAXB");  // experiment: largest batch for narrow int8 layers
+        return e ? std::atoi(e) : 128;
+    }();
+    if (B >= g_gemm_min_batch && B <= (L.fmt == FMT_DENSE ? 512 : i8_maxb) && dense_narrow_ok(L))
         return dense_narrow_cfg(L, B, sms);
     if (B >= g_gemm_min_batch && L.out >= gemm_min_out && gemm_supported(L)) return gemm_cfg(L, B, sms);  // tensor cores
     const bool i8 = L.fmt == FMT_I8_R32 || L.fmt == FMT_I8_WIDE;
